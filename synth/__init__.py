@@ -1,0 +1,101 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NO arithmetic of the method (no mesh, no FE, no solver): it
+only produces the *inputs* of the gravimetry problem -- cell-wise density
+anomalies delta_rho (kg/m^3, x-fastest, one value per hexahedral cell) and
+Robin-parameter candidates -- from a seed and a configuration name.
+
+Recipes:
+  * ``ball``       -- C1/C2/C4: 1000 kg/m^3 inside |x_c - (L/2)| < 0.25 L (cell
+                      centres), else 0.
+  * ``chicxulub``  -- C3/C5: layered crater-like field on the paper's
+                      250 x 250 x 15 km box ("buried under
+                      1 km of carbonate sediments", "about 200 km in rim
+                      diameter"); piecewise constant per cell, sampled at cell
+                      centres (SURVEY 8(d) field list).
+  * ``random``     -- i.i.d. N(0, 1000^2) per cell from numpy PCG64(seed):
+                      stresses every row class for parity tests.
+  * ``alpha_candidates`` -- C4: alpha_b = alpha0 * exp(0.5 z_b), z ~ N(0,1),
+                      PCG64(2112).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+PAPER_BOX_M = (250.0e3, 250.0e3, 15.0e3)  # PAPER.md:156 "250 x 250 x 15", read as km
+
+
+def cell_centres(nx: int, ny: int, nz: int, lx: float, ly: float, lz: float):
+    """Cell-centre coordinates, each returned as an (nz, ny, nx) array (x fastest when raveled)."""
+    xc = (np.arange(nx) + 0.5) * (lx / nx)
+    yc = (np.arange(ny) + 0.5) * (ly / ny)
+    zc = (np.arange(nz) + 0.5) * (lz / nz)
+    Z, Y, X = np.meshgrid(zc, yc, xc, indexing="ij")
+    return X, Y, Z
+
+
+def ball(nx, ny, nz, lx=1.0, ly=1.0, lz=1.0, amplitude=1000.0, radius_frac=0.25):
+    X, Y, Z = cell_centres(nx, ny, nz, lx, ly, lz)
+    r2 = ((X - lx / 2) / lx) ** 2 + ((Y - ly / 2) / ly) ** 2 + ((Z - lz / 2) / lz) ** 2
+    d = np.where(r2 < radius_frac**2, amplitude, 0.0)
+    return np.ascontiguousarray(d.ravel(), dtype=np.float64)
+
+
+def chicxulub(nx, ny, nz, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2]):
+    """Layered, crater-like anomaly (kg/m^3). Depth d = lz - z (z up), crater centre at the box centre.
+
+    Layers: -300 for d < 1 km (carbonate cover), -100 for 1-4 km.
+    Crater (1 <= d < 6 km): -250 for r < 0.4R, -120 for 0.4R..0.8R, +80 for 0.8R..R.
+    Central uplift: +150 for r < 0.2R and 6 <= d < 12 km.  R = 100 km.  Else 0.
+    Where rules overlap, the later rule in this list wins (crater overrides the
+    1-4 km layer inside r < R).
+    """
+    X, Y, Z = cell_centres(nx, ny, nz, lx, ly, lz)
+    R = 100.0e3 * (lx / PAPER_BOX_M[0])
+    km = 1.0e3 * (lz / PAPER_BOX_M[2])
+    d = lz - Z
+    r = np.sqrt((X - lx / 2) ** 2 + (Y - ly / 2) ** 2)
+    out = np.zeros_like(X)
+    out = np.where(d < 1 * km, -300.0, out)
+    out = np.where((d >= 1 * km) & (d < 4 * km), -100.0, out)
+    crater = (d >= 1 * km) & (d < 6 * km)
+    out = np.where(crater & (r < 0.4 * R), -250.0, out)
+    out = np.where(crater & (r >= 0.4 * R) & (r < 0.8 * R), -120.0, out)
+    out = np.where(crater & (r >= 0.8 * R) & (r < R), 80.0, out)
+    out = np.where((r < 0.2 * R) & (d >= 6 * km) & (d < 12 * km), 150.0, out)
+    return np.ascontiguousarray(out.ravel(), dtype=np.float64)
+
+
+def random_field(nx, ny, nz, seed=0, scale=1000.0):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.normal(0.0, scale, size=nx * ny * nz).astype(np.float64)
+
+
+def alpha_candidates(alpha0: float, B: int = 64, seed: int = 2112):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return alpha0 * np.exp(0.5 * rng.standard_normal(B))
+
+
+# Named workloads of BASELINE.json configs (C1..C5).  Values are
+# inputs only: mesh extents, order, subdomain count, the density recipe and the
+# frozen Robin alpha (per interface side, both sides equal).
+CONFIGS = {
+    "C1": dict(nx=8, ny=8, nz=8, lx=1.0, ly=1.0, lz=1.0, order=1, nsub=2, field="ball", alpha=20.0),
+    "C2": dict(nx=32, ny=32, nz=32, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=2, field="ball", alpha=56.0),
+    "C3": dict(nx=64, ny=64, nz=64, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
+               order=2, nsub=8, field="chicxulub", alpha=None),
+    "C5": dict(nx=192, ny=192, nz=192, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
+               order=2, nsub=8, field="chicxulub", alpha=None),
+}
+
+
+def density(cfg: dict, seed: int = 0):
+    f = cfg["field"]
+    args = (cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"])
+    if f == "ball":
+        return ball(*args)
+    if f == "chicxulub":
+        return chicxulub(*args)
+    if f == "random":
+        return random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=seed)
+    raise ValueError(f"unknown field recipe {f!r}")

@@ -1,0 +1,424 @@
+"""Pins of the CPU oracle against values the paper / mathematics fix (no GPU, no CUDA path).
+
+Each test names the passage or closed form it checks.  A plausible mistake in
+the oracle (dropped term, wrong sign/index, transposed operand) fails at least
+one of these.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from oracle import fe, linalg, mesh, quadrature, schwarz
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "pins.json")))
+
+
+def const_f_density(box, f=1.0):
+    return np.full(box.nx * box.ny * box.nz, f / (4 * np.pi * fe.G_NEWTON))
+
+
+# ---------------------------------------------------------------- paper constants
+def test_paper_constants():
+    assert fe.G_NEWTON == GOLD["G"]["value"]
+
+
+# ---------------------------------------------------------------- partition
+@pytest.mark.parametrize("case", GOLD["partition"])
+def test_partition_examples(case):
+    c = mesh.partition_x(case["nx"], case["nsub"])
+    assert list(np.diff(c)) == case["widths"]
+
+
+def test_partition_errors():
+    with pytest.raises(ValueError):
+        mesh.partition_x(4, 5)
+    with pytest.raises(ValueError):
+        mesh.partition_x(4, 0)
+
+
+# ---------------------------------------------------------------- CSR / PCG
+def test_csr_examples():
+    ex = GOLD["csr_examples"]
+    e = np.array(ex["two_by_two"]["entries"])
+    A = linalg.csr_from_triplets(2, 2, e[:, 0], e[:, 1], e[:, 2])
+    assert list(A.indptr) == ex["two_by_two"]["row_offsets"]
+    e = np.array(ex["dups"]["entries"])
+    A = linalg.csr_from_triplets(1, 1, e[:, 0], e[:, 1], e[:, 2])
+    assert A.nnz == 1 and A.data[0] == ex["dups"]["value"]
+    A = linalg.csr_from_triplets(3, 3, [], [], [])
+    assert list(A.indptr) == ex["empty3"]["row_offsets"]
+    # explicit zeros are kept
+    A = linalg.csr_from_triplets(2, 2, [0, 0], [1, 1], [1.0, -1.0])
+    assert A.nnz == 1 and A.data[0] == 0.0
+
+
+def test_csr_order_independent_and_dense_oracle():
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        n = int(rng.integers(1, 40))
+        m = int(rng.integers(0, 3 * n))
+        r, c = rng.integers(0, n, m), rng.integers(0, n, m)
+        v = rng.integers(-5, 6, m).astype(float)  # integers: sums exact in any order
+        A = linalg.csr_from_triplets(n, n, r, c, v)
+        perm = rng.permutation(m)
+        B = linalg.csr_from_triplets(n, n, r[perm], c[perm], v[perm])
+        assert np.array_equal(A.indptr, B.indptr) and np.array_equal(A.indices, B.indices)
+        assert np.array_equal(A.data, B.data)
+        D = np.zeros((n, n))
+        np.add.at(D, (r, c), v)
+        x = rng.standard_normal(n)
+        assert np.allclose(A @ x, D @ x, rtol=1e-13, atol=1e-12)
+
+
+def test_pcg_special_cases():
+    import scipy.sparse as sp
+
+    I3 = sp.identity(3, format="csr")
+    res = linalg.pcg(I3, np.array([1.0, 2, 3]))
+    assert res.iterations == 1 and np.allclose(res.x, [1, 2, 3])
+    res = linalg.pcg(I3, np.zeros(3))
+    assert res.iterations == 0 and not np.any(res.x)
+    with pytest.raises(linalg.PrecondError):
+        linalg.pcg(sp.csr_matrix(np.diag([1.0, 0.0])), np.ones(2))
+
+
+def test_pcg_anorm_monotone_and_direct():
+    # 1-D 3-point Laplacian, manufactured x*
+    import scipy.sparse as sp
+
+    n = 50
+    A = sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1], format="csr")
+    xs = np.sin(np.linspace(0, 3, n))
+    b = A @ xs
+    errs = []
+    for k in range(1, 60):
+        r = linalg.pcg(A, b, tol=1e-300, maxit=k)
+        e = r.x - xs
+        errs.append(e @ (A @ e))
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-12) + 1e-28 for i in range(len(errs) - 1))
+    assert np.allclose(linalg.pcg(A, b, tol=1e-12).x, xs, atol=1e-8)
+
+
+# ---------------------------------------------------------------- element level
+def _random_quadratic(rng):
+    c = rng.standard_normal(10)  # 1, x, y, z, x^2, y^2, z^2, xy, yz, xz
+
+    def q(x, y, z):
+        return c[0] + c[1] * x + c[2] * y + c[3] * z + c[4] * x * x + c[5] * y * y + c[6] * z * z + c[7] * x * y + c[8] * y * z + c[9] * x * z
+
+    def gq(x, y, z):
+        return np.stack([c[1] + 2 * c[4] * x + c[7] * y + c[9] * z,
+                         c[2] + 2 * c[5] * y + c[7] * x + c[8] * z,
+                         c[3] + 2 * c[6] * z + c[8] * y + c[9] * x], axis=-1)
+
+    return q, gq
+
+
+@pytest.mark.parametrize("h", [(1.0, 1.0, 1.0), (1.0, 0.8, 0.3)])
+def test_p2_element_energy_matches_exact_integral(h):
+    """v^T K_e v = int_T |grad q|^2 for v = P2 interpolant of a random quadratic q.
+
+    The right side uses q's own gradient and an independent high-order rule,
+    so it pins every entry of the symmetric K_e (P2 interpolation is exact on P2).
+    """
+    rng = np.random.default_rng(1)
+    bary, w = quadrature.tet_rule(5)
+    for perm in mesh.PERMS:
+        V = mesh.kuhn_tet_vertices(perm).astype(float) * np.array(h)
+        Ke = fe.p2_stiffness(V)
+        _, vol = fe.tet_geometry(V)
+        nodes = np.concatenate([V, [(V[a] + V[b]) / 2 for a, b in mesh.P2_EDGES]])
+        for _ in range(5):
+            q, gq = _random_quadratic(rng)
+            v = q(nodes[:, 0], nodes[:, 1], nodes[:, 2])
+            X = bary @ V
+            g = gq(X[:, 0], X[:, 1], X[:, 2])
+            exact = vol * np.sum(w * np.sum(g * g, axis=1))
+            assert abs(v @ Ke @ v - exact) <= 1e-12 * max(1.0, abs(exact))
+        assert np.array_equal(Ke, Ke.T)
+        assert np.allclose(Ke.sum(axis=1), 0, atol=1e-13)
+
+
+def test_p1_element_energy():
+    rng = np.random.default_rng(2)
+    for perm in mesh.PERMS:
+        V = mesh.kuhn_tet_vertices(perm).astype(float) * np.array([0.5, 0.7, 0.2])
+        Ke = fe.p1_stiffness(V)
+        _, vol = fe.tet_geometry(V)
+        a = rng.standard_normal(4)
+        v = a[0] + V @ a[1:]
+        assert abs(v @ Ke @ v - vol * a[1:] @ a[1:]) <= 1e-13
+
+
+def test_load_weights_exact():
+    """int_T phi_i against an independent quadrature (P2: vertex -|T|/20, edge |T|/5)."""
+    bary, w = quadrature.tet_rule(4)
+    for order in (1, 2):
+        phi = fe.basis_values(order, bary)
+        assert np.allclose(phi.T @ w, fe.load_weights(order, 1.0), atol=1e-14)
+
+
+def test_tri_mass_tables():
+    """Closed-form triangle mass tables vs independent quadrature of basis products; 1^T M 1 = area."""
+    bary, w = quadrature.tri_rule(6)
+    # P2 triangle basis in the table order (v0, v1, v2, e01, e12, e02)
+    L = bary
+    p2 = np.stack([L[:, 0] * (2 * L[:, 0] - 1), L[:, 1] * (2 * L[:, 1] - 1), L[:, 2] * (2 * L[:, 2] - 1),
+                   4 * L[:, 0] * L[:, 1], 4 * L[:, 1] * L[:, 2], 4 * L[:, 0] * L[:, 2]], axis=1)
+    assert np.allclose(fe.tri_mass(2, 1.0), (p2 * w[:, None]).T @ p2, atol=1e-14)
+    assert np.allclose(fe.tri_mass(1, 1.0), (L * w[:, None]).T @ L, atol=1e-14)
+    for order in (1, 2):
+        assert abs(fe.tri_mass(order, 0.37).sum() - 0.37) < 1e-14
+
+
+# ---------------------------------------------------------------- assembly level
+def test_p1_is_h_times_7point():
+    """On cubic cells the P1-Kuhn stiffness is h x the 7-point stencil (SURVEY 8(c) pins)."""
+    n, h = 5, 0.2
+    box = mesh.Box(n, n, n, 1.0, 1.0, 1.0, 1)
+    K = fe.assemble_stiffness(box, mesh.slabs(box, 1)[0]).toarray()
+    N = n - 1
+    ref = np.zeros_like(K)
+    for k in range(N):
+        for j in range(N):
+            for i in range(N):
+                r = i + N * (j + N * k)
+                ref[r, r] = 6 * h
+                for d, s in ((1, 1), (N, 1), (N * N, 1)):
+                    pass
+                if i > 0: ref[r, r - 1] = -h
+                if i < N - 1: ref[r, r + 1] = -h
+                if j > 0: ref[r, r - N] = -h
+                if j < N - 1: ref[r, r + N] = -h
+                if k > 0: ref[r, r - N * N] = -h
+                if k < N - 1: ref[r, r + N * N] = -h
+    assert np.allclose(K, ref, atol=1e-15)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_assembly_invariants(order):
+    """Unconstrained K 1 = 0 (no Dirichlet elimination), K = K^T bitwise, diag > 0, sum b = f V."""
+    box = mesh.Box(3, 4, 2, 1.0, 1.3, 0.4, order)
+    # unconstrained: a 'slab' whose local_index accepts every lattice point
+    Nx, Ny, Nz = box.lattice
+
+    class All(mesh.Slab):
+        @property
+        def n_local(self):
+            return Nx * Ny * Nz
+
+        def local_index(self, I, J, K):
+            return np.asarray(I) + Nx * (np.asarray(J) + Ny * np.asarray(K))
+
+    al = All(box, 0, 0, box.nx)
+    K = fe.assemble_stiffness(box, al)
+    assert np.abs(K @ np.ones(K.shape[0])).max() < 1e-14
+    b = fe.assemble_load(box, al, const_f_density(box, 2.0))
+    assert abs(b.sum() - 2.0 * 1.0 * 1.3 * 0.4) < 1e-13
+    full = mesh.slabs(box, 1)[0]
+    Kf = fe.assemble_stiffness(box, full)
+    assert (Kf != Kf.T).nnz == 0
+    assert np.all(Kf.diagonal() > 0)
+
+
+def test_structural_zeros_kept():
+    """P1 Kuhn interior rows: 15 structural nnz, 7 numeric nonzeros on cubic cells."""
+    box = mesh.Box(4, 4, 4, 1, 1, 1, 1)
+    K = fe.assemble_stiffness(box, mesh.slabs(box, 1)[0])
+    centre = box.n_free // 2
+    row = K.getrow(centre)
+    assert row.nnz == 15 and np.count_nonzero(row.data) == 7
+
+
+def test_p2_row_class_counts():
+    """P2 interior structural nnz per lattice parity class: 65 / 27 / 19 / 27."""
+    box = mesh.Box(4, 4, 4, 1, 1, 1, 2)
+    K = fe.assemble_stiffness(box, mesh.slabs(box, 1)[0])
+    sl = mesh.slabs(box, 1)[0]
+    for (I, J, Kk), want in (((4, 4, 4), 65), ((3, 4, 4), 27), ((3, 3, 4), 19), ((3, 3, 3), 27)):
+        r = int(sl.local_index(I, J, Kk))
+        assert K.indptr[r + 1] - K.indptr[r] == want
+
+
+def test_tiny_problems():
+    g = GOLD["p1_tiny"]
+    box = mesh.Box(2, 2, 2, 1, 1, 1, 1)
+    full = mesh.slabs(box, 1)[0]
+    K = fe.assemble_stiffness(box, full).toarray()
+    b = fe.assemble_load(box, full, const_f_density(box))
+    assert K.shape == (1, 1) and abs(K[0, 0] - g["K"]) < 1e-15 and abs(b[0] - g["b"]) < 1e-15
+    assert abs(b[0] / K[0, 0] - g["u"]) < 1e-16
+    g = GOLD["p2_tiny"]
+    box = mesh.Box(2, 2, 2, 1, 1, 1, 2)
+    full = mesh.slabs(box, 1)[0]
+    K = fe.assemble_stiffness(box, full).toarray()
+    b = fe.assemble_load(box, full, const_f_density(box))
+    u = np.linalg.solve(K, b)
+    assert K.shape[0] == g["n_free"] and abs(b.sum() - g["sum_b"]) < 1e-14
+    assert abs(u[13] - g["u_centre"]) < 1e-14
+
+
+def test_interface_mass_quadratic_form():
+    """v^T M_Gamma v = int_Gamma v_h^2 for random nodal values v (independent route: quadrature of the
+    FE function over every plane triangle); M symmetric bitwise; row sums of the P1 table = area/3."""
+    rng = np.random.default_rng(7)
+    bary, w = quadrature.tri_rule(6)
+    for order in (1, 2):
+        box = mesh.Box(2, 3, 4, 1.0, 0.6, 0.9, order)
+        M = fe.interface_mass(box)
+        assert (M != M.T).nnz == 0
+        _, Ny, Nz = box.lattice
+        nJ = Ny - 2
+        v = rng.standard_normal(M.shape[0])
+        hy, hz = box.h[1], box.h[2]
+
+        def val(Jp, Kp):
+            free = (Jp >= 1) & (Jp <= Ny - 2) & (Kp >= 1) & (Kp <= Nz - 2)
+            return np.where(free, v[np.clip((Jp - 1) + nJ * (Kp - 1), 0, v.size - 1)], 0.0)
+
+        total = 0.0
+        L = bary
+        if order == 1:
+            phi = L
+        else:
+            phi = np.stack([L[:, 0] * (2 * L[:, 0] - 1), L[:, 1] * (2 * L[:, 1] - 1), L[:, 2] * (2 * L[:, 2] - 1),
+                            4 * L[:, 0] * L[:, 1], 4 * L[:, 1] * L[:, 2], 4 * L[:, 0] * L[:, 2]], axis=1)
+        for ck in range(box.nz):
+            for cj in range(box.ny):
+                for tri in (np.array([[0, 0], [1, 0], [1, 1]]), np.array([[0, 0], [0, 1], [1, 1]])):
+                    pts = tri if order == 1 else np.concatenate([2 * tri, [tri[0] + tri[1], tri[1] + tri[2], tri[0] + tri[2]]])
+                    nv = val(order * cj + pts[:, 0], order * ck + pts[:, 1])
+                    total += 0.5 * hy * hz * np.sum(w * (phi @ nv) ** 2)
+        assert abs(v @ (M @ v) - total) <= 1e-13 * abs(total)
+    assert np.allclose(fe.tri_mass(1, 3.0).sum(axis=1), 1.0)
+    for order in (1, 2):
+        assert abs(fe.tri_mass(order, 0.37).sum() - 0.37) < 1e-15
+
+
+@pytest.mark.parametrize("n,err", list(zip(GOLD["manufactured_p2_l2"]["n"][:2], GOLD["manufactured_p2_l2"]["err"][:2])))
+def test_manufactured_p2(n, err):
+    """P2 L2 error and order 3 for u = sin sin sin (BASELINE north_star 'optimal L2 order')."""
+    q = quadrature.tet_rule(5)
+    ue = lambda x, y, z: np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
+    f = lambda x, y, z: 3 * np.pi**2 * ue(x, y, z)
+    box = mesh.Box(n, n, n, 1, 1, 1, 2)
+    full = mesh.slabs(box, 1)[0]
+    K = fe.assemble_stiffness(box, full)
+    b = fe.assemble_load_function(box, full, f, q)
+    u = spla.spsolve(K.tocsc(), b)
+    e = fe.l2_error(box, u, ue, q)
+    assert abs(e - err) <= GOLD["manufactured_p2_l2"]["rel_tol"] * err
+
+
+def test_manufactured_orders():
+    q = quadrature.tet_rule(5)
+    ue = lambda x, y, z: np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
+    f = lambda x, y, z: 3 * np.pi**2 * ue(x, y, z)
+    errs = {}
+    for order, ns in ((2, (3, 6)), (1, (4, 8, 16))):
+        for n in ns:
+            box = mesh.Box(n, n, n, 1, 1, 1, order)
+            full = mesh.slabs(box, 1)[0]
+            u = spla.spsolve(fe.assemble_stiffness(box, full).tocsc(), fe.assemble_load_function(box, full, f, q))
+            errs[(order, n)] = fe.l2_error(box, u, ue, q)
+    p2 = np.log2(errs[(2, 3)] / errs[(2, 6)])
+    p1 = np.log2(errs[(1, 8)] / errs[(1, 16)])
+    assert 2.85 < p2 < 3.3, p2
+    assert 1.85 < p1 < 2.1, p1
+
+
+# ---------------------------------------------------------------- Schwarz level
+def _prob(n=6, order=2, nsub=2, field="ball", lz=1.0):
+    box = mesh.Box(n, n, n, 1.0, 1.0, lz, order)
+    d = synth.ball(n, n, n, 1.0, 1.0, lz) if field == "ball" else synth.random_field(n, n, n, seed=3)
+    return schwarz.build_problem(box, nsub, drho=d)
+
+
+@pytest.mark.parametrize("order,nsub", [(1, 2), (2, 2), (2, 3), (1, 4)])
+def test_schwarz_equals_monolithic(order, nsub):
+    """Converged Schwarz = monolithic FE solution (~1e-11 at tol 1e-10)."""
+    prob = _prob(6, order, nsub)
+    A = schwarz.robin_operators(prob, [15.0] * (nsub - 1), [15.0] * (nsub - 1))
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-10, tol_inner=1e-12)
+    assert rep.converged
+    us = schwarz.monolithic(prob)
+    assert np.linalg.norm(rep.ut - us) / np.linalg.norm(us) < 1e-8
+    # h really is the relative residual of the returned glued vector
+    assert abs(schwarz.global_residual(prob, rep.ut) - rep.h[-1]) < 1e-15
+
+
+def test_exact_dtn_two_iterations():
+    """with the exact (DtN) symbol, two subdomains converge in two iterations."""
+    prob = _prob(4, 2, 2)
+    A = schwarz.exact_dtn_operators(prob)
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-300, max_outer=3, direct=True, diverge_window=0)
+    assert rep.h[0] > 1e-2
+    assert rep.h[1] < GOLD["exact_dtn"]["h2_max"]
+    us = schwarz.monolithic(prob)
+    assert np.linalg.norm(rep.ut - us) / np.linalg.norm(us) < 1e-12
+
+
+def test_exact_dtn_unsymmetric_recombination():
+    """A^(1) != A^(2): exact DtN on one side only still gives the fixed point (checks the
+    general (A_s + A_t) u - lambda recombination)."""
+    prob = _prob(4, 2, 2)
+    A = schwarz.exact_dtn_operators(prob)
+    A[(0, 1)] = 5.0 * prob.MG
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-12, max_outer=200, direct=True)
+    assert rep.converged
+    us = schwarz.monolithic(prob)
+    assert np.linalg.norm(rep.ut - us) / np.linalg.norm(us) < 1e-10
+
+
+def test_zero_density_one_iteration():
+    """delta rho = 0 -> Phi = 0 at iteration 1."""
+    box = mesh.Box(4, 4, 4, 1, 1, 1, 2)
+    prob = schwarz.build_problem(box, 2, drho=np.zeros(64))
+    A = schwarz.robin_operators(prob, [10.0], [10.0])
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-8)
+    assert rep.outer_iters == 1 and rep.h[0] == 0.0 and not np.any(rep.ut)
+
+
+def test_left_right_relabelling_symmetry():
+    """Relabelling slabs right-to-left gives the same history.
+
+    The Kuhn mesh is invariant under the central inversion x -> L - x (all three axes:
+    the (0,0,0)-(1,1,1) diagonal maps to itself), which swaps the two slabs and the
+    two interface sides; so an inversion-symmetric density with (alpha_1, alpha_2)
+    swapped must reproduce the history."""
+    n = 6
+    box = mesh.Box(n, n, n, 1, 1, 1, 2)
+    d = synth.random_field(n, n, n, seed=5).reshape(n, n, n)
+    d_sym = d + d[::-1, ::-1, ::-1]
+    prob = schwarz.build_problem(box, 2, drho=d_sym.ravel())
+    A = schwarz.robin_operators(prob, [12.0], [30.0])
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-9, tol_inner=1e-12)
+    A2 = schwarz.robin_operators(prob, [30.0], [12.0])
+    rep2 = schwarz.schwarz(prob, A2, tol_outer=1e-9, tol_inner=1e-12)
+    assert rep.outer_iters == rep2.outer_iters
+    assert np.allclose(rep.h, rep2.h, rtol=1e-6, atol=1e-13)
+
+
+def test_warm_start_same_history_fewer_inner():
+    """Warm start changes inner counts, not the outer history beyond eps-level."""
+    prob = _prob(6, 2, 2)
+    A = schwarz.robin_operators(prob, [20.0], [20.0])
+    w = schwarz.schwarz(prob, A, tol_outer=1e-8)
+    c = schwarz.schwarz(prob, A, tol_outer=1e-8, warm_start=False)
+    assert sum(map(sum, w.inner)) < sum(map(sum, c.inner))
+    assert abs(w.outer_iters - c.outer_iters) <= 1
+
+
+def test_divergence_flag():
+    """Negative Robin alpha makes the iteration blow up: DIVERGED after 10 growing steps."""
+    prob = _prob(4, 1, 2)
+    A = schwarz.robin_operators(prob, [-0.3], [-0.3])
+    try:
+        rep = schwarz.schwarz(prob, A, tol_outer=1e-8, max_outer=300)
+    except linalg.PrecondError:
+        return  # negative alpha may already break the preconditioner: also an error path
+    assert rep.diverged or not rep.converged

@@ -1,0 +1,199 @@
+/*
+ * osm.h -- C ABI of the B200-native optimized-Schwarz gravimetry solver.
+ *
+ * Method: arXiv 2112.03851 ("stochastic-based optimized Schwarz method for the
+ * gravimetry equation on GPU clusters").  The library solves
+ *     -Delta Phi = 4 pi G drho  in a box,  Phi = 0 on the boundary
+ * ("Delta Phi = -4 pi G delta rho", "homogeneous
+ * Dirichlet condition") with P1/P2 tetrahedral finite elements on a Kuhn box
+ * mesh ("high order finite element"; reading SURVEY.md 8(c) Q1/Q2),
+ * partitioned into x-slabs ("partionned in the x-direction"), by the
+ * non-overlapping Schwarz iteration with Robin transmission,
+ * each subdomain solved by Jacobi-preconditioned CG to eps = 1e-10
+ * (PAPER.md:165).  Everything on the solve path runs in this library's CUDA
+ * kernels (sm_100a); there is no CPU fallback.
+ *
+ * Conventions shared by every call:
+ *  - All floating point is IEEE fp64.  All arrays are plain C arrays.
+ *  - "host" pointers are ordinary CPU memory; "device" pointers are CUDA device
+ *    memory on the context's device.  The caller owns every buffer it passes;
+ *    the library copies what it needs before returning (inputs) or writes into
+ *    the caller's buffer (outputs).  The context owns all of its device memory
+ *    and its NCCL communicator.
+ *  - Lattice ordering: points of the (o*nx+1) x (o*ny+1) x (o*nz+1) lattice
+ *    (o = element order) have id = I + Nx*(J + Ny*K), x fastest.  Cells are
+ *    ordered the same way (ci + nx*(cj + ny*ck)).
+ *  - Subdomain s is the x-slab of cells [c_s, c_{s+1}) (widths differ by <= 1,
+ *    remainder to the left).  Its local unknowns are its free
+ *    lattice points (interface planes duplicated in both neighbours), numbered
+ *    x fastest over the slab ("contract order").  Interface i lies between
+ *    slabs i and i+1; side 0 = the left slab, side 1 = the right slab.
+ *  - Every call returns an osm_status.  On failure the call has no partial
+ *    effect on results previously read back, and osm_last_error() returns a
+ *    thread-local message.  No C++ exception crosses this boundary.
+ *  - Output-size queries: where noted, passing NULL for the output buffer
+ *    writes the required element count to the size argument and returns OSM_OK.
+ *  - Collective calls (marked [collective]) must be made by every rank of the
+ *    communicator in the same order.
+ */
+#ifndef OSM_H_
+#define OSM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSM_ABI_VERSION 1
+
+typedef enum osm_status {
+  OSM_OK = 0,
+  OSM_ERR_INVALID_ARG = 1,    /* a count/extent <= 0, size mismatch, bad index, NULL where required */
+  OSM_ERR_GRID_TOO_SMALL = 2, /* fewer than 3 lattice points per axis: no interior */
+  OSM_ERR_ILL_POSED = 3,      /* Robin alpha < 0, or alpha = 0 on both sides of an interface */
+  OSM_ERR_PRECOND = 4,        /* a diagonal entry <= 0: Jacobi preconditioner undefined */
+  OSM_NOT_CONVERGED = 5,      /* max_outer reached; report and iterate stay readable */
+  OSM_ERR_DIVERGED = 6,       /* h(n) grew for diverge_window consecutive iterations */
+  OSM_ERR_CUDA = 7,           /* a CUDA runtime error (message has the CUDA error string) */
+  OSM_ERR_NCCL = 8,           /* an NCCL error */
+  OSM_ERR_STATE = 9           /* call out of order (e.g. solve before assemble) */
+} osm_status;
+
+typedef struct osm_ctx osm_ctx;
+
+/* Box mesh: nx*ny*nz hexahedral cells on [0,lx]x[0,ly]x[0,lz] (metres), each
+ * split into the 6 Kuhn tetrahedra sharing the (0,0,0)-(1,1,1) diagonal;
+ * order = 1 (P1) or 2 (P2) Lagrange elements. */
+typedef struct osm_mesh_desc {
+  int64_t nx, ny, nz;
+  double lx, ly, lz;
+  int order;
+} osm_mesh_desc;
+
+/* Distribution: this process is `rank` of `nranks` (one process per GPU),
+ * driving CUDA device `device`.  nccl_uid: 128-byte ncclUniqueId made by
+ * osm_nccl_unique_id() on rank 0 and broadcast by the caller (e.g. with
+ * torch.distributed); NULL when nranks == 1.  stream: a cudaStream_t to run
+ * on, or NULL for a library-owned stream. */
+typedef struct osm_dist_desc {
+  int rank, nranks, device;
+  const void* nccl_uid;
+  void* stream;
+} osm_dist_desc;
+
+/* Solve options.  tol_outer: stop when h(n) = ||f - K u~||_2/||f||_2 <= tol_outer
+ * (PAPER.md:215 uses 1e-6; BASELINE metric 1e-8).  tol_inner: PCG stops when the
+ * recursive residual ||r||_2 <= tol_inner * ||rhs||_2 (1e-10).
+ * warm_start: start each inner solve from the previous outer iterate.
+ * diverge_window: DIVERGED after this many consecutive growing h(n) (0 = off). */
+typedef struct osm_solve_opts {
+  double tol_outer;
+  int max_outer;
+  double tol_inner;
+  int max_inner;
+  int warm_start;
+  int diverge_window;
+} osm_solve_opts;
+
+typedef struct osm_report {
+  int outer_iters;     /* N: outer iterations performed */
+  int converged;       /* 1 if h(N) <= tol_outer */
+  double h_final;      /* h(N) */
+  double seconds;      /* wall time of the solve (host clock around the device work) */
+  int64_t inner_total; /* sum over outer iterations and subdomains of PCG iterations (all ranks) */
+  int inner_maxed;     /* number of (n, s) inner solves that hit max_inner */
+} osm_report;
+
+/* Per-kernel device timing (CUDA events on the library stream), accumulated
+ * while osm_set_kernel_timing(ctx, 1) is on. */
+typedef struct osm_kernel_time {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+} osm_kernel_time;
+
+int osm_abi_version(void);
+const char* osm_last_error(void);
+
+/* Writes a fresh 128-byte ncclUniqueId to uid128 (host).  Call on rank 0 only. */
+osm_status osm_nccl_unique_id(void* uid128);
+
+/* [collective] Creates a context.  INVALID_ARG if a count/extent <= 0, order not
+ * in {1,2}, rank/nranks inconsistent; GRID_TOO_SMALL if o*n+1 < 3 on an axis. */
+osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_ctx** out);
+void osm_destroy(osm_ctx* ctx);
+
+/* Splits the box into nsub x-slabs; slab s goes to rank floor(s*nranks/nsub).
+ * INVALID_ARG if nsub < 1, nsub > nx, or nsub % nranks != 0.  Invalidates assembly. */
+osm_status osm_decompose(osm_ctx* ctx, int nsub);
+
+/* Robin parameters (OO0: A^(s) = alpha_s, weak form alpha_s M_Gamma; PAPER.md:77-79,
+ * SURVEY Q8).  alpha_left[i] is used by the slab left of interface i (side 0),
+ * alpha_right[i] by the slab right of it (side 1); nsub-1 host values each.
+ * ILL_POSED if any alpha < 0 or both alphas of an interface are 0.  May be
+ * called between solves; the Robin term is re-applied on the device. */
+osm_status osm_set_robin(osm_ctx* ctx, const double* alpha_left, const double* alpha_right);
+
+/* [device work] Builds, per local subdomain: the Neumann stiffness K_s^N
+ * (structural pattern, Dirichlet rows/cols removed), the interface mass
+ * M_Gamma, interface maps, the SELL-32 hot-path copy and the Jacobi diagonal.
+ * PRECOND if a diagonal <= 0. */
+osm_status osm_assemble(osm_ctx* ctx);
+
+/* Density anomaly drho[nx*ny*nz] (kg/m^3, cell-wise constant, x fastest; host
+ * pointer) and the gravity constant G (6.672e-11).  The load is
+ * f = 4 pi G drho, integrated exactly per tet.  Requires osm_assemble. */
+osm_status osm_upload_density(osm_ctx* ctx, const double* drho, double G);
+/* Same, from a device pointer (nx*ny*nz doubles on the context's device). */
+osm_status osm_upload_density_device(osm_ctx* ctx, const double* drho_dev, double G);
+
+/* [collective] Runs the Schwarz iteration from u^0 = lambda^0 = 0.  Returns OK,
+ * NOT_CONVERGED (max_outer reached), DIVERGED, or an error.  report may be NULL. */
+osm_status osm_solve(osm_ctx* ctx, const osm_solve_opts* opts, osm_report* report);
+
+/* h(1..N) of the last solve (every rank holds it).  h == NULL: *n = N. */
+osm_status osm_get_history(osm_ctx* ctx, double* h, int cap, int* n);
+/* PCG iterations its[n*nsub + s] of the last solve, for the subdomains of this
+ * rank (-1 for subdomains of other ranks).  its == NULL: *n_outer = N. */
+osm_status osm_get_inner_iters(osm_ctx* ctx, int32_t* its, int cap_outer, int* n_outer);
+
+/* [collective] Phi of the last solve on the full lattice (Nx*Ny*Nz host doubles,
+ * x fastest, Dirichlet points 0, interface points averaged between the two slab
+ * copies).  Gathered to rank 0; other ranks may pass NULL.  phi == NULL on
+ * rank 0: *n = Nx*Ny*Nz. */
+osm_status osm_get_solution(osm_ctx* ctx, double* phi, int64_t* n);
+/* Local subdomain iterate u_s (contract order, host).  u == NULL: *n = n_s. */
+osm_status osm_get_local_solution(osm_ctx* ctx, int s, double* u, int64_t* n);
+/* lambda_{s,Gamma} of interface `iface`, side 0/1 (owner rank only; host). */
+osm_status osm_get_trace(osm_ctx* ctx, int iface, int side, double* lam, int64_t* n);
+
+/* Parity dumps (owner rank only, host buffers).  K_s^N in canonical CSR
+ * (columns ascending, explicit structural zeros kept, SURVEY
+ * Q17), contract order.  rowptr == NULL: writes *nrows and *nnz only. */
+osm_status osm_get_csr(osm_ctx* ctx, int s, int64_t* rowptr, int32_t* col, double* val, int64_t* nrows,
+                       int64_t* nnz);
+/* Interface map of interface `iface`, side 0 (left slab) or 1 (right slab): the
+ * local contract index of each plane point, plane points ordered j fastest then
+ * k (interior points only).  idx == NULL: *n = n_Gamma. */
+osm_status osm_get_interface_map(osm_ctx* ctx, int iface, int side, int32_t* idx, int64_t* n);
+/* The interface mass matrix M_Gamma (n_Gamma rows, plane-point order, CSR). */
+osm_status osm_get_interface_mass(osm_ctx* ctx, int64_t* rowptr, int32_t* col, double* val, int64_t* nrows,
+                                  int64_t* nnz);
+
+/* Device-timing instrumentation: events around every launch of the named
+ * kernels, on the library stream.  Reset on enable. */
+osm_status osm_set_kernel_timing(osm_ctx* ctx, int enable);
+osm_status osm_get_kernel_timing(osm_ctx* ctx, osm_kernel_time* out, int cap, int* n);
+
+/* Algorithmic HBM bytes of one PCG iteration of local subdomain-set work,
+ * summed over this rank's subdomains weighted by their inner iteration counts in
+ * the last solve: out[0] = SpMV kernel bytes, out[1] =
+ * update kernel bytes, out[2] = direction kernel bytes, out[3] = SELL padding
+ * entries, out[4] = structural nnz (local), out[5] = local rows. */
+osm_status osm_get_traffic_model(osm_ctx* ctx, double* out, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OSM_H_ */

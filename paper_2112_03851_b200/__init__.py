@@ -1,0 +1,275 @@
+"""B200-native optimized-Schwarz gravimetry solver (arXiv 2112.03851) -- thin Python binding.
+
+Argument marshalling only: every step of the solve runs in libosm's CUDA
+kernels (``csrc/``), behind the C ABI declared in ``include/osm.h``.  The names
+mirror the C entry points.  There is no CPU fallback: if ``libosm.so`` is
+missing or cannot load, importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libosm.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libosm.so not built ({LIB_PATH}); run `python -m paper_2112_03851_b200.build`")
+_lib = C.CDLL(LIB_PATH)
+
+OSM_OK, OSM_ERR_INVALID_ARG, OSM_ERR_GRID_TOO_SMALL, OSM_ERR_ILL_POSED, OSM_ERR_PRECOND = 0, 1, 2, 3, 4
+OSM_NOT_CONVERGED, OSM_ERR_DIVERGED, OSM_ERR_CUDA, OSM_ERR_NCCL, OSM_ERR_STATE = 5, 6, 7, 8, 9
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "GRID_TOO_SMALL", 3: "ILL_POSED", 4: "PRECOND", 5: "NOT_CONVERGED",
+                6: "DIVERGED", 7: "CUDA", 8: "NCCL", 9: "STATE"}
+
+# symbols declared in include/osm.h (checked by tests/test_abi.py)
+ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_create", "osm_destroy",
+               "osm_decompose", "osm_set_robin", "osm_assemble", "osm_upload_density", "osm_upload_density_device",
+               "osm_solve", "osm_get_history", "osm_get_inner_iters", "osm_get_solution", "osm_get_local_solution",
+               "osm_get_trace", "osm_get_csr", "osm_get_interface_map", "osm_get_interface_mass",
+               "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model"]
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64), ("lx", C.c_double), ("ly", C.c_double),
+                ("lz", C.c_double), ("order", C.c_int)]
+
+
+class DistDesc(C.Structure):
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("device", C.c_int), ("nccl_uid", C.c_void_p),
+                ("stream", C.c_void_p)]
+
+
+class SolveOpts(C.Structure):
+    _fields_ = [("tol_outer", C.c_double), ("max_outer", C.c_int), ("tol_inner", C.c_double), ("max_inner", C.c_int),
+                ("warm_start", C.c_int), ("diverge_window", C.c_int)]
+
+
+class Report(C.Structure):
+    _fields_ = [("outer_iters", C.c_int), ("converged", C.c_int), ("h_final", C.c_double), ("seconds", C.c_double),
+                ("inner_total", C.c_int64), ("inner_maxed", C.c_int)]
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double)]
+
+
+_P = C.c_void_p
+_pd = C.POINTER(C.c_double)
+_pi32 = C.POINTER(C.c_int32)
+_pi64 = C.POINTER(C.c_int64)
+_pint = C.POINTER(C.c_int)
+_sigs = {
+    "osm_abi_version": (C.c_int, []),
+    "osm_last_error": (C.c_char_p, []),
+    "osm_nccl_unique_id": (C.c_int, [_P]),
+    "osm_create": (C.c_int, [C.POINTER(MeshDesc), C.POINTER(DistDesc), C.POINTER(_P)]),
+    "osm_destroy": (None, [_P]),
+    "osm_decompose": (C.c_int, [_P, C.c_int]),
+    "osm_set_robin": (C.c_int, [_P, _pd, _pd]),
+    "osm_assemble": (C.c_int, [_P]),
+    "osm_upload_density": (C.c_int, [_P, _pd, C.c_double]),
+    "osm_upload_density_device": (C.c_int, [_P, C.c_void_p, C.c_double]),
+    "osm_solve": (C.c_int, [_P, C.POINTER(SolveOpts), C.POINTER(Report)]),
+    "osm_get_history": (C.c_int, [_P, _pd, C.c_int, _pint]),
+    "osm_get_inner_iters": (C.c_int, [_P, _pi32, C.c_int, _pint]),
+    "osm_get_solution": (C.c_int, [_P, _pd, _pi64]),
+    "osm_get_local_solution": (C.c_int, [_P, C.c_int, _pd, _pi64]),
+    "osm_get_trace": (C.c_int, [_P, C.c_int, C.c_int, _pd, _pi64]),
+    "osm_get_csr": (C.c_int, [_P, C.c_int, _pi64, _pi32, _pd, _pi64, _pi64]),
+    "osm_get_interface_map": (C.c_int, [_P, C.c_int, C.c_int, _pi32, _pi64]),
+    "osm_get_interface_mass": (C.c_int, [_P, _pi64, _pi32, _pd, _pi64, _pi64]),
+    "osm_set_kernel_timing": (C.c_int, [_P, C.c_int]),
+    "osm_get_kernel_timing": (C.c_int, [_P, C.POINTER(KernelTime), C.c_int, _pint]),
+    "osm_get_traffic_model": (C.c_int, [_P, _pd, C.c_int]),
+}
+for _name, (_res, _args) in _sigs.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class OsmError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st, ok=(OSM_OK,)):
+    if st not in ok:
+        raise OsmError(st, _lib.osm_last_error().decode())
+    return st
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def abi_version():
+    return _lib.osm_abi_version()
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.osm_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Osm:
+    """One optimized-Schwarz context (one per process / GPU).  Mirrors include/osm.h."""
+
+    def __init__(self, nx, ny, nz, lx, ly, lz, order, rank=0, nranks=1, device=0, nccl_uid: bytes | None = None,
+                 stream: int | None = None):
+        self.mesh = MeshDesc(nx, ny, nz, lx, ly, lz, order)
+        self._uid = C.create_string_buffer(nccl_uid, 128) if nccl_uid else None
+        dist = DistDesc(rank, nranks, device, C.cast(self._uid, C.c_void_p) if self._uid else None, stream)
+        h = _P()
+        _check(_lib.osm_create(C.byref(self.mesh), C.byref(dist), C.byref(h)))
+        self._h = h
+        self.order = order
+        self.nsub = 0
+        self.lattice = (order * nx + 1, order * ny + 1, order * nz + 1)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.osm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- setup
+    def decompose(self, nsub):
+        _check(_lib.osm_decompose(self._h, int(nsub)))
+        self.nsub = int(nsub)
+
+    def set_robin(self, alpha_left, alpha_right):
+        al = np.ascontiguousarray(alpha_left, dtype=np.float64)
+        ar = np.ascontiguousarray(alpha_right, dtype=np.float64)
+        if al.size != max(self.nsub - 1, 0) or ar.size != al.size:
+            raise ValueError("need nsub-1 alphas per side")
+        _check(_lib.osm_set_robin(self._h, _ptr(al, C.c_double), _ptr(ar, C.c_double)))
+
+    def assemble(self):
+        _check(_lib.osm_assemble(self._h))
+
+    def upload_density(self, drho, G=6.672e-11):
+        d = np.ascontiguousarray(drho, dtype=np.float64)
+        if d.size != self.mesh.nx * self.mesh.ny * self.mesh.nz:
+            raise ValueError("density must have nx*ny*nz cells")
+        _check(_lib.osm_upload_density(self._h, _ptr(d, C.c_double), float(G)))
+
+    def upload_density_device(self, ptr: int, G=6.672e-11):
+        _check(_lib.osm_upload_density_device(self._h, C.c_void_p(ptr), float(G)))
+
+    # -- solve
+    def solve(self, tol_outer=1e-8, max_outer=500, tol_inner=1e-10, max_inner=20000, warm_start=True,
+              diverge_window=10):
+        opts = SolveOpts(tol_outer, max_outer, tol_inner, max_inner, int(warm_start), diverge_window)
+        rep = Report()
+        st = _check(_lib.osm_solve(self._h, C.byref(opts), C.byref(rep)),
+                    ok=(OSM_OK, OSM_NOT_CONVERGED, OSM_ERR_DIVERGED))
+        return st, rep
+
+    # -- readback
+    def history(self):
+        n = C.c_int()
+        _check(_lib.osm_get_history(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(_lib.osm_get_history(self._h, _ptr(out, C.c_double), n.value, C.byref(n)))
+        return out
+
+    def inner_iters(self):
+        n = C.c_int()
+        _check(_lib.osm_get_inner_iters(self._h, None, 0, C.byref(n)))
+        out = np.zeros((n.value, self.nsub), dtype=np.int32)
+        _check(_lib.osm_get_inner_iters(self._h, _ptr(out, C.c_int32), n.value, C.byref(n)))
+        return out
+
+    def solution(self):
+        n = C.c_int64(0)
+        _check(_lib.osm_get_solution(self._h, None, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(_lib.osm_get_solution(self._h, _ptr(out, C.c_double), C.byref(n)))
+        return out
+
+    def local_solution(self, s):
+        n = C.c_int64(0)
+        _check(_lib.osm_get_local_solution(self._h, s, None, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(_lib.osm_get_local_solution(self._h, s, _ptr(out, C.c_double), C.byref(n)))
+        return out
+
+    def trace(self, iface, side):
+        n = C.c_int64(0)
+        _check(_lib.osm_get_trace(self._h, iface, side, None, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(_lib.osm_get_trace(self._h, iface, side, _ptr(out, C.c_double), C.byref(n)))
+        return out
+
+    def csr(self, s):
+        nr, nz = C.c_int64(0), C.c_int64(0)
+        _check(_lib.osm_get_csr(self._h, s, None, None, None, C.byref(nr), C.byref(nz)))
+        rp = np.zeros(nr.value + 1, dtype=np.int64)
+        col = np.zeros(nz.value, dtype=np.int32)
+        val = np.zeros(nz.value)
+        _check(_lib.osm_get_csr(self._h, s, _ptr(rp, C.c_int64), _ptr(col, C.c_int32), _ptr(val, C.c_double),
+                                C.byref(nr), C.byref(nz)))
+        return rp, col, val
+
+    def interface_map(self, iface, side):
+        n = C.c_int64(0)
+        _check(_lib.osm_get_interface_map(self._h, iface, side, None, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int32)
+        _check(_lib.osm_get_interface_map(self._h, iface, side, _ptr(out, C.c_int32), C.byref(n)))
+        return out
+
+    def interface_mass(self):
+        nr, nz = C.c_int64(0), C.c_int64(0)
+        _check(_lib.osm_get_interface_mass(self._h, None, None, None, C.byref(nr), C.byref(nz)))
+        rp = np.zeros(nr.value + 1, dtype=np.int64)
+        col = np.zeros(nz.value, dtype=np.int32)
+        val = np.zeros(nz.value)
+        _check(_lib.osm_get_interface_mass(self._h, _ptr(rp, C.c_int64), _ptr(col, C.c_int32), _ptr(val, C.c_double),
+                                           C.byref(nr), C.byref(nz)))
+        return rp, col, val
+
+    # -- instrumentation
+    def set_kernel_timing(self, enable: bool):
+        _check(_lib.osm_set_kernel_timing(self._h, int(enable)))
+
+    def kernel_timing(self):
+        n = C.c_int()
+        _check(_lib.osm_get_kernel_timing(self._h, None, 0, C.byref(n)))
+        arr = (KernelTime * n.value)()
+        _check(_lib.osm_get_kernel_timing(self._h, arr, n.value, C.byref(n)))
+        return {a.name.decode(): (a.launches, a.total_ms) for a in arr}
+
+    def traffic_model(self):
+        out = np.zeros(6)
+        _check(_lib.osm_get_traffic_model(self._h, _ptr(out, C.c_double), 6))
+        return dict(spmv_bytes=out[0], update_bytes=out[1], dir_bytes=out[2], pad_entries=out[3], nnz=out[4],
+                    rows=out[5])
+
+
+def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None) -> Osm:
+    """Create, decompose, assemble, set alpha (both sides) and upload the density of a config dict."""
+    o = Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], rank, nranks, device,
+            nccl_uid)
+    o.decompose(cfg["nsub"])
+    if cfg["nsub"] > 1:
+        a = cfg.get("alpha") if alpha is None else alpha
+        al = np.full(cfg["nsub"] - 1, a) if np.isscalar(a) else np.asarray(a[0])
+        ar = np.full(cfg["nsub"] - 1, a) if np.isscalar(a) else np.asarray(a[1])
+        o.set_robin(al, ar)
+    o.assemble()
+    o.upload_density(drho)
+    return o

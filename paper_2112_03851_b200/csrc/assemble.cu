@@ -1,0 +1,274 @@
+// Device-side setup of libosm: structural CSR assembly of K_s^N from the
+// per-parity-class stencil tables, the load vector of 4 pi G drho, the SELL-32
+// hot-path copy, and the Robin fold list.  (8(c) steps 2-8.)
+//
+// One thread per row: a row (lattice point P of class r = P mod o) visits the
+// table's column offsets dQ in column order and, for each, sums the element
+// contributions K_e[t][a][b] of the tets (cell P div o + dc, tet t) that lie in
+// the slab, in element order (cell id ascending, then tet), exactly as a
+// sequential element-by-element assembly would.  A column exists when the
+// point P + dQ is a free point of the slab and at least one of its tets lies in
+// the slab -- the structural pattern, independent of rounding.
+#include "ctx.h"
+
+namespace osm {
+
+namespace {
+
+__device__ __forceinline__ void lattice_of(const SlabGeom& g, int64_t i, int64_t& I, int64_t& J, int64_t& K) {
+  I = g.I_lo + i % g.nI;
+  const int64_t t = i / g.nI;
+  J = 1 + t % g.nJ;
+  K = 1 + t / g.nJ;
+}
+
+__device__ __forceinline__ bool cell_in_slab(const SlabGeom& g, int64_t cx, int64_t cy, int64_t cz) {
+  return cx >= g.c0 && cx < g.c1 && cy >= 0 && cy < g.ny && cz >= 0 && cz < g.nz;
+}
+
+__device__ __forceinline__ int64_t local_of(const SlabGeom& g, int64_t I, int64_t J, int64_t K) {
+  if (I < g.I_lo || I > g.I_hi || J < 1 || J > g.Ny - 2 || K < 1 || K > g.Nz - 2) return -1;
+  return (I - g.I_lo) + g.nI * ((J - 1) + g.nJ * (K - 1));
+}
+
+template <bool kFill>
+__global__ void k_assemble(SlabGeom g, int64_t n, StencilDev T, int32_t* __restrict__ rowlen,
+                           const int64_t* __restrict__ rowptr, int32_t* __restrict__ col, double* __restrict__ val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t I, J, K;
+  lattice_of(g, i, I, J, K);
+  const int o = g.order;
+  const int rx = (int)(I % o), ry = (int)(J % o), rz = (int)(K % o);
+  const int cls = rx + o * (ry + o * rz);
+  const int64_t qx = (I - rx) / o, qy = (J - ry) / o, qz = (K - rz) / o;
+  int cnt = 0;
+  int64_t pos = kFill ? rowptr[i] : 0;
+  for (int e = T.col_begin[cls]; e < T.col_begin[cls + 1]; ++e) {
+    const StencilCol sc = T.cols[e];
+    const int64_t jc = local_of(g, I + sc.dx, J + sc.dy, K + sc.dz);
+    if (jc < 0) continue;
+    double s = 0.0;
+    bool any = false;
+    for (int k = sc.c0; k < sc.c1; ++k) {
+      const StiffContrib cb = T.contribs[k];
+      if (cell_in_slab(g, qx + cb.dcx, qy + cb.dcy, qz + cb.dcz)) {
+        s = __dadd_rn(s, cb.val);
+        any = true;
+      }
+    }
+    if (!any) continue;
+    if (kFill) {
+      col[pos] = (int32_t)jc;
+      val[pos] = s;
+      ++pos;
+    } else {
+      ++cnt;
+    }
+  }
+  if (!kFill) rowlen[i] = cnt;
+}
+
+// Load b_i = sum_T f_T int_T phi_i with f_T = 4 pi G drho_cell, written in
+// internal order.
+__global__ void k_load(SlabGeom g, int64_t n, StencilDev T, const double* __restrict__ drho, double fourpiG,
+                       const int32_t* __restrict__ iperm, int64_t row0, double* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t I, J, K;
+  lattice_of(g, i, I, J, K);
+  const int o = g.order;
+  const int rx = (int)(I % o), ry = (int)(J % o), rz = (int)(K % o);
+  const int cls = rx + o * (ry + o * rz);
+  const int64_t qx = (I - rx) / o, qy = (J - ry) / o, qz = (K - rz) / o;
+  double s = 0.0;
+  for (int e = T.load_begin[cls]; e < T.load_begin[cls + 1]; ++e) {
+    const LoadContrib L = T.loads[e];
+    const int64_t cx = qx + L.dcx, cy = qy + L.dcy, cz = qz + L.dcz;
+    if (!cell_in_slab(g, cx, cy, cz)) continue;
+    const double f = __dmul_rn(fourpiG, drho[cx + g.nx * (cy + g.ny * cz)]);
+    s = __dadd_rn(s, __dmul_rn(f, L.w));
+  }
+  b[row0 + iperm[i]] = s;
+}
+
+// Copy contract CSR rows into SELL-32 slices (column-major), remapping columns to
+// internal concatenated indices; padding = (val 0, col = own row).  Also dinv from K^N.
+__global__ void k_sell_build(int64_t npad, int64_t row0, int64_t slice0, const int32_t* __restrict__ perm,
+                             const int32_t* __restrict__ iperm, const int64_t* __restrict__ rowptr,
+                             const int32_t* __restrict__ ccol, const double* __restrict__ cval,
+                             const int64_t* __restrict__ soff, const int32_t* __restrict__ swidth,
+                             double* __restrict__ sval, int32_t* __restrict__ scol, double* __restrict__ dinv,
+                             int32_t* __restrict__ flags) {
+  const int64_t ri = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ri >= npad) return;
+  const int64_t slice = slice0 + ri / kWarp;
+  const int lane = (int)(ri % kWarp);
+  const int64_t off = soff[slice] + lane;
+  const int w = swidth[slice];
+  const int64_t grow = row0 + ri;
+  const int c = perm[ri];
+  if (c < 0) {
+    for (int k = 0; k < w; ++k) {
+      scol[off + (int64_t)kWarp * k] = (int32_t)grow;
+      sval[off + (int64_t)kWarp * k] = 0.0;
+    }
+    dinv[grow] = 0.0;
+    return;
+  }
+  const int64_t beg = rowptr[c];
+  const int len = (int)(rowptr[c + 1] - beg);
+  double d = 0.0;
+  bool found = false;
+  for (int k = 0; k < w; ++k) {
+    if (k < len) {
+      const int cc = ccol[beg + k];
+      scol[off + (int64_t)kWarp * k] = (int32_t)(row0 + iperm[cc]);
+      sval[off + (int64_t)kWarp * k] = cval[beg + k];
+      if (cc == c) {
+        d = cval[beg + k];
+        found = true;
+      }
+    } else {
+      scol[off + (int64_t)kWarp * k] = (int32_t)grow;
+      sval[off + (int64_t)kWarp * k] = 0.0;
+    }
+  }
+  if (!found || !(d > 0.0)) atomicOr(flags, 1);
+  dinv[grow] = (found && d > 0.0) ? 1.0 / d : 0.0;
+}
+
+// For each M_Gamma entry (g, g2) of a side: the SELL position of K_s entry (map[g], map[g2]).
+__global__ void k_fold_build(int64_t nG, const int32_t* __restrict__ map_c, const int32_t* __restrict__ mrow,
+                             const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                             const int64_t* __restrict__ rowptr, const int32_t* __restrict__ ccol,
+                             const double* __restrict__ cval, const int32_t* __restrict__ iperm, int64_t row0,
+                             int64_t slice0, const int64_t* __restrict__ soff, int64_t fold0, int side_idx,
+                             int64_t* __restrict__ fold_pos, double* __restrict__ fold_m, double* __restrict__ fold_kn,
+                             int32_t* __restrict__ fold_diag_row, int32_t* __restrict__ fold_side,
+                             int32_t* __restrict__ flags) {
+  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gi >= nG) return;
+  const int c = map_c[gi];
+  const int ri = iperm[c];
+  const int64_t slice = slice0 + ri / kWarp;
+  const int lane = ri % kWarp;
+  const int64_t beg = rowptr[c], end = rowptr[c + 1];
+  for (int j = mrow[gi]; j < mrow[gi + 1]; ++j) {
+    const int cc = map_c[mcol[j]];
+    int64_t lo = beg, hi = end;  // binary search in the sorted row
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (ccol[mid] < cc) lo = mid + 1; else hi = mid;
+    }
+    const int64_t e = fold0 + j;
+    if (lo >= end || ccol[lo] != cc) {
+      atomicOr(flags, 2);
+      fold_pos[e] = -1;
+      continue;
+    }
+    fold_pos[e] = soff[slice] + (int64_t)kWarp * (lo - beg) + lane;
+    fold_m[e] = mval[j];
+    fold_kn[e] = cval[lo];
+    fold_diag_row[e] = (cc == c) ? (int32_t)(row0 + ri) : -1;
+    fold_side[e] = side_idx;
+  }
+}
+
+// K_s = K_s^N + alpha_s M_Gamma on the interface rows, and the
+// Jacobi diagonal of the Robin-augmented rows.
+__global__ void k_fold_apply(int64_t nfold, const double* __restrict__ alpha_side, const int64_t* __restrict__ pos,
+                             const double* __restrict__ m, const double* __restrict__ kn,
+                             const int32_t* __restrict__ diag_row, const int32_t* __restrict__ side,
+                             double* __restrict__ sval, double* __restrict__ dinv, int32_t* __restrict__ flags) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nfold) return;
+  const int64_t p = pos[e];
+  if (p < 0) return;
+  const double v = __dadd_rn(kn[e], __dmul_rn(alpha_side[side[e]], m[e]));
+  sval[p] = v;
+  const int dr = diag_row[e];
+  if (dr >= 0) {
+    if (!(v > 0.0)) atomicOr(flags, 1);
+    dinv[dr] = v > 0.0 ? 1.0 / v : 0.0;
+  }
+}
+
+__global__ void k_scatter_phi(SlabGeom g, int64_t npad, int64_t row0, const int32_t* __restrict__ perm,
+                              const double* __restrict__ ut, int only_owned, double* __restrict__ phi) {
+  const int64_t ri = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ri >= npad) return;
+  const int c = perm[ri];
+  if (c < 0) return;
+  int64_t I, J, K;
+  lattice_of(g, c, I, J, K);
+  if (only_owned && g.c0 > 0 && I == g.order * g.c0) return;  // left plane belongs to the left slab
+  const int64_t Nx = g.order * g.nx + 1;
+  phi[I + Nx * (J + g.Ny * K)] = ut[row0 + ri];
+}
+
+__global__ void k_gather_local(int64_t npad, int64_t row0, const int32_t* __restrict__ perm,
+                               const double* __restrict__ x, double* __restrict__ out) {
+  const int64_t ri = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ri >= npad) return;
+  const int c = perm[ri];
+  if (c >= 0) out[c] = x[row0 + ri];
+}
+
+inline int grid_for(int64_t n, int threads = 256) { return (int)ceil_div(n > 0 ? n : 1, threads); }
+
+StencilDev tables_of(const Ctx& c) {
+  return StencilDev{c.d_col_begin, c.d_cols, c.d_contribs, c.d_load_begin, c.d_loads, c.mesh.order};
+}
+
+}  // namespace
+
+void launch_count(const Ctx& c, const Sub& s, int32_t* rowlen) {
+  k_assemble<false><<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), rowlen, nullptr, nullptr, nullptr);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_fill(const Ctx& c, const Sub& s) {
+  k_assemble<true><<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), nullptr, s.rowptr, s.col, s.val);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_sell_build(const Ctx& c, const Sub& s, const int32_t*) {
+  k_sell_build<<<grid_for(s.npad), 256, 0, c.stream>>>(s.npad, s.row0, s.slice0, s.perm, s.iperm, s.rowptr, s.col,
+                                                      s.val, c.sell_soff, c.sell_swidth, c.sell_val, c.sell_col,
+                                                      c.dinv, c.d_flags);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s) {
+  const int side_idx = (int)(&sd - c.sides.data());
+  k_fold_build<<<grid_for(c.nG), 256, 0, c.stream>>>(c.nG, sd.map_c, c.d_mrow, c.d_mcol, c.d_mval, s.rowptr, s.col,
+                                                    s.val, s.iperm, s.row0, s.slice0, c.sell_soff, sd.fold0, side_idx,
+                                                    c.fold_pos, c.fold_m, c.fold_kn, c.fold_diag_row, c.fold_side,
+                                                    c.d_flags);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_fold_apply(const Ctx& c, const double* d_alpha_side) {
+  if (c.nfold == 0) return;
+  k_fold_apply<<<grid_for(c.nfold), 256, 0, c.stream>>>(c.nfold, d_alpha_side, c.fold_pos, c.fold_m, c.fold_kn,
+                                                       c.fold_diag_row, c.fold_side, c.sell_val, c.dinv, c.d_flags);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_load(const Ctx& c, const Sub& s, double fourpiG) {
+  k_load<<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), c.drho, fourpiG, s.iperm, s.row0, c.b);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned) {
+  k_scatter_phi<<<grid_for(s.npad), 256, 0, c.stream>>>(s.g, s.npad, s.row0, s.perm, c.ut, only_owned, c.phi);
+  OSM_CHECK_LAUNCH();
+}
+
+void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract) {
+  k_gather_local<<<grid_for(s.npad), 256, 0, c.stream>>>(s.npad, s.row0, s.perm, c.x, out_contract);
+  OSM_CHECK_LAUNCH();
+}
+
+}  // namespace osm

@@ -1,0 +1,229 @@
+// Internal context of libosm: per-GPU subdomain store, interface sides and the
+// launchers of the device kernels (assemble.cu, schwarz_kernels.cu).
+#pragma once
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "lattice.h"
+
+namespace osm {
+
+// Free-point box of one x-slab in lattice coordinates.
+struct SlabGeom {
+  int64_t c0, c1;          // cells [c0, c1) in x
+  int64_t nx, ny, nz;      // global cell counts
+  int64_t Ny, Nz;          // lattice points in y, z
+  int64_t I_lo, I_hi;      // inclusive free I range
+  int64_t nI, nJ, nK;      // free box extents
+  int order;
+};
+
+// Device view of the stencil tables.
+struct StencilDev {
+  const int32_t* col_begin;
+  const StencilCol* cols;
+  const StiffContrib* contribs;
+  const int32_t* load_begin;
+  const LoadContrib* loads;
+  int order;
+};
+
+// SELL-32 matrix over the concatenated internal rows of every local subdomain.
+// Slice k holds internal rows [32k, 32k+32); entry j of its row l sits at
+// soff[k] + 32 j + l (column major); padding entries have val 0, col = own row.
+struct SellDev {
+  const double* val;
+  const int32_t* col;
+  const int64_t* soff;
+  const int32_t* swidth;
+};
+
+// Per-subdomain device scalars of the batched PCG / Schwarz kernels.
+struct SubState {
+  double rho;      // r.z
+  double alpha;    // CG step
+  double beta;     // CG direction factor
+  double bb;       // ||rhs||^2
+  double rr;       // ||r||^2
+  double resid;    // interior part of sum (f - K u~)^2 for this subdomain
+  int64_t blk0;    // first block (256 rows) of the subdomain
+  int32_t nblk;    // number of blocks
+  int32_t active;  // PCG still running
+  int32_t iters;   // PCG iterations of the current inner solve
+  int32_t status;  // 0 running, 1 converged, 2 max_inner, 3 breakdown
+  int32_t zero_rhs;
+  uint32_t cnt;    // last-block counter
+};
+
+// Device view of one interface side (grid.y of the interface kernels).
+struct SideDev {
+  const int32_t* map;  // internal (concatenated) row of each plane point
+  double* lam;         // lambda_{s,Gamma}
+  double* out;         // outbox [g | u | w] (3 nG)
+  const double* in;    // partner outbox (local) or receive buffer (remote) [g | u | w]
+  double* unbr;        // neighbour trace u_t|Gamma (for gluing)
+  double* wif;         // residual (f - K^N u~) at this side's plane rows
+  double alpha_own, alpha_sum;
+  int32_t sub;         // local subdomain index
+  int32_t which;       // 0: this slab is the left slab of the interface (its right plane), 1: right slab
+  int32_t slot0;       // first islot index of the side (= side * nG)
+  int32_t pad;
+};
+
+struct Sub {
+  int s = -1;  // global subdomain id
+  SlabGeom g{};
+  int64_t n = 0;                 // local rows (contract)
+  int64_t row0 = 0, npad = 0;    // internal range in the concatenated vectors
+  int64_t slice0 = 0, nslice = 0;
+  int64_t blk0 = 0, nblk = 0;
+  int64_t nnz = 0;               // structural nnz of K_s^N
+  int64_t sell_entries = 0;      // including padding
+  int64_t* rowptr = nullptr;     // contract CSR of K_s^N (device)
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  int32_t* perm = nullptr;       // internal local -> contract local (device, npad, -1 for pad)
+  int32_t* iperm = nullptr;      // contract local -> internal local (device, n)
+  int side[2] = {-1, -1};        // [0] left plane, [1] right plane (indices into Ctx::sides)
+};
+
+struct Side {
+  int iface = -1, which = 0, sub = -1;
+  bool remote = false;
+  int peer = -1;                  // rank of the neighbour
+  int partner = -1;               // local side index of the neighbour side (local only)
+  int32_t* map_c = nullptr;       // contract local rows (device, nG)
+  int32_t* map_g = nullptr;       // internal concatenated rows (device, nG)
+  double* out = nullptr;          // outbox (device, 3 nG)
+  double* inbuf = nullptr;        // receive buffer (remote only, device, 3 nG)
+  int64_t fold0 = 0;              // first Robin fold entry
+};
+
+struct KernelTimer {
+  std::string name;
+  std::vector<cudaEvent_t> ev;  // start/end pairs
+  int64_t used = 0;
+  double total_ms = 0;
+  int64_t launches = 0;
+};
+
+struct Ctx {
+  // configuration
+  osm_mesh_desc mesh{};
+  int rank = 0, nranks = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  int nsub = 0;
+  std::vector<int64_t> cstart;  // slab cell starts
+  int s_begin = 0, s_end = 0;   // local subdomains [s_begin, s_end)
+  std::vector<double> alpha_left, alpha_right;
+  bool robin_set = false, assembled = false, density_set = false;
+  bool robin_dirty = true;
+  double G = 6.672e-11;
+
+  // stencil tables (device)
+  StencilTables tables;
+  int32_t *d_col_begin = nullptr, *d_load_begin = nullptr;
+  StencilCol* d_cols = nullptr;
+  StiffContrib* d_contribs = nullptr;
+  LoadContrib* d_loads = nullptr;
+
+  // interface mass (host + device), plane-point order
+  int64_t nG = 0;
+  std::vector<int32_t> h_mrow, h_mcol;
+  std::vector<double> h_mval;
+  int32_t *d_mrow = nullptr, *d_mcol = nullptr;
+  double* d_mval = nullptr;
+
+  // subdomains and sides
+  std::vector<Sub> subs;
+  std::vector<Side> sides;
+  int64_t nrows_total = 0, nslices_total = 0, nblk_total = 0, sell_total = 0;
+
+  // SELL matrix (device)
+  double* sell_val = nullptr;
+  int32_t* sell_col = nullptr;
+  int64_t* sell_soff = nullptr;
+  int32_t* sell_swidth = nullptr;
+  int32_t* blk_sub = nullptr;  // block -> local subdomain
+  int32_t* islot = nullptr;    // per internal row: -2 pad, -1 interior, >= 0 interface slot
+
+  // Robin fold list (device): sell position, M value, K^N value, diag row (-1 if off-diagonal)
+  int64_t nfold = 0;
+  int64_t* fold_pos = nullptr;
+  double* fold_m = nullptr;
+  double* fold_kn = nullptr;
+  int32_t* fold_diag_row = nullptr;
+  int32_t* fold_side = nullptr;
+
+  // vectors (device, nrows_total)
+  double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *b = nullptr, *ut = nullptr;
+  double* drho = nullptr;  // cell density (device, nx ny nz)
+  // interface arrays (device, nsides * nG)
+  double *lam_all = nullptr, *unbr_all = nullptr, *wif_all = nullptr;
+  SideDev* d_sides = nullptr;
+  std::vector<SideDev> h_sides;
+  // reductions
+  double* part = nullptr;  // 3 * nblk_total block partials
+  double* side_part = nullptr;  // per side block partials
+  double* side_sum = nullptr;   // per side result
+  uint32_t* side_cnt = nullptr;
+  int64_t side_nblk = 0;
+  SubState* st = nullptr;       // per local subdomain
+  int32_t* d_nactive = nullptr;
+  int32_t* d_flags = nullptr;   // [0] precond failure, [1] fold miss
+  // host staging (pinned)
+  int32_t* h_nactive = nullptr;  // 2 slots
+  SubState* h_st = nullptr;
+  double* h_side_sum = nullptr;
+  cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
+
+  // full-lattice output buffer (device)
+  double* phi = nullptr;
+
+  // last solve results
+  std::vector<double> hist;
+  std::vector<int32_t> inner;  // [outer][nsub]
+  double fnorm2 = 0;
+
+  // instrumentation
+  bool timing = false;
+  std::vector<KernelTimer> timers;
+
+  // traffic model of the last solve
+  double traffic[6] = {0};
+};
+
+// ---- launchers (assemble.cu)
+void launch_count(const Ctx& c, const Sub& s, int32_t* rowlen);
+void launch_fill(const Ctx& c, const Sub& s);
+void launch_sell_build(const Ctx& c, const Sub& s, const int32_t* d_slice_width_local);
+void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s);
+void launch_fold_apply(const Ctx& c, const double* d_alpha_side);
+void launch_load(const Ctx& c, const Sub& s, double fourpiG);
+void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned);
+void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract);
+
+// ---- launchers (schwarz_kernels.cu)
+void launch_warm(Ctx& c, double tol, int warm);
+void launch_zero_if(Ctx& c);
+void launch_cg_spmv(Ctx& c);
+void launch_cg_update(Ctx& c, double tol, int maxit);
+void launch_cg_dir(Ctx& c);
+void launch_trace(Ctx& c);
+void launch_accept(Ctx& c);
+void launch_glue(Ctx& c, int zero);
+void launch_resid(Ctx& c);
+void launch_iface_w(Ctx& c);
+void launch_iface_sum(Ctx& c);
+
+// timing helpers (osm.cu)
+void timer_begin(Ctx& c, int id);
+void timer_end(Ctx& c, int id);
+enum TimerId { T_SPMV = 0, T_UPDATE, T_DIR, T_WARM, T_RESID, T_OUTER_MISC, T_COUNT };
+
+}  // namespace osm

@@ -1,0 +1,983 @@
+// libosm C ABI and host driver of the optimized Schwarz iteration.
+//
+// Host side only orchestrates: every arithmetic step of the solve runs in the
+// kernels of assemble.cu / schwarz_kernels.cu.  Cross-GPU traffic (interface
+// traces, interface-row residuals, per-subdomain residual sums, the solution
+// gather) goes through NCCL over NVLink; subdomains that share a GPU exchange
+// through device memory inside the interface kernels.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+
+namespace osm {
+
+thread_local std::string g_last_error;
+
+#define OSM_NCCL(call)                                                                         \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess) ::osm::fail(OSM_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class T>
+static T* dalloc(int64_t n) {
+  void* p = nullptr;
+  if (n <= 0) n = 1;
+  OSM_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)n));
+  return (T*)p;
+}
+template <class T>
+static void dfree(T*& p) {
+  if (p) cudaFree((void*)p);
+  p = nullptr;
+}
+template <class T>
+static T* dupload(const Ctx& c, const std::vector<T>& h) {
+  T* d = dalloc<T>((int64_t)h.size());
+  if (!h.empty()) OSM_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, c.stream));
+  return d;
+}
+
+// ------------------------------------------------------------------ timers
+void timer_begin(Ctx& c, int id) {
+  if (!c.timing) return;
+  KernelTimer& t = c.timers[id];
+  if ((int64_t)t.ev.size() < 2 * (t.used + 1)) {
+    for (int k = 0; k < 256; ++k) {
+      cudaEvent_t e;
+      OSM_CUDA(cudaEventCreate(&e));
+      t.ev.push_back(e);
+    }
+  }
+  OSM_CUDA(cudaEventRecord(t.ev[2 * t.used], c.stream));
+}
+void timer_end(Ctx& c, int id) {
+  if (!c.timing) return;
+  KernelTimer& t = c.timers[id];
+  OSM_CUDA(cudaEventRecord(t.ev[2 * t.used + 1], c.stream));
+  t.used++;
+}
+static void timers_collect(Ctx& c) {
+  if (!c.timing) return;
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  for (auto& t : c.timers) {
+    for (int64_t i = 0; i < t.used; ++i) {
+      float ms = 0.f;
+      OSM_CUDA(cudaEventElapsedTime(&ms, t.ev[2 * i], t.ev[2 * i + 1]));
+      t.total_ms += ms;
+    }
+    t.launches += t.used;
+    t.used = 0;
+  }
+}
+
+// ------------------------------------------------------------------ teardown
+static void free_assembly(Ctx& c) {
+  for (auto& s : c.subs) {
+    dfree(s.rowptr);
+    dfree(s.col);
+    dfree(s.val);
+    dfree(s.perm);
+    dfree(s.iperm);
+  }
+  c.subs.clear();
+  for (auto& sd : c.sides) {
+    dfree(sd.map_c);
+    dfree(sd.map_g);
+    dfree(sd.out);
+    dfree(sd.inbuf);
+  }
+  c.sides.clear();
+  dfree(c.d_col_begin);
+  dfree(c.d_load_begin);
+  dfree(c.d_cols);
+  dfree(c.d_contribs);
+  dfree(c.d_loads);
+  dfree(c.d_mrow);
+  dfree(c.d_mcol);
+  dfree(c.d_mval);
+  dfree(c.sell_val);
+  dfree(c.sell_col);
+  dfree(c.sell_soff);
+  dfree(c.sell_swidth);
+  dfree(c.blk_sub);
+  dfree(c.islot);
+  dfree(c.fold_pos);
+  dfree(c.fold_m);
+  dfree(c.fold_kn);
+  dfree(c.fold_diag_row);
+  dfree(c.fold_side);
+  dfree(c.x);
+  dfree(c.r);
+  dfree(c.p);
+  dfree(c.q);
+  dfree(c.dinv);
+  dfree(c.b);
+  dfree(c.ut);
+  dfree(c.lam_all);
+  dfree(c.unbr_all);
+  dfree(c.wif_all);
+  dfree(c.d_sides);
+  dfree(c.part);
+  dfree(c.side_part);
+  dfree(c.side_sum);
+  dfree(c.side_cnt);
+  dfree(c.st);
+  dfree(c.phi);
+  c.assembled = false;
+  c.density_set = false;
+}
+
+// ------------------------------------------------------------------ assembly
+static SlabGeom slab_geom(const Ctx& c, int s) {
+  SlabGeom g{};
+  const int o = c.mesh.order;
+  g.c0 = c.cstart[s];
+  g.c1 = c.cstart[s + 1];
+  g.nx = c.mesh.nx;
+  g.ny = c.mesh.ny;
+  g.nz = c.mesh.nz;
+  g.Ny = o * c.mesh.ny + 1;
+  g.Nz = o * c.mesh.nz + 1;
+  const int64_t Nx = o * c.mesh.nx + 1;
+  g.I_lo = std::max<int64_t>(o * g.c0, 1);
+  g.I_hi = std::min<int64_t>(o * g.c1, Nx - 2);
+  g.nI = g.I_hi - g.I_lo + 1;
+  g.nJ = g.Ny - 2;
+  g.nK = g.Nz - 2;
+  g.order = o;
+  return g;
+}
+
+static constexpr int kSigma = 1024;  // SELL sorting window (rows)
+
+static void assemble(Ctx& c) {
+  free_assembly(c);
+  const int o = c.mesh.order;
+  const double h[3] = {c.mesh.lx / c.mesh.nx, c.mesh.ly / c.mesh.ny, c.mesh.lz / c.mesh.nz};
+  c.tables = build_stencil_tables(o, h);
+  c.d_col_begin = dupload(c, c.tables.col_begin);
+  c.d_cols = dupload(c, c.tables.cols);
+  c.d_contribs = dupload(c, c.tables.contribs);
+  c.d_load_begin = dupload(c, c.tables.load_begin);
+  c.d_loads = dupload(c, c.tables.loads);
+  interface_mass(o, c.mesh.ny, c.mesh.nz, h[1], h[2], c.h_mrow, c.h_mcol, c.h_mval);
+  c.nG = (int64_t)c.h_mrow.size() - 1;
+  c.d_mrow = dupload(c, c.h_mrow);
+  c.d_mcol = dupload(c, c.h_mcol);
+  c.d_mval = dupload(c, c.h_mval);
+  if (!c.d_flags) c.d_flags = dalloc<int32_t>(4);
+  OSM_CUDA(cudaMemsetAsync(c.d_flags, 0, 4 * sizeof(int32_t), c.stream));
+
+  // --- per-subdomain structural CSR of K_s^N (contract order) and SELL layout
+  const int nloc = c.s_end - c.s_begin;
+  c.subs.resize(nloc);
+  std::vector<std::vector<int32_t>> h_perm(nloc);
+  std::vector<std::vector<int32_t>> h_iperm(nloc);
+  std::vector<int64_t> h_soff;
+  std::vector<int32_t> h_swidth;
+  int64_t row0 = 0, slice0 = 0, sell_off = 0;
+  for (int ls = 0; ls < nloc; ++ls) {
+    Sub& S = c.subs[ls];
+    S.s = c.s_begin + ls;
+    S.g = slab_geom(c, S.s);
+    S.n = S.g.nI * S.g.nJ * S.g.nK;
+    if (S.n >= (int64_t)INT32_MAX) fail(OSM_ERR_INVALID_ARG, "subdomain too large for int32 local indices");
+    int32_t* d_len = dalloc<int32_t>(S.n);
+    launch_count(c, S, d_len);
+    std::vector<int32_t> len(S.n);
+    OSM_CUDA(cudaMemcpyAsync(len.data(), d_len, sizeof(int32_t) * S.n, cudaMemcpyDeviceToHost, c.stream));
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+    dfree(d_len);
+    std::vector<int64_t> rowptr(S.n + 1, 0);
+    for (int64_t i = 0; i < S.n; ++i) rowptr[i + 1] = rowptr[i] + len[i];
+    S.nnz = rowptr[S.n];
+    S.rowptr = dupload(c, rowptr);
+    S.col = dalloc<int32_t>(S.nnz);
+    S.val = dalloc<double>(S.nnz);
+    launch_fill(c, S);
+
+    // SELL-32-sigma: within windows of kSigma rows, sort rows by length (descending, stable)
+    S.npad = round_up(S.n, kRowsPerBlock);
+    S.row0 = row0;
+    S.slice0 = slice0;
+    S.nslice = S.npad / kWarp;
+    S.blk0 = row0 / kRowsPerBlock;
+    S.nblk = S.npad / kRowsPerBlock;
+    auto& perm = h_perm[ls];
+    auto& iperm = h_iperm[ls];
+    perm.assign(S.npad, -1);
+    iperm.assign(S.n, -1);
+    std::vector<int32_t> idx;
+    for (int64_t w0 = 0; w0 < S.n; w0 += kSigma) {
+      const int64_t w1 = std::min<int64_t>(S.n, w0 + kSigma);
+      idx.resize(w1 - w0);
+      std::iota(idx.begin(), idx.end(), (int32_t)w0);
+      std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+      for (int64_t k = 0; k < w1 - w0; ++k) {
+        perm[w0 + k] = idx[k];
+        iperm[idx[k]] = (int32_t)(w0 + k);
+      }
+    }
+    S.sell_entries = 0;
+    for (int64_t sl = 0; sl < S.nslice; ++sl) {
+      int w = 0;
+      for (int l = 0; l < kWarp; ++l) {
+        const int32_t cr = perm[sl * kWarp + l];
+        if (cr >= 0) w = std::max(w, len[cr]);
+      }
+      h_soff.push_back(sell_off);
+      h_swidth.push_back(w);
+      sell_off += (int64_t)w * kWarp;
+      S.sell_entries += (int64_t)w * kWarp;
+    }
+    S.perm = dupload(c, perm);
+    S.iperm = dupload(c, iperm);
+    row0 += S.npad;
+    slice0 += S.nslice;
+  }
+  c.nrows_total = row0;
+  c.nslices_total = slice0;
+  c.nblk_total = row0 / kRowsPerBlock;
+  c.sell_total = sell_off;
+  if (c.nrows_total >= (int64_t)INT32_MAX) fail(OSM_ERR_INVALID_ARG, "too many rows per GPU for int32 columns");
+  c.sell_soff = dupload(c, h_soff);
+  c.sell_swidth = dupload(c, h_swidth);
+  c.sell_val = dalloc<double>(c.sell_total);
+  c.sell_col = dalloc<int32_t>(c.sell_total);
+  c.x = dalloc<double>(c.nrows_total);
+  c.r = dalloc<double>(c.nrows_total);
+  c.p = dalloc<double>(c.nrows_total);
+  c.q = dalloc<double>(c.nrows_total);
+  c.dinv = dalloc<double>(c.nrows_total);
+  c.b = dalloc<double>(c.nrows_total);
+  c.ut = dalloc<double>(c.nrows_total);
+  for (double* v : {c.x, c.r, c.p, c.q, c.dinv, c.b, c.ut})
+    OSM_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * c.nrows_total, c.stream));
+  for (int ls = 0; ls < nloc; ++ls) launch_sell_build(c, c.subs[ls], nullptr);
+
+  std::vector<int32_t> blk_sub(c.nblk_total);
+  for (int ls = 0; ls < nloc; ++ls)
+    for (int64_t k = 0; k < c.subs[ls].nblk; ++k) blk_sub[c.subs[ls].blk0 + k] = ls;
+  c.blk_sub = dupload(c, blk_sub);
+
+  // --- interface sides
+  const int64_t nG = c.nG;
+  std::vector<int32_t> islot(c.nrows_total, -1);
+  for (int ls = 0; ls < nloc; ++ls) {
+    const Sub& S = c.subs[ls];
+    for (int64_t k = S.n; k < S.npad; ++k) islot[S.row0 + k] = -2;
+  }
+  for (int ls = 0; ls < nloc; ++ls) {
+    Sub& S = c.subs[ls];
+    for (int which_plane = 0; which_plane < 2; ++which_plane) {  // 0: left plane, 1: right plane
+      const bool has = which_plane == 0 ? S.s > 0 : S.s < c.nsub - 1;
+      if (!has) continue;
+      Side sd;
+      sd.sub = ls;
+      sd.iface = which_plane == 0 ? S.s - 1 : S.s;
+      sd.which = which_plane == 0 ? 1 : 0;  // a left plane means this slab is the right slab of the interface
+      const int nbr = which_plane == 0 ? S.s - 1 : S.s + 1;
+      sd.remote = !(nbr >= c.s_begin && nbr < c.s_end);
+      sd.peer = (int)((int64_t)nbr * c.nranks / c.nsub);
+      const int64_t I = which_plane == 0 ? (int64_t)o * S.g.c0 : (int64_t)o * S.g.c1;
+      std::vector<int32_t> mc(nG), mg(nG);
+      const int k = (int)c.sides.size();
+      for (int64_t kk = 0; kk < S.g.nK; ++kk)
+        for (int64_t jj = 0; jj < S.g.nJ; ++jj) {
+          const int64_t gidx = jj + S.g.nJ * kk;
+          const int64_t lc = (I - S.g.I_lo) + S.g.nI * (jj + S.g.nJ * kk);
+          mc[gidx] = (int32_t)lc;
+          mg[gidx] = (int32_t)(S.row0 + h_iperm[ls][lc]);
+          islot[mg[gidx]] = (int32_t)(k * nG + gidx);
+        }
+      sd.map_c = dupload(c, mc);
+      sd.map_g = dupload(c, mg);
+      sd.out = dalloc<double>(3 * nG);
+      OSM_CUDA(cudaMemsetAsync(sd.out, 0, sizeof(double) * 3 * nG, c.stream));
+      if (sd.remote) {
+        sd.inbuf = dalloc<double>(3 * nG);
+        OSM_CUDA(cudaMemsetAsync(sd.inbuf, 0, sizeof(double) * 3 * nG, c.stream));
+      }
+      S.side[which_plane] = k;
+      c.sides.push_back(sd);
+    }
+  }
+  const int nsides = (int)c.sides.size();
+  for (int k = 0; k < nsides; ++k) {
+    Side& sd = c.sides[k];
+    if (sd.remote) continue;
+    for (int j = 0; j < nsides; ++j)
+      if (j != k && c.sides[j].iface == sd.iface) sd.partner = j;
+  }
+  c.islot = dupload(c, islot);
+  c.lam_all = dalloc<double>(nsides * nG);
+  c.unbr_all = dalloc<double>(nsides * nG);
+  c.wif_all = dalloc<double>(nsides * nG);
+  for (double* v : {c.lam_all, c.unbr_all, c.wif_all})
+    OSM_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * std::max<int64_t>(1, nsides * nG), c.stream));
+
+  // --- Robin fold list: one entry per M_Gamma nonzero per side
+  const int64_t mnnz = c.h_mrow.empty() ? 0 : c.h_mrow.back();
+  c.nfold = nsides * mnnz;
+  c.fold_pos = dalloc<int64_t>(c.nfold);
+  c.fold_m = dalloc<double>(c.nfold);
+  c.fold_kn = dalloc<double>(c.nfold);
+  c.fold_diag_row = dalloc<int32_t>(c.nfold);
+  c.fold_side = dalloc<int32_t>(c.nfold);
+  for (int k = 0; k < nsides; ++k) {
+    c.sides[k].fold0 = k * mnnz;
+    launch_fold_build(c, c.sides[k], c.subs[c.sides[k].sub]);
+  }
+
+  // --- reductions and device side table
+  c.part = dalloc<double>(3 * c.nblk_total);
+  c.side_nblk = std::max<int64_t>(1, ceil_div(nG, 256));
+  c.side_part = dalloc<double>(std::max(1, nsides) * c.side_nblk);
+  c.side_sum = dalloc<double>(std::max(1, nsides));
+  c.side_cnt = dalloc<uint32_t>(std::max(1, nsides));
+  OSM_CUDA(cudaMemsetAsync(c.side_cnt, 0, sizeof(uint32_t) * std::max(1, nsides), c.stream));
+  OSM_CUDA(cudaMemsetAsync(c.side_sum, 0, sizeof(double) * std::max(1, nsides), c.stream));
+  c.st = dalloc<SubState>(nloc);
+  std::vector<SubState> hst(nloc);
+  for (int ls = 0; ls < nloc; ++ls) {
+    std::memset(&hst[ls], 0, sizeof(SubState));
+    hst[ls].blk0 = c.subs[ls].blk0;
+    hst[ls].nblk = (int32_t)c.subs[ls].nblk;
+  }
+  OSM_CUDA(cudaMemcpyAsync(c.st, hst.data(), sizeof(SubState) * nloc, cudaMemcpyHostToDevice, c.stream));
+  if (c.h_st) cudaFreeHost(c.h_st);
+  OSM_CUDA(cudaMallocHost((void**)&c.h_st, sizeof(SubState) * std::max(1, nloc)));
+  if (c.h_side_sum) cudaFreeHost(c.h_side_sum);
+  OSM_CUDA(cudaMallocHost((void**)&c.h_side_sum, sizeof(double) * std::max(1, nsides)));
+  c.h_sides.assign(nsides, SideDev{});
+  for (int k = 0; k < nsides; ++k) {
+    const Side& sd = c.sides[k];
+    SideDev& D = c.h_sides[k];
+    D.map = sd.map_g;
+    D.lam = c.lam_all + k * nG;
+    D.out = sd.out;
+    D.in = sd.remote ? sd.inbuf : c.sides[sd.partner].out;
+    D.unbr = c.unbr_all + k * nG;
+    D.wif = c.wif_all + k * nG;
+    D.alpha_own = D.alpha_sum = 0.0;
+    D.sub = sd.sub;
+    D.which = sd.which;
+    D.slot0 = (int32_t)(k * nG);
+  }
+  c.d_sides = dalloc<SideDev>(std::max(1, nsides));
+  if (nsides)
+    OSM_CUDA(cudaMemcpyAsync(c.d_sides, c.h_sides.data(), sizeof(SideDev) * nsides, cudaMemcpyHostToDevice, c.stream));
+
+  int32_t flags[4];
+  OSM_CUDA(cudaMemcpyAsync(flags, c.d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  if (flags[1]) fail(OSM_ERR_INVALID_ARG, "internal: interface mass entry outside the stiffness pattern");
+  if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry in K_s^N");
+  c.assembled = true;
+  c.robin_dirty = true;
+  c.density_set = false;
+}
+
+// Apply alpha to the SELL values of interface rows (K_s = K_s^N + alpha_s M_Gamma).
+static void apply_robin(Ctx& c) {
+  if (!c.robin_dirty) return;
+  const int nsides = (int)c.sides.size();
+  if (nsides == 0) {
+    c.robin_dirty = false;
+    return;
+  }
+  if (!c.robin_set) fail(OSM_ERR_STATE, "osm_set_robin must be called before solving with nsub > 1");
+  std::vector<double> a(nsides);
+  for (int k = 0; k < nsides; ++k) {
+    const Side& sd = c.sides[k];
+    const double al = c.alpha_left[sd.iface], ar = c.alpha_right[sd.iface];
+    a[k] = sd.which == 0 ? al : ar;
+    c.h_sides[k].alpha_own = a[k];
+    c.h_sides[k].alpha_sum = al + ar;
+  }
+  double* d_a = dupload(c, a);
+  OSM_CUDA(cudaMemsetAsync(c.d_flags, 0, 4 * sizeof(int32_t), c.stream));
+  launch_fold_apply(c, d_a);
+  OSM_CUDA(cudaMemcpyAsync(c.d_sides, c.h_sides.data(), sizeof(SideDev) * nsides, cudaMemcpyHostToDevice, c.stream));
+  int32_t flags[4];
+  OSM_CUDA(cudaMemcpyAsync(flags, c.d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  dfree(d_a);
+  if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
+  c.robin_dirty = false;
+}
+
+// ------------------------------------------------------------------ exchange
+// part 1: [g | u] both directions for every remote side; part 2: the right slab's
+// interface-row residual w to the owner (left slab).
+static void exchange(Ctx& c, int part) {
+  if (c.nranks == 1) return;
+  bool any = false;
+  for (const Side& sd : c.sides) any = any || sd.remote;
+  if (!any) return;
+  const int64_t nG = c.nG;
+  OSM_NCCL(ncclGroupStart());
+  for (const Side& sd : c.sides) {
+    if (!sd.remote) continue;
+    if (part == 1) {
+      OSM_NCCL(ncclSend(sd.out, 2 * nG, ncclDouble, sd.peer, c.comm, c.stream));
+      OSM_NCCL(ncclRecv(sd.inbuf, 2 * nG, ncclDouble, sd.peer, c.comm, c.stream));
+    } else if (sd.which == 1) {
+      OSM_NCCL(ncclSend(sd.out + 2 * nG, nG, ncclDouble, sd.peer, c.comm, c.stream));
+    } else {
+      OSM_NCCL(ncclRecv(sd.inbuf + 2 * nG, nG, ncclDouble, sd.peer, c.comm, c.stream));
+    }
+  }
+  OSM_NCCL(ncclGroupEnd());
+}
+
+// Per-subdomain values (local, in subdomain order) -> all nsub values on every rank.
+static std::vector<double> allgather_sub(Ctx& c, const std::vector<double>& local, int width) {
+  const int nloc = c.s_end - c.s_begin;
+  if (c.nranks == 1) return local;
+  double* d = dalloc<double>((int64_t)c.nsub * width);
+  OSM_CUDA(cudaMemcpyAsync(d + (int64_t)c.s_begin * width, local.data(), sizeof(double) * nloc * width,
+                           cudaMemcpyHostToDevice, c.stream));
+  OSM_NCCL(ncclAllGather(d + (int64_t)c.s_begin * width, d, (size_t)nloc * width, ncclDouble, c.comm, c.stream));
+  std::vector<double> all((size_t)c.nsub * width);
+  OSM_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  dfree(d);
+  return all;
+}
+
+// Glued residual pipeline: sum over global free rows of (f - K u~)^2,
+// each interface row counted once (owned by the left slab).  zero = 1 gives ||f||^2.
+static double glued_residual2(Ctx& c, int zero, std::vector<int32_t>* iters_out) {
+  launch_glue(c, zero);
+  launch_resid(c);
+  launch_iface_w(c);
+  exchange(c, 2);
+  launch_iface_sum(c);
+  const int nloc = c.s_end - c.s_begin;
+  const int nsides = (int)c.sides.size();
+  OSM_CUDA(cudaMemcpyAsync(c.h_st, c.st, sizeof(SubState) * nloc, cudaMemcpyDeviceToHost, c.stream));
+  if (nsides)
+    OSM_CUDA(cudaMemcpyAsync(c.h_side_sum, c.side_sum, sizeof(double) * nsides, cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<double> loc(2 * nloc);
+  for (int ls = 0; ls < nloc; ++ls) {
+    double v = c.h_st[ls].resid;
+    const int k = c.subs[ls].side[1];
+    if (k >= 0) v += c.h_side_sum[k];
+    loc[2 * ls] = v;
+    loc[2 * ls + 1] = (double)c.h_st[ls].iters + 1e6 * (c.h_st[ls].status == 2);
+  }
+  std::vector<double> all = allgather_sub(c, loc, 2);
+  double tot = 0.0;
+  for (int s = 0; s < c.nsub; ++s) tot += all[2 * s];
+  if (iters_out) {
+    iters_out->resize(c.nsub);
+    for (int s = 0; s < c.nsub; ++s) (*iters_out)[s] = (int32_t)all[2 * s + 1];
+  }
+  return tot;
+}
+
+// ------------------------------------------------------------------ solve
+static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
+  if (!c.assembled) fail(OSM_ERR_STATE, "osm_assemble must precede osm_solve");
+  if (!c.density_set) fail(OSM_ERR_STATE, "osm_upload_density must precede osm_solve");
+  if (o.max_outer < 1 || o.max_inner < 1 || !(o.tol_outer > 0) || !(o.tol_inner > 0))
+    fail(OSM_ERR_INVALID_ARG, "bad solve options");
+  const auto t0 = std::chrono::steady_clock::now();
+  apply_robin(c);
+  const int64_t nGs = (int64_t)c.sides.size() * c.nG;
+  c.fnorm2 = glued_residual2(c, 1, nullptr);
+  const double fnorm = std::sqrt(c.fnorm2);
+  OSM_CUDA(cudaMemsetAsync(c.x, 0, sizeof(double) * c.nrows_total, c.stream));
+  if (nGs) {
+    OSM_CUDA(cudaMemsetAsync(c.lam_all, 0, sizeof(double) * nGs, c.stream));
+    OSM_CUDA(cudaMemsetAsync(c.unbr_all, 0, sizeof(double) * nGs, c.stream));
+  }
+  c.hist.clear();
+  c.inner.clear();
+  int status = OSM_NOT_CONVERGED;
+  int grow = 0;
+  int64_t inner_total = 0;
+  int inner_maxed = 0;
+  constexpr int kChunk = 8;
+  for (int n = 1; n <= o.max_outer; ++n) {
+    if (!o.warm_start) OSM_CUDA(cudaMemsetAsync(c.x, 0, sizeof(double) * c.nrows_total, c.stream));
+    OSM_CUDA(cudaMemsetAsync(c.d_nactive, 0, sizeof(int32_t), c.stream));
+    launch_warm(c, o.tol_inner, o.warm_start);
+    launch_zero_if(c);
+    OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[0], c.d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.h_nactive[0] > 0) {
+      // batched masked PCG: enqueue chunks; poll the active count one chunk behind
+      for (int ch = 0;; ++ch) {
+        for (int it = 0; it < kChunk; ++it) {
+          launch_cg_spmv(c);
+          launch_cg_update(c, o.tol_inner, o.max_inner);
+          launch_cg_dir(c);
+        }
+        OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[ch & 1], c.d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        OSM_CUDA(cudaEventRecord(c.ev_chunk[ch & 1], c.stream));
+        if (ch > 0) {
+          OSM_CUDA(cudaEventSynchronize(c.ev_chunk[(ch - 1) & 1]));
+          if (c.h_nactive[(ch - 1) & 1] == 0) break;
+        }
+        if ((int64_t)ch * kChunk > (int64_t)o.max_inner + 2 * kChunk) break;  // safety net
+      }
+    }
+    launch_trace(c);
+    exchange(c, 1);
+    launch_accept(c);
+    std::vector<int32_t> its;
+    const double r2 = glued_residual2(c, 0, &its);
+    const double h = fnorm > 0 ? std::sqrt(r2) / fnorm : std::sqrt(r2);
+    c.hist.push_back(h);
+    for (int s = 0; s < c.nsub; ++s) {
+      int32_t k = its[s];
+      if (k >= 1000000) {
+        ++inner_maxed;
+        k -= 1000000;
+      }
+      c.inner.push_back((s >= c.s_begin && s < c.s_end) ? k : -1);
+      inner_total += k;
+    }
+    if (c.hist.size() >= 2 && c.hist[c.hist.size() - 1] > c.hist[c.hist.size() - 2]) ++grow; else grow = 0;
+    if (!std::isfinite(h)) {
+      status = OSM_ERR_DIVERGED;
+      break;
+    }
+    if (h <= o.tol_outer) {
+      status = OSM_OK;
+      break;
+    }
+    if (o.diverge_window > 0 && grow >= o.diverge_window) {
+      status = OSM_ERR_DIVERGED;
+      break;
+    }
+  }
+  timers_collect(c);
+  // traffic model: algorithmic bytes per CG iteration per subdomain x its iterations
+  for (double& t : c.traffic) t = 0;
+  const int nloc = c.s_end - c.s_begin;
+  for (int ls = 0; ls < nloc; ++ls) {
+    const Sub& S = c.subs[ls];
+    int64_t its = 0;
+    for (size_t k = S.s; k < c.inner.size(); k += c.nsub) its += std::max(0, c.inner[k]);
+    c.traffic[0] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);
+    c.traffic[1] += (double)its * 56.0 * S.n;
+    c.traffic[2] += (double)its * 32.0 * S.n;
+    c.traffic[3] += (double)(S.sell_entries - S.nnz);
+    c.traffic[4] += (double)S.nnz;
+    c.traffic[5] += (double)S.n;
+  }
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rep) {
+    rep->outer_iters = (int)c.hist.size();
+    rep->converged = status == OSM_OK;
+    rep->h_final = c.hist.empty() ? 0.0 : c.hist.back();
+    rep->seconds = secs;
+    rep->inner_total = inner_total;
+    rep->inner_maxed = inner_maxed;
+  }
+  return (osm_status)status;
+}
+
+}  // namespace osm
+
+// ================================================================== C ABI
+using namespace osm;
+
+struct osm_ctx {
+  Ctx c;
+};
+
+#define OSM_API_BEGIN try {
+#define OSM_API_END                                 \
+  }                                                 \
+  catch (const Error& e) {                          \
+    g_last_error = e.what();                        \
+    return e.status;                                \
+  }                                                 \
+  catch (const std::exception& e) {                 \
+    g_last_error = e.what();                        \
+    return OSM_ERR_CUDA;                            \
+  }                                                 \
+  catch (...) {                                     \
+    g_last_error = "unknown error";                 \
+    return OSM_ERR_CUDA;                            \
+  }
+
+static Ctx& ctx_of(osm_ctx* c) {
+  if (!c) fail(OSM_ERR_INVALID_ARG, "NULL context");
+  OSM_CUDA(cudaSetDevice(c->c.device));
+  return c->c;
+}
+
+extern "C" {
+
+int osm_abi_version(void) { return OSM_ABI_VERSION; }
+
+const char* osm_last_error(void) { return g_last_error.c_str(); }
+
+osm_status osm_nccl_unique_id(void* uid128) {
+  OSM_API_BEGIN
+  if (!uid128) fail(OSM_ERR_INVALID_ARG, "NULL uid buffer");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  OSM_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(uid128, &id, sizeof(id));
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_ctx** out) {
+  OSM_API_BEGIN
+  if (!mesh || !out) fail(OSM_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  const osm_mesh_desc& m = *mesh;
+  if (m.nx <= 0 || m.ny <= 0 || m.nz <= 0 || !(m.lx > 0) || !(m.ly > 0) || !(m.lz > 0))
+    fail(OSM_ERR_INVALID_ARG, "cell counts and extents must be positive");
+  if (m.order != 1 && m.order != 2) fail(OSM_ERR_INVALID_ARG, "order must be 1 or 2");
+  if (m.order * m.nx + 1 < 3 || m.order * m.ny + 1 < 3 || m.order * m.nz + 1 < 3)
+    fail(OSM_ERR_GRID_TOO_SMALL, "fewer than 3 lattice points on an axis: no interior");
+  osm_dist_desc d{0, 1, 0, nullptr, nullptr};
+  if (dist) d = *dist;
+  if (d.nranks < 1 || d.rank < 0 || d.rank >= d.nranks) fail(OSM_ERR_INVALID_ARG, "bad rank/nranks");
+  if (d.nranks > 1 && !d.nccl_uid) fail(OSM_ERR_INVALID_ARG, "nccl_uid required when nranks > 1");
+  auto* h = new osm_ctx();
+  Ctx& c = h->c;
+  try {
+    c.mesh = m;
+    c.rank = d.rank;
+    c.nranks = d.nranks;
+    c.device = d.device;
+    OSM_CUDA(cudaSetDevice(c.device));
+    if (d.stream) {
+      c.stream = (cudaStream_t)d.stream;
+    } else {
+      OSM_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.own_stream = true;
+    }
+    OSM_CUDA(cudaMallocHost((void**)&c.h_nactive, 2 * sizeof(int32_t)));
+    c.d_nactive = dalloc<int32_t>(1);
+    OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[0], cudaEventDisableTiming));
+    OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[1], cudaEventDisableTiming));
+    c.timers.resize(T_COUNT);
+    const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};
+    for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
+    if (c.nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, d.nccl_uid, sizeof(id));
+      OSM_NCCL(ncclCommInitRank(&c.comm, c.nranks, id, c.rank));
+    }
+  } catch (...) {
+    osm_destroy(h);
+    throw;
+  }
+  *out = h;
+  return OSM_OK;
+  OSM_API_END
+}
+
+void osm_destroy(osm_ctx* h) {
+  if (!h) return;
+  Ctx& c = h->c;
+  cudaSetDevice(c.device);
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  try {
+    free_assembly(c);
+  } catch (...) {
+  }
+  dfree(c.drho);
+  dfree(c.d_nactive);
+  dfree(c.d_flags);
+  if (c.h_nactive) cudaFreeHost(c.h_nactive);
+  if (c.h_st) cudaFreeHost(c.h_st);
+  if (c.h_side_sum) cudaFreeHost(c.h_side_sum);
+  for (auto& e : c.ev_chunk)
+    if (e) cudaEventDestroy(e);
+  for (auto& t : c.timers)
+    for (auto& e : t.ev) cudaEventDestroy(e);
+  if (c.comm) ncclCommDestroy(c.comm);
+  if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+  delete h;
+}
+
+osm_status osm_decompose(osm_ctx* h, int nsub) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (nsub < 1 || nsub > c.mesh.nx || nsub % c.nranks != 0)
+    fail(OSM_ERR_INVALID_ARG, "need 1 <= nsub <= nx and nsub % nranks == 0");
+  free_assembly(c);
+  c.nsub = nsub;
+  c.cstart = partition_x(c.mesh.nx, nsub);
+  c.s_begin = (int)((int64_t)c.rank * nsub / c.nranks);
+  c.s_end = (int)((int64_t)(c.rank + 1) * nsub / c.nranks);
+  c.robin_set = nsub == 1;
+  c.alpha_left.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
+  c.alpha_right.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_set_robin(osm_ctx* h, const double* al, const double* ar) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (c.nsub < 1) fail(OSM_ERR_STATE, "osm_decompose must precede osm_set_robin");
+  const int ni = c.nsub - 1;
+  if (ni > 0 && (!al || !ar)) fail(OSM_ERR_INVALID_ARG, "NULL alpha array");
+  for (int i = 0; i < ni; ++i) {
+    if (!(al[i] >= 0) || !(ar[i] >= 0) || !std::isfinite(al[i]) || !std::isfinite(ar[i]))
+      fail(OSM_ERR_ILL_POSED, "Robin alpha must be finite and >= 0");
+    if (al[i] == 0 && ar[i] == 0) fail(OSM_ERR_ILL_POSED, "alpha = 0 on both sides of an interface");
+  }
+  c.alpha_left.assign(al, al + ni);
+  c.alpha_right.assign(ar, ar + ni);
+  c.robin_set = true;
+  c.robin_dirty = true;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_assemble(osm_ctx* h) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (c.nsub < 1) fail(OSM_ERR_STATE, "osm_decompose must precede osm_assemble");
+  assemble(c);
+  return OSM_OK;
+  OSM_API_END
+}
+
+static void upload_density(Ctx& c, const double* drho, bool device, double G) {
+  if (!c.assembled) fail(OSM_ERR_STATE, "osm_assemble must precede osm_upload_density");
+  if (!drho) fail(OSM_ERR_INVALID_ARG, "NULL density");
+  if (!std::isfinite(G)) fail(OSM_ERR_INVALID_ARG, "G must be finite");
+  const int64_t ncell = c.mesh.nx * c.mesh.ny * c.mesh.nz;
+  if (!c.drho) c.drho = dalloc<double>(ncell);
+  OSM_CUDA(cudaMemcpyAsync(c.drho, drho, sizeof(double) * ncell,
+                           device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+  c.G = G;
+  const double fourpiG = 4.0 * M_PI * G;
+  for (const Sub& S : c.subs) launch_load(c, S, fourpiG);
+  if (!device) OSM_CUDA(cudaStreamSynchronize(c.stream));  // the caller may free its host buffer
+  c.density_set = true;
+}
+
+osm_status osm_upload_density(osm_ctx* h, const double* drho, double G) {
+  OSM_API_BEGIN
+  upload_density(ctx_of(h), drho, false, G);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_upload_density_device(osm_ctx* h, const double* drho, double G) {
+  OSM_API_BEGIN
+  upload_density(ctx_of(h), drho, true, G);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_solve(osm_ctx* h, const osm_solve_opts* o, osm_report* rep) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!o) fail(OSM_ERR_INVALID_ARG, "NULL options");
+  return solve(c, *o, rep);
+  OSM_API_END
+}
+
+osm_status osm_get_history(osm_ctx* h, double* out, int cap, int* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  *n = (int)c.hist.size();
+  if (out) std::copy(c.hist.begin(), c.hist.begin() + std::min<int>(cap, (int)c.hist.size()), out);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_inner_iters(osm_ctx* h, int32_t* its, int cap_outer, int* n_outer) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n_outer) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  *n_outer = (int)c.hist.size();
+  if (its) {
+    const size_t m = std::min<size_t>((size_t)cap_outer * c.nsub, c.inner.size());
+    std::copy(c.inner.begin(), c.inner.begin() + m, its);
+  }
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_solution(osm_ctx* h, double* phi, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  const int o = c.mesh.order;
+  const int64_t N = (o * c.mesh.nx + 1) * (o * c.mesh.ny + 1) * (o * c.mesh.nz + 1);
+  if (!phi && c.rank == 0) {
+    *n = N;
+    return OSM_OK;
+  }
+  if (!c.assembled) fail(OSM_ERR_STATE, "nothing solved");
+  if (c.rank == 0 && *n < N) fail(OSM_ERR_INVALID_ARG, "solution buffer too small");
+  if (!c.phi) c.phi = dalloc<double>(N);
+  OSM_CUDA(cudaMemsetAsync(c.phi, 0, sizeof(double) * N, c.stream));
+  for (const Sub& S : c.subs) launch_scatter_phi(c, S, c.nranks > 1 ? 1 : 0);
+  if (c.nranks > 1) OSM_NCCL(ncclReduce(c.phi, c.phi, N, ncclDouble, ncclSum, 0, c.comm, c.stream));
+  if (c.rank == 0 && phi)
+    OSM_CUDA(cudaMemcpyAsync(phi, c.phi, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  *n = N;
+  return OSM_OK;
+  OSM_API_END
+}
+
+static const Sub& local_sub(const Ctx& c, int s) {
+  if (!c.assembled) fail(OSM_ERR_STATE, "not assembled");
+  if (s < c.s_begin || s >= c.s_end) fail(OSM_ERR_INVALID_ARG, "subdomain not owned by this rank");
+  return c.subs[s - c.s_begin];
+}
+
+osm_status osm_get_local_solution(osm_ctx* h, int s, double* u, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  const Sub& S = local_sub(c, s);
+  if (!u) {
+    *n = S.n;
+    return OSM_OK;
+  }
+  if (*n < S.n) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+  double* d = dalloc<double>(S.n);
+  launch_gather_local(c, S, d);
+  OSM_CUDA(cudaMemcpyAsync(u, d, sizeof(double) * S.n, cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  dfree(d);
+  *n = S.n;
+  return OSM_OK;
+  OSM_API_END
+}
+
+static int find_side(const Ctx& c, int iface, int side) {
+  if (iface < 0 || iface >= c.nsub - 1 || (side != 0 && side != 1)) fail(OSM_ERR_INVALID_ARG, "bad interface/side");
+  for (size_t k = 0; k < c.sides.size(); ++k)
+    if (c.sides[k].iface == iface && c.sides[k].which == side) return (int)k;
+  fail(OSM_ERR_INVALID_ARG, "interface side not owned by this rank");
+}
+
+osm_status osm_get_trace(osm_ctx* h, int iface, int side, double* lam, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  const int k = find_side(c, iface, side);
+  if (!lam) {
+    *n = c.nG;
+    return OSM_OK;
+  }
+  if (*n < c.nG) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+  OSM_CUDA(cudaMemcpyAsync(lam, c.lam_all + k * c.nG, sizeof(double) * c.nG, cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  *n = c.nG;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_csr(osm_ctx* h, int s, int64_t* rowptr, int32_t* col, double* val, int64_t* nrows, int64_t* nnz) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!nrows || !nnz) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  const Sub& S = local_sub(c, s);
+  if (rowptr) {
+    if (*nrows < S.n || *nnz < S.nnz) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+    OSM_CUDA(cudaMemcpyAsync(rowptr, S.rowptr, sizeof(int64_t) * (S.n + 1), cudaMemcpyDeviceToHost, c.stream));
+    if (col) OSM_CUDA(cudaMemcpyAsync(col, S.col, sizeof(int32_t) * S.nnz, cudaMemcpyDeviceToHost, c.stream));
+    if (val) OSM_CUDA(cudaMemcpyAsync(val, S.val, sizeof(double) * S.nnz, cudaMemcpyDeviceToHost, c.stream));
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+  }
+  *nrows = S.n;
+  *nnz = S.nnz;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_interface_map(osm_ctx* h, int iface, int side, int32_t* idx, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  const int k = find_side(c, iface, side);
+  if (idx) {
+    if (*n < c.nG) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+    OSM_CUDA(cudaMemcpyAsync(idx, c.sides[k].map_c, sizeof(int32_t) * c.nG, cudaMemcpyDeviceToHost, c.stream));
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+  }
+  *n = c.nG;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_interface_mass(osm_ctx* h, int64_t* rowptr, int32_t* col, double* val, int64_t* nrows,
+                                  int64_t* nnz) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!nrows || !nnz) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  if (!c.assembled) fail(OSM_ERR_STATE, "not assembled");
+  const int64_t m = c.h_mrow.back();
+  if (rowptr) {
+    if (*nrows < c.nG || *nnz < m) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+    for (int64_t i = 0; i <= c.nG; ++i) rowptr[i] = c.h_mrow[i];
+    if (col) std::copy(c.h_mcol.begin(), c.h_mcol.end(), col);
+    if (val) std::copy(c.h_mval.begin(), c.h_mval.end(), val);
+  }
+  *nrows = c.nG;
+  *nnz = m;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_set_kernel_timing(osm_ctx* h, int enable) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  c.timing = enable != 0;
+  for (auto& t : c.timers) {
+    t.used = 0;
+    t.total_ms = 0;
+    t.launches = 0;
+  }
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_kernel_timing(osm_ctx* h, osm_kernel_time* out, int cap, int* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  *n = (int)c.timers.size();
+  if (out)
+    for (int i = 0; i < std::min(cap, *n); ++i) {
+      std::memset(out[i].name, 0, sizeof(out[i].name));
+      std::strncpy(out[i].name, c.timers[i].name.c_str(), sizeof(out[i].name) - 1);
+      out[i].launches = c.timers[i].launches;
+      out[i].total_ms = c.timers[i].total_ms;
+    }
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_traffic_model(osm_ctx* h, double* out, int n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!out) fail(OSM_ERR_INVALID_ARG, "NULL output");
+  for (int i = 0; i < std::min(n, 6); ++i) out[i] = c.traffic[i];
+  return OSM_OK;
+  OSM_API_END
+}
+
+}  // extern "C"

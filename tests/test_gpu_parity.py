@@ -1,0 +1,125 @@
+"""CUDA path vs oracle on the same seeded inputs (through the C ABI).
+
+Bars (BASELINE north_star):
+  * bit-exact: CSR patterns of every K_s^N, interface maps, DOF numbering;
+  * CSR values and M_Gamma within 1e-13 relative (different but exact element integrals);
+  * Schwarz history |h_gpu - h_or| <= 1e-8 h_or + 1e-14 at every n, same outer count
+    (+-1 only at a stopping tie), inner PCG counts equal (+-1 at a tie);
+  * final Phi within 1e-10 relative L2 (same outer count).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import fe, mesh, schwarz
+
+from parity_util import history_ok, oracle_run, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    # name: (config, field, alpha_left, alpha_right)
+    "C1_p1_8cube_S2": (dict(nx=8, ny=8, nz=8, lx=1.0, ly=1.0, lz=1.0, order=1, nsub=2), "ball", 20.0, 20.0),
+    "p2_6cube_S2": (dict(nx=6, ny=6, nz=6, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=2), "ball", 25.0, 25.0),
+    "p2_ragged_S3_unsym": (dict(nx=10, ny=5, nz=4, lx=1.0, ly=0.6, lz=0.5, order=2, nsub=3), "random", 30.0, 12.0),
+    "p1_thin_S4": (dict(nx=12, ny=9, nz=3, lx=250e3, ly=250e3, lz=15e3, order=1, nsub=4), "chicxulub", 3e-4, 4e-4),
+    "p2_single": (dict(nx=5, ny=4, nz=6, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=1), "random", None, None),
+}
+
+
+def _field(cfg, kind):
+    args = (cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"])
+    if kind == "ball":
+        return synth.ball(*args)
+    if kind == "chicxulub":
+        return synth.chicxulub(*args)
+    return synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=11)
+
+
+def _gpu(cfg, drho, al, ar):
+    import paper_2112_03851_b200 as P
+
+    o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+    o.decompose(cfg["nsub"])
+    if cfg["nsub"] > 1:
+        o.set_robin(np.full(cfg["nsub"] - 1, al), np.full(cfg["nsub"] - 1, ar))
+    o.assemble()
+    o.upload_density(drho)
+    return o
+
+
+@pytest.fixture(scope="module", params=sorted(CASES))
+def case(request):
+    cfg, kind, al, ar = CASES[request.param]
+    drho = _field(cfg, kind)
+    S = cfg["nsub"]
+    prob, rep = oracle_run(cfg, drho, [al] * (S - 1), [ar] * (S - 1))
+    o = _gpu(cfg, drho, al, ar)
+    st, grep = o.solve(tol_outer=1e-8, max_outer=500)
+    yield dict(name=request.param, cfg=cfg, prob=prob, rep=rep, o=o, st=st, grep=grep, al=al, ar=ar)
+    o.close()
+
+
+def test_csr_patterns_bitexact_values_close(case):
+    o, prob = case["o"], case["prob"]
+    for s, sub in enumerate(prob.subs):
+        rp, col, val = o.csr(s)
+        K = sub.KN
+        assert np.array_equal(rp, K.indptr.astype(np.int64)), "row pointers"
+        assert np.array_equal(col, K.indices.astype(np.int32)), "column indices"
+        scale = np.abs(K.data).max()
+        assert np.abs(val - K.data).max() <= 1e-13 * scale
+
+
+def test_interface_maps_and_mass(case):
+    o, prob = case["o"], case["prob"]
+    for i in range(prob.nsub - 1):
+        assert np.array_equal(o.interface_map(i, 0), prob.subs[i].right.astype(np.int32))
+        assert np.array_equal(o.interface_map(i, 1), prob.subs[i + 1].left.astype(np.int32))
+    if prob.nsub > 1:
+        rp, col, val = o.interface_mass()
+        M = prob.MG
+        assert np.array_equal(rp, M.indptr.astype(np.int64)) and np.array_equal(col, M.indices.astype(np.int32))
+        assert np.abs(val - M.data).max() <= 1e-13 * np.abs(M.data).max()
+
+
+def test_history_and_inner_counts(case):
+    rep, o = case["rep"], case["o"]
+    h_gpu = o.history()
+    h_or = np.array(rep.h)
+    ok, d = history_ok(h_gpu, h_or)
+    assert ok, f"max |dh| = {d.max():.3e}"
+    assert abs(len(h_gpu) - len(h_or)) <= 1
+    if len(h_gpu) != len(h_or):  # only at a stopping tie
+        assert abs(h_or[-1] - 1e-8) <= 1e-4 * 1e-8 or abs(h_gpu[-1] - 1e-8) <= 1e-4 * 1e-8
+    its = o.inner_iters()
+    n = min(len(its), len(rep.inner))
+    diff = np.abs(its[:n] - np.array(rep.inner[:n]))
+    assert diff.max() <= 1 and (diff > 0).mean() < 0.05, diff
+
+
+def test_solution_phi(case):
+    rep, o, prob = case["rep"], case["o"], case["prob"]
+    if o.history().size != len(rep.h):
+        pytest.skip("stopping tie: different outer counts")
+    phi = o.solution()
+    phi_or = schwarz.full_lattice(prob, rep.ut)
+    assert rel_l2(phi, phi_or) <= 1e-10
+    for s in range(prob.nsub):
+        assert rel_l2(o.local_solution(s), rep.u[s]) <= 1e-10
+    for i in range(prob.nsub - 1):
+        assert rel_l2(o.trace(i, 0), rep.lam[(i, 0)]) <= 1e-9
+        assert rel_l2(o.trace(i, 1), rep.lam[(i, 1)]) <= 1e-9
+
+
+def test_converged_to_monolithic(case):
+    """The GPU fixed point is the FE solution: ||f - K Phi|| / ||f|| equals the reported h."""
+    o, prob = case["o"], case["prob"]
+    phi = o.solution()
+    box = prob.box
+    Nx, Ny, Nz = box.lattice
+    K, J, I = np.meshgrid(np.arange(1, Nz - 1), np.arange(1, Ny - 1), np.arange(1, Nx - 1), indexing="ij")
+    ut = phi[box.lattice_id(I.ravel(), J.ravel(), K.ravel())]
+    h = schwarz.global_residual(prob, ut)
+    assert abs(h - o.history()[-1]) <= 1e-10 * h + 1e-14
+    assert case["st"] == 0 and h <= 1e-8

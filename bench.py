@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 optimized-Schwarz gravimetry solve (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+One "step" = one full Schwarz solve to h <= 1e-8 (every row of SURVEY 8(a): load
+update from the resident density, warm-start residuals, batched PCG to 1e-10,
+Robin traces, exchange, glued residual) on the BASELINE config C3 (P2, 64^3
+cells on the paper's 250 x 250 x 15 km box, Chicxulub-like density, 8 x-slab
+subdomains).  value = DOF_global x outer iterations / second (whole job).
+For N > 1 launch with torchrun (one rank per GPU, NCCL); the 8 subdomains are
+split over the ranks (strong scaling at fixed S).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "DOF*iter/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel="k_cg_spmv"):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(kernel)
+
+
+class ClockSampler(threading.Thread):
+    """NVML clocks / throttle reasons sampled every 100 ms during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        super().__init__(daemon=True)
+        self.index, self.samples, self.reasons, self.stop_ev, self.max_mhz = index, [], 0, threading.Event(), None
+        self.ok = False
+
+    def run(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            while not self.stop_ev.is_set():
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                try:
+                    self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    self.reasons |= pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                time.sleep(0.1)
+        except Exception as e:  # NVML missing: report, do not fail the bench
+            self.err = str(e)
+
+    def summary(self):
+        self.stop_ev.set()
+        self.join(timeout=2)
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b], "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- oracle sample (CPU)
+def oracle_sample(cfg, drho, alpha, iters):
+    """Times the CPU oracle (oracle/, as it stands) on a bounded sample of the workload.
+
+    Sample: `iters` Jacobi-PCG iterations of the oracle on interior subdomain 1 (Robin-augmented
+    K_1, cold start, rhs = b_1), single thread.  Returns (seconds per CG iteration, rows of the slab,
+    threads used).  Assembly of the sample is not timed.
+    """
+    from threadpoolctl import threadpool_limits
+
+    from oracle import linalg, mesh, schwarz
+
+    box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+    s = 1 if cfg["nsub"] > 2 else 0
+    prob = schwarz.build_problem(box, cfg["nsub"], drho=drho, only=[s], monolithic=False)
+    al, ar = synth.alphas(cfg, alpha)
+    A = schwarz.robin_operators(prob, al, ar)
+    Ks = schwarz.subdomain_operator(prob, s, A)
+    b = prob.subs[s].b
+    with threadpool_limits(limits=1):
+        t = time.perf_counter()
+        linalg.pcg(Ks, b, tol=1e-300, maxit=iters)
+        dt = time.perf_counter() - t
+    return dt / iters, Ks.shape[0], 1
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg, drho, rank):
+    if rank != 0:
+        return
+    fz = cfg.get("frozen")
+    if not fz:
+        print(json.dumps({"impl": "reference", "unavailable": f"no frozen iteration counts for {args.config}"}))
+        return
+    vals = []
+    sample_iters = args.ref_iters
+    for k in range(args.warmup + args.steps):
+        t_iter, n_s, cores = oracle_sample(cfg, drho, cfg["alpha"], sample_iters)
+        t_solve = t_iter / n_s * fz["cg_work"]  # CG time of the whole solve, scaled by DOF x CG-iterations
+        v = cfg["dof"] * fz["outer"] / t_solve
+        if k >= args.warmup:
+            vals.append((v, t_solve))
+    v = statistics.median([a for a, _ in vals])
+    t = statistics.median([b for _, b in vals])
+    sample = (f"{sample_iters} oracle Jacobi-PCG iterations on subdomain 1 of {args.config} (scipy CSR, 1 thread), "
+              f"extrapolated by the workload's DOF x CG-iteration count {fz['cg_work']:.4g} and {fz['outer']} outer "
+              f"iterations (identical in oracle and GPU path, tests/test_gpu_parity.py); glued-residual SpMVs not timed")
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, cfg):
+    return {"workload": f"{args.config}: P{cfg['order']} {cfg['nx']}x{cfg['ny']}x{cfg['nz']} Kuhn box "
+                        f"{cfg['lx']/1e3:g}x{cfg['ly']/1e3:g}x{cfg['lz']/1e3:g} km, {cfg['field']} density, "
+                        f"{cfg['nsub']} x-slab subdomains",
+            "dof": cfg["dof"], "nsub": cfg["nsub"], "alpha": cfg["alpha"], "tol_outer": 1e-8, "tol_inner": 1e-10,
+            "l2": "no flush: CG working set >> 126 MB L2 (939 MB per CG iteration at C3 on 1 GPU)",
+            "parallelism": f"{cfg['nsub']} subdomains over {args.gpus} GPU(s)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--alpha", default=None, help="alpha or alpha_1:alpha_2 (two-sided)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-iters", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--timing-steps", type=int, default=1)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = dict(synth.CONFIGS[args.config])
+    if args.alpha is not None:
+        cfg["alpha"] = tuple(float(v) for v in args.alpha.split(":")) if ":" in args.alpha else float(args.alpha)
+    o_ = cfg["order"]
+    cfg["dof"] = (o_ * cfg["nx"] - 1) * (o_ * cfg["ny"] - 1) * (o_ * cfg["nz"] - 1)
+    drho = synth.density(cfg)
+
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+        run_reference(args, cfg, drho, rank)
+        return
+
+    import torch
+
+    import paper_2112_03851_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.Stream()
+    osm = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], rank=rank,
+                nranks=world, device=local_rank, nccl_uid=uid, stream=stream.cuda_stream)
+    osm.decompose(cfg["nsub"])
+    S = cfg["nsub"]
+    osm.set_robin(*synth.alphas(cfg))
+    t_setup = time.perf_counter()
+    osm.assemble()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    d_drho = torch.from_numpy(drho).to(f"cuda:{local_rank}")  # inputs resident in HBM
+    torch.cuda.synchronize()
+
+    def step():
+        osm.upload_density_device(d_drho.data_ptr())
+        return osm.solve(tol_outer=1e-8, max_outer=1000)
+
+    for _ in range(args.warmup):
+        st, rep = step()
+    if st != 0:
+        raise SystemExit(f"warm-up solve did not converge: status {st}, h = {rep.h_final}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = osm.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    outer, inner, cg_work = 0, 0, 0.0
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st, rep = step()
+        outer += rep.outer_iters
+        inner += rep.inner_total
+        cg_work += local_cg_work(osm, S, rank, world)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.summary()
+    launches = osm.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        w = torch.tensor([cg_work], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(w)
+        cg_work = float(w.item())
+    ms_step = ms / args.steps
+    value = cfg["dof"] * outer / (ms / 1e3)
+
+    # Dominant kernel roofline (k_cg_spmv): CUDA events around every launch on the library
+    # stream, recorded during instrumented solves run right after the timed region (per-launch
+    # events cost ~1 us of GPU time each, so they stay out of the timed steps).
+    osm.set_kernel_timing(True)
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    traffic = dict(spmv_bytes=0.0, update_bytes=0.0, dir_bytes=0.0)
+    ev2.record(stream)
+    for _ in range(args.timing_steps):
+        step()
+        tm = osm.traffic_model()
+        for k in traffic:
+            traffic[k] += tm[k]
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    ms_instr = ev2.elapsed_time(ev3)
+    kt = osm.kernel_timing()
+    osm.set_kernel_timing(False)
+    peak, peak_src = hbm_peak()
+    spmv_launches, spmv_ms = kt["cg_spmv"]
+    achieved = traffic["spmv_bytes"] / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
+    tr = ncu_traffic()
+    per_launch_alg = traffic["spmv_bytes"] / max(1, spmv_launches)
+    roofline = {"bound": "hbm", "kernel": "k_cg_spmv", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None,
+                "traffic": tr, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": per_launch_alg,
+                "share_of_cg_time": spmv_ms / sum(kt[k][1] for k in ("cg_spmv", "cg_update", "cg_dir")),
+                "share_of_step": spmv_ms / ms_instr if ms_instr > 0 else None,
+                "instrumented_steps": args.timing_steps,
+                "cg_kernels_gbs": {k: (traffic[b] / (kt[k][1] / 1e3) / 1e9 if kt[k][1] > 0 else None)
+                                   for k, b in (("cg_update", "update_bytes"), ("cg_dir", "dir_bytes"))},
+                "kernel_ms": {k: v[1] for k, v in kt.items()}, "kernel_launches": {k: v[0] for k, v in kt.items()}}
+
+    # e2e through the C ABI with host buffers: pinned drho H2D + solve + Phi D2H, every step
+    h_drho = torch.from_numpy(drho).pin_memory()
+    phi = torch.empty(int(np.prod(osm.lattice)), dtype=torch.float64).pin_memory() if rank == 0 else None
+    barrier()
+    t0 = time.perf_counter()
+    e2e_outer = 0
+    for _ in range(args.e2e_steps):
+        osm.upload_density(h_drho.numpy())
+        st2, rep2 = osm.solve(tol_outer=1e-8, max_outer=1000)
+        e2e_outer += rep2.outer_iters
+        osm.solution(out=phi.numpy() if phi is not None else None)
+    barrier()
+    t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([t_e2e], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = {"value": cfg["dof"] * e2e_outer / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(drho.nbytes),
+           "d2h_bytes_per_step": int(np.prod(osm.lattice)) * 8, "steps": args.e2e_steps,
+           "path": "osm_upload_density(host pinned) + osm_solve + osm_get_solution(host pinned)"}
+
+    if rank != 0:
+        osm.close()
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        t_iter, n_s, cores = oracle_sample(cfg, drho, cfg["alpha"], args.ref_iters)
+        t_solve = t_iter / n_s * (cg_work / args.steps)
+        cpu = {"value": cfg["dof"] * (outer / args.steps) / t_solve, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{args.ref_iters} oracle Jacobi-PCG iterations on subdomain 1 (scipy CSR, 1 thread), "
+                         f"extrapolated with this run's DOF x CG-iteration count and outer count; glued-residual "
+                         f"SpMVs not timed", "seconds_per_cg_iteration": t_iter, "sample_rows": n_s}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
+            "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
+            "cg_dof_iter_per_s": cg_work / (ms / 1e3), "setup_s": t_setup,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "status": int(st)}
+    print(json.dumps(line), flush=True)
+    osm.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+_rows = {}
+
+
+def local_cg_work(osm, S, rank, world):
+    """sum over local subdomains s and outer iterations n of n_s x PCG iterations (DOF x CG-iter)."""
+    lo, hi = rank * S // world, (rank + 1) * S // world
+    its = osm.inner_iters().astype(np.int64)
+    w = 0
+    for s in range(lo, hi):
+        if s not in _rows:
+            _rows[s] = osm.local_solution_size(s)
+        w += _rows[s] * int(np.clip(its[:, s], 0, None).sum())
+    return float(w)
+
+
+if __name__ == "__main__":
+    main()

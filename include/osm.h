@@ -193,6 +193,10 @@ osm_status osm_get_kernel_timing(osm_ctx* ctx, osm_kernel_time* out, int cap, in
  * entries, out[4] = structural nnz (local), out[5] = local rows. */
 osm_status osm_get_traffic_model(osm_ctx* ctx, double* out, int n);
 
+/* Number of this library's kernel launches on the context's stream since
+ * creation (every kernel of setup, solve and readback). */
+osm_status osm_get_launch_count(osm_ctx* ctx, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

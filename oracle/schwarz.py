@@ -38,12 +38,19 @@ class Problem:
     f: np.ndarray  # monolithic load
 
 
-def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None) -> Problem:
-    """Assemble every K_s^N, b_s, interface maps, M_Gamma and the monolithic K, f."""
+def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=None, monolithic=True) -> Problem:
+    """Assemble every K_s^N, b_s, interface maps, M_Gamma and the monolithic K, f.
+
+    ``only``: assemble just these subdomains (others are None); ``monolithic=False`` skips K, f
+    (used for bounded timing samples of large workloads).
+    """
     sls = slabs(box, nsub)
     full = slabs(box, 1)[0]
     subs = []
     for sl in sls:
+        if only is not None and sl.s not in only:
+            subs.append(Subdomain(sl, None, None, None))
+            continue
         KN = fe.assemble_stiffness(box, sl)
         if load_fn is not None:
             b = fe.assemble_load_function(box, sl, load_fn, quad)
@@ -56,6 +63,8 @@ def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None) -> Pr
         subs[i].right = l
         subs[i + 1].left = r
     MG = fe.interface_mass(box)
+    if not monolithic:
+        return Problem(box, nsub, subs, MG, None, None)
     K = fe.assemble_stiffness(box, full)
     f = fe.assemble_load_function(box, full, load_fn, quad) if load_fn is not None else fe.assemble_load(box, full, drho)
     return Problem(box, nsub, subs, MG, K, f)

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libosm.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"libosm.so not built ({LIB_PATH}); run `python -m paper_2112_03851_b200.build`")
+    raise ImportError(f"libosm.so not built ({LIB_PATH}); run `python paper_2112_03851_b200/build.py`")
 _lib = C.CDLL(LIB_PATH)
 
 OSM_OK, OSM_ERR_INVALID_ARG, OSM_ERR_GRID_TOO_SMALL, OSM_ERR_ILL_POSED, OSM_ERR_PRECOND = 0, 1, 2, 3, 4
@@ -29,7 +29,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_decompose", "osm_set_robin", "osm_assemble", "osm_upload_density", "osm_upload_density_device",
                "osm_solve", "osm_get_history", "osm_get_inner_iters", "osm_get_solution", "osm_get_local_solution",
                "osm_get_trace", "osm_get_csr", "osm_get_interface_map", "osm_get_interface_mass",
-               "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model"]
+               "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model", "osm_get_launch_count"]
 
 
 class MeshDesc(C.Structure):
@@ -84,6 +84,7 @@ _sigs = {
     "osm_set_kernel_timing": (C.c_int, [_P, C.c_int]),
     "osm_get_kernel_timing": (C.c_int, [_P, C.POINTER(KernelTime), C.c_int, _pint]),
     "osm_get_traffic_model": (C.c_int, [_P, _pd, C.c_int]),
+    "osm_get_launch_count": (C.c_int, [_P, _pi64]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -129,6 +130,7 @@ class Osm:
         _check(_lib.osm_create(C.byref(self.mesh), C.byref(dist), C.byref(h)))
         self._h = h
         self.order = order
+        self.rank = rank
         self.nsub = 0
         self.lattice = (order * nx + 1, order * ny + 1, order * nz + 1)
 
@@ -194,12 +196,23 @@ class Osm:
         _check(_lib.osm_get_inner_iters(self._h, _ptr(out, C.c_int32), n.value, C.byref(n)))
         return out
 
-    def solution(self):
-        n = C.c_int64(0)
-        _check(_lib.osm_get_solution(self._h, None, C.byref(n)))
-        out = np.zeros(n.value)
+    def solution(self, out=None):
+        """[collective] Phi on the full lattice, gathered to rank 0 (other ranks get None)."""
+        n = C.c_int64(int(np.prod(self.lattice)))
+        if self.rank != 0:
+            _check(_lib.osm_get_solution(self._h, None, C.byref(n)))
+            return None
+        if out is None:
+            out = np.zeros(n.value)
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size < n.value:
+            raise ValueError("out must be a contiguous float64 array of the lattice size")
         _check(_lib.osm_get_solution(self._h, _ptr(out, C.c_double), C.byref(n)))
         return out
+
+    def local_solution_size(self, s) -> int:
+        n = C.c_int64(0)
+        _check(_lib.osm_get_local_solution(self._h, s, None, C.byref(n)))
+        return n.value
 
     def local_solution(self, s):
         n = C.c_int64(0)
@@ -253,6 +266,11 @@ class Osm:
         _check(_lib.osm_get_kernel_timing(self._h, arr, n.value, C.byref(n)))
         return {a.name.decode(): (a.launches, a.total_ms) for a in arr}
 
+    def launch_count(self) -> int:
+        n = C.c_int64(0)
+        _check(_lib.osm_get_launch_count(self._h, C.byref(n)))
+        return n.value
+
     def traffic_model(self):
         out = np.zeros(6)
         _check(_lib.osm_get_traffic_model(self._h, _ptr(out, C.c_double), 6))
@@ -267,8 +285,12 @@ def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None
     o.decompose(cfg["nsub"])
     if cfg["nsub"] > 1:
         a = cfg.get("alpha") if alpha is None else alpha
-        al = np.full(cfg["nsub"] - 1, a) if np.isscalar(a) else np.asarray(a[0])
-        ar = np.full(cfg["nsub"] - 1, a) if np.isscalar(a) else np.asarray(a[1])
+        n = cfg["nsub"] - 1
+        if np.isscalar(a):
+            al = ar = np.full(n, float(a))
+        else:
+            al = np.broadcast_to(np.asarray(a[0], dtype=np.float64), (n,))
+            ar = np.broadcast_to(np.asarray(a[1], dtype=np.float64), (n,))
         o.set_robin(al, ar)
     o.assemble()
     o.upload_density(drho)

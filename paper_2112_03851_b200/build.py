@@ -1,6 +1,6 @@
 """Builds libosm.so in-tree with nvcc for sm_100a (no JIT cache; the .so travels with the repo snapshot).
 
-    python -m paper_2112_03851_b200.build [--verbose-ptxas]
+    python paper_2112_03851_b200/build.py [--verbose-ptxas] [--force]   (or __graft_entry__.build())
 """
 from __future__ import annotations
 

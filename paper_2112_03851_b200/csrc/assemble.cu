@@ -226,11 +226,13 @@ StencilDev tables_of(const Ctx& c) {
 void launch_count(const Ctx& c, const Sub& s, int32_t* rowlen) {
   k_assemble<false><<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), rowlen, nullptr, nullptr, nullptr);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_fill(const Ctx& c, const Sub& s) {
   k_assemble<true><<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), nullptr, s.rowptr, s.col, s.val);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_sell_build(const Ctx& c, const Sub& s, const int32_t*) {
@@ -238,6 +240,7 @@ void launch_sell_build(const Ctx& c, const Sub& s, const int32_t*) {
                                                       s.val, c.sell_soff, c.sell_swidth, c.sell_val, c.sell_col,
                                                       c.dinv, c.d_flags);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s) {
@@ -247,6 +250,7 @@ void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s) {
                                                     c.fold_pos, c.fold_m, c.fold_kn, c.fold_diag_row, c.fold_side,
                                                     c.d_flags);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_fold_apply(const Ctx& c, const double* d_alpha_side) {
@@ -254,21 +258,25 @@ void launch_fold_apply(const Ctx& c, const double* d_alpha_side) {
   k_fold_apply<<<grid_for(c.nfold), 256, 0, c.stream>>>(c.nfold, d_alpha_side, c.fold_pos, c.fold_m, c.fold_kn,
                                                        c.fold_diag_row, c.fold_side, c.sell_val, c.dinv, c.d_flags);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_load(const Ctx& c, const Sub& s, double fourpiG) {
   k_load<<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), c.drho, fourpiG, s.iperm, s.row0, c.b);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned) {
   k_scatter_phi<<<grid_for(s.npad), 256, 0, c.stream>>>(s.g, s.npad, s.row0, s.perm, c.ut, only_owned, c.phi);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract) {
   k_gather_local<<<grid_for(s.npad), 256, 0, c.stream>>>(s.npad, s.row0, s.perm, c.x, out_contract);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 }  // namespace osm

@@ -190,12 +190,20 @@ struct Ctx {
   std::vector<int32_t> inner;  // [outer][nsub]
   double fnorm2 = 0;
 
+  // CUDA graph of one chunk of PCG iterations (spmv, update, dir) x kCgChunk, with PDL edges
+  cudaGraphExec_t cg_graph = nullptr;
+  double graph_tol = -1;
+  int graph_maxit = -1;
+  bool use_graph = true;
+  int sigma = 8192;  // SELL sorting window
+
   // instrumentation
   bool timing = false;
   std::vector<KernelTimer> timers;
 
   // traffic model of the last solve
   double traffic[6] = {0};
+  mutable int64_t launches = 0;  // kernel launches issued by this context
 };
 
 // ---- launchers (assemble.cu)

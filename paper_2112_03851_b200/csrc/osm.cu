@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -78,7 +79,13 @@ static void timers_collect(Ctx& c) {
 }
 
 // ------------------------------------------------------------------ teardown
+static void drop_graph(Ctx& c) {
+  if (c.cg_graph) cudaGraphExecDestroy(c.cg_graph);
+  c.cg_graph = nullptr;
+}
+
 static void free_assembly(Ctx& c) {
+  drop_graph(c);
   for (auto& s : c.subs) {
     dfree(s.rowptr);
     dfree(s.col);
@@ -155,7 +162,6 @@ static SlabGeom slab_geom(const Ctx& c, int s) {
   return g;
 }
 
-static constexpr int kSigma = 1024;  // SELL sorting window (rows)
 
 static void assemble(Ctx& c) {
   free_assembly(c);
@@ -215,8 +221,9 @@ static void assemble(Ctx& c) {
     perm.assign(S.npad, -1);
     iperm.assign(S.n, -1);
     std::vector<int32_t> idx;
-    for (int64_t w0 = 0; w0 < S.n; w0 += kSigma) {
-      const int64_t w1 = std::min<int64_t>(S.n, w0 + kSigma);
+    const int64_t sigma = std::max(kRowsPerBlock, c.sigma);
+    for (int64_t w0 = 0; w0 < S.n; w0 += sigma) {
+      const int64_t w1 = std::min<int64_t>(S.n, w0 + sigma);
       idx.resize(w1 - w0);
       std::iota(idx.begin(), idx.end(), (int32_t)w0);
       std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
@@ -486,6 +493,53 @@ static double glued_residual2(Ctx& c, int zero, std::vector<int32_t>* iters_out)
 }
 
 // ------------------------------------------------------------------ solve
+static constexpr int kCgChunk = 8;  // PCG iterations per enqueued chunk
+
+// One chunk of kCgChunk batched PCG iterations: replayed from a CUDA graph (kernels
+// chained by programmatic dependent launch) unless per-launch timing is on.
+static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
+  if (c.timing || !c.use_graph) {
+    for (int it = 0; it < kCgChunk; ++it) {
+      launch_cg_spmv(c);
+      launch_cg_update(c, tol, maxit);
+      launch_cg_dir(c);
+    }
+    return;
+  }
+  if (!c.cg_graph || c.graph_tol != tol || c.graph_maxit != maxit) {
+    drop_graph(c);
+    const int64_t l0 = c.launches;
+    cudaGraph_t g = nullptr;
+    OSM_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int it = 0; it < kCgChunk; ++it) {
+        launch_cg_spmv(c);
+        launch_cg_update(c, tol, maxit);
+        launch_cg_dir(c);
+      }
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    OSM_CUDA(cudaStreamEndCapture(c.stream, &g));
+    const cudaError_t e = cudaGraphInstantiate(&c.cg_graph, g, 0);
+    cudaGraphDestroy(g);
+    c.launches = l0;
+    if (e != cudaSuccess) {  // graphs unavailable: plain stream launches (same kernels)
+      cudaGetLastError();
+      c.cg_graph = nullptr;
+      c.use_graph = false;
+      enqueue_cg_chunk(c, tol, maxit);
+      return;
+    }
+    c.graph_tol = tol;
+    c.graph_maxit = maxit;
+  }
+  OSM_CUDA(cudaGraphLaunch(c.cg_graph, c.stream));
+  c.launches += 3 * kCgChunk;
+}
+
 static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   if (!c.assembled) fail(OSM_ERR_STATE, "osm_assemble must precede osm_solve");
   if (!c.density_set) fail(OSM_ERR_STATE, "osm_upload_density must precede osm_solve");
@@ -507,7 +561,6 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   int grow = 0;
   int64_t inner_total = 0;
   int inner_maxed = 0;
-  constexpr int kChunk = 8;
   for (int n = 1; n <= o.max_outer; ++n) {
     if (!o.warm_start) OSM_CUDA(cudaMemsetAsync(c.x, 0, sizeof(double) * c.nrows_total, c.stream));
     OSM_CUDA(cudaMemsetAsync(c.d_nactive, 0, sizeof(int32_t), c.stream));
@@ -518,11 +571,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     if (c.h_nactive[0] > 0) {
       // batched masked PCG: enqueue chunks; poll the active count one chunk behind
       for (int ch = 0;; ++ch) {
-        for (int it = 0; it < kChunk; ++it) {
-          launch_cg_spmv(c);
-          launch_cg_update(c, o.tol_inner, o.max_inner);
-          launch_cg_dir(c);
-        }
+        enqueue_cg_chunk(c, o.tol_inner, o.max_inner);
         OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[ch & 1], c.d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c.stream));
         OSM_CUDA(cudaEventRecord(c.ev_chunk[ch & 1], c.stream));
@@ -530,7 +579,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
           OSM_CUDA(cudaEventSynchronize(c.ev_chunk[(ch - 1) & 1]));
           if (c.h_nactive[(ch - 1) & 1] == 0) break;
         }
-        if ((int64_t)ch * kChunk > (int64_t)o.max_inner + 2 * kChunk) break;  // safety net
+        if ((int64_t)ch * kCgChunk > (int64_t)o.max_inner + 2 * kCgChunk) break;  // safety net
       }
     }
     launch_trace(c);
@@ -670,6 +719,8 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     c.d_nactive = dalloc<int32_t>(1);
     OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[0], cudaEventDisableTiming));
     OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[1], cudaEventDisableTiming));
+    if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
+    if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
@@ -967,6 +1018,15 @@ osm_status osm_get_kernel_timing(osm_ctx* h, osm_kernel_time* out, int cap, int*
       out[i].launches = c.timers[i].launches;
       out[i].total_ms = c.timers[i].total_ms;
     }
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_launch_count(osm_ctx* h, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL output");
+  *n = c.launches;
   return OSM_OK;
   OSM_API_END
 }

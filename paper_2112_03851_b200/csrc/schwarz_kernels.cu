@@ -38,9 +38,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block sum of N values (256 threads, fixed order); result valid in thread 0.
-template <int N>
-__device__ __forceinline__ void block_sum(double (&v)[N], double* sm /* 8*N */) {
+// Block sum of N values over NW warps (fixed order); result valid in thread 0.
+template <int N, int NW = kSlicesPerBlock>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* sm /* NW*N */) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
@@ -53,7 +53,7 @@ __device__ __forceinline__ void block_sum(double (&v)[N], double* sm /* 8*N */) 
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = 0.0;
-      for (int w = 0; w < kSlicesPerBlock; ++w) s += sm[w * N + i];
+      for (int w = 0; w < NW; ++w) s += sm[w * N + i];
       v[i] = s;
     }
   }
@@ -77,7 +77,7 @@ __device__ __forceinline__ bool publish(const double (&v)[N], double* part, int6
 }
 
 // Fixed-order sum of one subdomain's block partials; result valid in thread 0.
-template <int N>
+template <int N, int NW = kSlicesPerBlock>
 __device__ __forceinline__ void gather_partials(double (&out)[N], const double* part, int64_t stride, int64_t blk0,
                                                 int nblk, double* sm) {
   __threadfence();
@@ -88,36 +88,60 @@ __device__ __forceinline__ void gather_partials(double (&out)[N], const double* 
     for (int i = 0; i < N; ++i) out[i] += __ldcg(part + i * stride + blk0 + k);
   }
   __syncthreads();
-  block_sum<N>(out, sm);
+  block_sum<N, NW>(out, sm);
+}
+
+// Programmatic dependent launch (sm_90+): wait for the producer grid, then let the
+// next kernel in the stream begin launching while this one runs.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // y_row = sum_j A[row, j] x[j] for the lane's row of a SELL-32 slice, entries in
-// column order (sequential per row, deterministic).
+// column order (sequential per row, deterministic).  Software-pipelined: the
+// value/column chunk k+1 is requested before the gathers of chunk k are consumed,
+// so every warp keeps two chunks of streaming loads in flight.  The slice width
+// is warp-uniform, so the tail predicates never diverge.
+template <int CH>
 __device__ __forceinline__ double sell_row(const SellDev& A, int64_t slice, int lane, const double* __restrict__ x) {
   const int w = A.swidth[slice];
   const int64_t base = A.soff[slice] + lane;
   const double* vp = A.val + base;
   const int32_t* cp = A.col + base;
   double s = 0.0;
-  int k = 0;
-  for (; k + 4 <= w; k += 4) {
-    const double v0 = ld_stream(vp), v1 = ld_stream(vp + 32), v2 = ld_stream(vp + 64), v3 = ld_stream(vp + 96);
-    const int32_t c0 = ld_stream(cp), c1 = ld_stream(cp + 32), c2 = ld_stream(cp + 64), c3 = ld_stream(cp + 96);
-    const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
-    s = fma(v0, x0, s);
-    s = fma(v1, x1, s);
-    s = fma(v2, x2, s);
-    s = fma(v3, x3, s);
-    vp += 128;
-    cp += 128;
+  double v[CH];
+  int32_t c[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    v[j] = j < w ? ld_stream(vp + 32 * j) : 0.0;
+    c[j] = j < w ? ld_stream(cp + 32 * j) : 0;
   }
-  for (; k < w; ++k) {
-    s = fma(ld_stream(vp), __ldg(x + ld_stream(cp)), s);
-    vp += 32;
-    cp += 32;
+  for (int k = 0; k < w; k += CH) {
+    double xv[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) xv[j] = (k + j < w) ? __ldg(x + c[j]) : 0.0;
+    double vn[CH];
+    int32_t cn[CH];
+    const int kn = k + CH;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      vn[j] = (kn + j < w) ? ld_stream(vp + 32 * (kn + j)) : 0.0;
+      cn[j] = (kn + j < w) ? ld_stream(cp + 32 * (kn + j)) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (k + j < w) s = fma(v[j], xv[j], s);
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      v[j] = vn[j];
+      c[j] = cn[j];
+    }
   }
   return s;
 }
+
+constexpr int kChunk = 4;
 
 // ---------------------------------------------------------------- PCG kernels
 
@@ -127,13 +151,14 @@ __global__ void __launch_bounds__(kThreads) k_cg_spmv(SellDev A, const int32_t* 
                                                       double* __restrict__ q, double* __restrict__ part,
                                                       int64_t stride, int32_t* __restrict__ nactive) {
   __shared__ double sm[kSlicesPerBlock * 1];
+  pdl_enter();
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   if (!st[ls].active) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = blk * kSlicesPerBlock + warp;
   const int64_t row = slice * kWarp + lane;
-  const double y = sell_row(A, slice, lane, p);
+  const double y = sell_row<kChunk>(A, slice, lane, p);
   q[row] = y;
   double v[1] = {p[row] * y};
   block_sum<1>(v, sm);
@@ -155,30 +180,40 @@ __global__ void __launch_bounds__(kThreads) k_cg_spmv(SellDev A, const int32_t* 
   }
 }
 
-// x += alpha p ; r -= alpha q ; z = D^{-1} r ; r.z, r.r ; stop test ||r|| <= tol ||rhs||; beta
-__global__ void __launch_bounds__(kThreads) k_cg_update(const int32_t* __restrict__ blk_sub, SubState* __restrict__ st,
-                                                        double* __restrict__ x, double* __restrict__ r,
-                                                        const double* __restrict__ p, const double* __restrict__ q,
-                                                        const double* __restrict__ dinv, double* __restrict__ part,
-                                                        int64_t stride, double tol, int maxit,
-                                                        int32_t* __restrict__ nactive) {
-  __shared__ double sm[kSlicesPerBlock * 2];
+// x += alpha p ; r -= alpha q ; z = D^{-1} r ; r.z, r.r ; stop test ||r|| <= tol ||rhs||; beta.
+// 128 threads x 2 rows (16-byte loads) per 256-row block.
+constexpr int kVecThreads = kRowsPerBlock / 2;
+__global__ void __launch_bounds__(kVecThreads) k_cg_update(const int32_t* __restrict__ blk_sub, SubState* __restrict__ st,
+                                                           double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ p, const double* __restrict__ q,
+                                                           const double* __restrict__ dinv, double* __restrict__ part,
+                                                           int64_t stride, double tol, int maxit,
+                                                           int32_t* __restrict__ nactive) {
+  __shared__ double sm[(kVecThreads / 32) * 2];
+  pdl_enter();
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   if (!st[ls].active) return;
-  const int64_t row = blk * kRowsPerBlock + threadIdx.x;
+  const int64_t i2 = blk * kVecThreads + threadIdx.x;  // index of the row pair
   const double a = st[ls].alpha;
-  const double xv = fma(a, p[row], x[row]);
-  const double rv = fma(-a, q[row], r[row]);
-  x[row] = xv;
-  r[row] = rv;
-  const double z = dinv[row] * rv;
-  double v[2] = {rv * z, rv * rv};
-  block_sum<2>(v, sm);
+  const double2 pv = reinterpret_cast<const double2*>(p)[i2];
+  const double2 qv = reinterpret_cast<const double2*>(q)[i2];
+  double2 xv = reinterpret_cast<const double2*>(x)[i2];
+  double2 rv = reinterpret_cast<const double2*>(r)[i2];
+  const double2 dv = reinterpret_cast<const double2*>(dinv)[i2];
+  xv.x = fma(a, pv.x, xv.x);
+  xv.y = fma(a, pv.y, xv.y);
+  rv.x = fma(-a, qv.x, rv.x);
+  rv.y = fma(-a, qv.y, rv.y);
+  reinterpret_cast<double2*>(x)[i2] = xv;
+  reinterpret_cast<double2*>(r)[i2] = rv;
+  const double z0 = dv.x * rv.x, z1 = dv.y * rv.y;
+  double v[2] = {rv.x * z0 + rv.y * z1, rv.x * rv.x + rv.y * rv.y};
+  block_sum<2, kVecThreads / 32>(v, sm);
   SubState& S = st[ls];
   if (publish<2>(v, part, stride, blk, &S.cnt, S.nblk)) {
     double t[2];
-    gather_partials<2>(t, part, stride, S.blk0, S.nblk, sm);
+    gather_partials<2, kVecThreads / 32>(t, part, stride, S.blk0, S.nblk, sm);
     if (threadIdx.x == 0) {
       S.cnt = 0;
       const double rz = t[0], rr = t[1];
@@ -200,15 +235,22 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(const int32_t* __restric
   }
 }
 
-// p = D^{-1} r + beta p
-__global__ void __launch_bounds__(kThreads) k_cg_dir(const int32_t* __restrict__ blk_sub,
-                                                     const SubState* __restrict__ st, const double* __restrict__ r,
-                                                     const double* __restrict__ dinv, double* __restrict__ p) {
+// p = D^{-1} r + beta p  (128 threads x 2 rows per 256-row block)
+__global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restrict__ blk_sub,
+                                                        const SubState* __restrict__ st, const double* __restrict__ r,
+                                                        const double* __restrict__ dinv, double* __restrict__ p) {
+  pdl_enter();
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   if (!st[ls].active) return;
-  const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  p[row] = fma(st[ls].beta, p[row], dinv[row] * r[row]);
+  const int64_t i2 = blk * kVecThreads + threadIdx.x;
+  const double beta = st[ls].beta;
+  const double2 rv = reinterpret_cast<const double2*>(r)[i2];
+  const double2 dv = reinterpret_cast<const double2*>(dinv)[i2];
+  double2 pv = reinterpret_cast<const double2*>(p)[i2];
+  pv.x = fma(beta, pv.x, dv.x * rv.x);
+  pv.y = fma(beta, pv.y, dv.y * rv.y);
+  reinterpret_cast<double2*>(p)[i2] = pv;
 }
 
 // Warm start: rhs = b + P^T lambda ; r = rhs - K_s x ; z = D^{-1} r ; p = z ;
@@ -226,7 +268,7 @@ __global__ void __launch_bounds__(kThreads) k_warm(SellDev A, const int32_t* __r
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = blk * kSlicesPerBlock + warp;
   const int64_t row = slice * kWarp + lane;
-  const double ax = sell_row(A, slice, lane, x);
+  const double ax = sell_row<kChunk>(A, slice, lane, x);
   const int sl = islot[row];
   const double rhs = sl >= 0 ? b[row] + lam_all[sl] : b[row];
   const double rv = rhs - ax;
@@ -318,7 +360,7 @@ __global__ void __launch_bounds__(kThreads) k_resid(SellDev A, const int32_t* __
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = blk * kSlicesPerBlock + warp;
   const int64_t row = slice * kWarp + lane;
-  const double w = b[row] - sell_row(A, slice, lane, ut);
+  const double w = b[row] - sell_row<kChunk>(A, slice, lane, ut);
   const int sl = islot[row];
   if (sl >= 0) wif_all[sl] = w;
   double v[1] = {sl == -1 ? w * w : 0.0};
@@ -382,34 +424,53 @@ void launch_warm(Ctx& c, double tol, int) {
   k_warm<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot, c.lam_all,
                                                             c.dinv, c.r, c.p, c.part, c.nblk_total, tol, c.d_nactive);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
   timer_end(c, T_WARM);
 }
 
 void launch_zero_if(Ctx& c) {
   k_zero_if<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(c.blk_sub, c.st, c.x);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsigned block, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
-  k_cg_spmv<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.p, c.q, c.part,
-                                                               c.nblk_total, c.d_nactive);
-  OSM_CHECK_LAUNCH();
+  launch_pdl(c, k_cg_spmv, (unsigned)c.nblk_total, kThreads, sell_of(c), (const int32_t*)c.blk_sub, c.st,
+             (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
+  ++c.launches;
   timer_end(c, T_SPMV);
 }
 
 void launch_cg_update(Ctx& c, double tol, int maxit) {
   timer_begin(c, T_UPDATE);
-  k_cg_update<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(c.blk_sub, c.st, c.x, c.r, c.p, c.q, c.dinv, c.part,
-                                                                 c.nblk_total, tol, maxit, c.d_nactive);
-  OSM_CHECK_LAUNCH();
+  launch_pdl(c, k_cg_update, (unsigned)c.nblk_total, kVecThreads, (const int32_t*)c.blk_sub, c.st, c.x, c.r,
+             (const double*)c.p, (const double*)c.q, (const double*)c.dinv, c.part, c.nblk_total, tol, maxit,
+             c.d_nactive);
+  ++c.launches;
   timer_end(c, T_UPDATE);
 }
 
 void launch_cg_dir(Ctx& c) {
   timer_begin(c, T_DIR);
-  k_cg_dir<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(c.blk_sub, c.st, c.r, c.dinv, c.p);
-  OSM_CHECK_LAUNCH();
+  launch_pdl(c, k_cg_dir, (unsigned)c.nblk_total, kVecThreads, (const int32_t*)c.blk_sub, (const SubState*)c.st,
+             (const double*)c.r, (const double*)c.dinv, c.p);
+  ++c.launches;
   timer_end(c, T_DIR);
 }
 
@@ -418,6 +479,7 @@ void launch_trace(Ctx& c) {
   dim3 grid((unsigned)ceil_div(c.nG, 256), (unsigned)c.sides.size());
   k_trace<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG, c.d_mrow, c.d_mcol, c.d_mval, c.x);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_accept(Ctx& c) {
@@ -425,12 +487,14 @@ void launch_accept(Ctx& c) {
   dim3 grid((unsigned)ceil_div(c.nG, 256), (unsigned)c.sides.size());
   k_accept<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_glue(Ctx& c, int zero) {
   k_glue<<<(unsigned)ceil_div(c.nrows_total, 256), 256, 0, c.stream>>>(c.nrows_total, c.islot, c.x, c.unbr_all, zero,
                                                                          c.ut);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_resid(Ctx& c) {
@@ -438,6 +502,7 @@ void launch_resid(Ctx& c) {
   k_resid<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot,
                                                              c.wif_all, c.part, c.nblk_total);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
   timer_end(c, T_RESID);
 }
 
@@ -446,6 +511,7 @@ void launch_iface_w(Ctx& c) {
   dim3 grid((unsigned)ceil_div(c.nG, 256), (unsigned)c.sides.size());
   k_iface_w<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG, c.d_mrow, c.d_mcol, c.d_mval, c.ut);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 void launch_iface_sum(Ctx& c) {
@@ -453,6 +519,7 @@ void launch_iface_sum(Ctx& c) {
   dim3 grid((unsigned)c.side_nblk, (unsigned)c.sides.size());
   k_iface_sum<<<grid, kThreads, 0, c.stream>>>(c.d_sides, c.nG, c.side_part, c.side_nblk, c.side_cnt, c.side_sum);
   OSM_CHECK_LAUNCH();
+  ++c.launches;
 }
 
 }  // namespace osm

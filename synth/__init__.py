@@ -82,11 +82,22 @@ def alpha_candidates(alpha0: float, B: int = 64, seed: int = 2112):
 CONFIGS = {
     "C1": dict(nx=8, ny=8, nz=8, lx=1.0, ly=1.0, lz=1.0, order=1, nsub=2, field="ball", alpha=20.0),
     "C2": dict(nx=32, ny=32, nz=32, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=2, field="ball", alpha=56.0),
+    # C3 alpha: two-sided OO0 (Table 1 'oo0_unsymmetric' form), (alpha_1, alpha_2) in 1/m,
+    # frozen from the GPU alpha scans in profiles/alpha_scan_C3.md (best: 159 outer iterations to 1e-8).
     "C3": dict(nx=64, ny=64, nz=64, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
-               order=2, nsub=8, field="chicxulub", alpha=None),
+               order=2, nsub=8, field="chicxulub", alpha=(0.1, 5.0e-4)),
     "C5": dict(nx=192, ny=192, nz=192, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
                order=2, nsub=8, field="chicxulub", alpha=None),
 }
+
+
+def alphas(cfg: dict, alpha=None):
+    """(alpha_left[nsub-1], alpha_right[nsub-1]) from a scalar or an (alpha_1, alpha_2) pair."""
+    a = cfg.get("alpha") if alpha is None else alpha
+    n = max(cfg["nsub"] - 1, 0)
+    if np.isscalar(a):
+        return np.full(n, float(a)), np.full(n, float(a))
+    return np.full(n, float(a[0])), np.full(n, float(a[1]))
 
 
 def density(cfg: dict, seed: int = 0):

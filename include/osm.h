@@ -152,6 +152,29 @@ osm_status osm_upload_density_device(osm_ctx* ctx, const double* drho_dev, doubl
  * NOT_CONVERGED (max_outer reached), DIVERGED, or an error.  report may be NULL. */
 osm_status osm_solve(osm_ctx* ctx, const osm_solve_opts* opts, osm_report* report);
 
+/* Batched-alpha solve (BASELINE config C4): B <= 64 candidate Robin
+ * parameter sets solved simultaneously, sharing K_s^N (each matrix entry is read once per
+ * batched PCG iteration for all candidates; alpha_b M_Gamma is applied on the fly).
+ * alphas: host array [b][side][iface], i.e. alphas[(b*2 + side)*(nsub-1) + i], side 0 =
+ * the slab left of interface i.  Every candidate runs exactly the osm_solve iteration and
+ * stops at its own h_b(n) <= tol_outer or max_outer (PAPER.md:95 population of 25 fits).
+ * Single rank only (INVALID_ARG otherwise).  ILL_POSED as osm_set_robin. */
+typedef struct osm_batch_report {
+  int B;               /* candidates */
+  int outer_max;       /* largest outer count over candidates */
+  int n_converged;     /* candidates with h_b <= tol_outer */
+  int64_t inner_total; /* PCG iterations summed over candidates, outer iterations, subdomains */
+  double seconds;
+} osm_batch_report;
+osm_status osm_solve_batch(osm_ctx* ctx, int B, const double* alphas, const osm_solve_opts* opts,
+                           osm_batch_report* report);
+/* h_b(1..N_b) of candidate b of the last batched solve.  h == NULL: *n = N_b. */
+osm_status osm_get_batch_history(osm_ctx* ctx, int b, double* h, int cap, int* n);
+/* PCG iterations [n][s] (local subdomains) of candidate b.  its == NULL: *n = N_b * nsub_local. */
+osm_status osm_get_batch_inner_iters(osm_ctx* ctx, int b, int32_t* its, int cap, int* n);
+/* Candidate b's final u_s (contract order, host).  u == NULL: *n = n_s. */
+osm_status osm_get_batch_local_solution(osm_ctx* ctx, int b, int s, double* u, int64_t* n);
+
 /* h(1..N) of the last solve (every rank holds it).  h == NULL: *n = N. */
 osm_status osm_get_history(osm_ctx* ctx, double* h, int cap, int* n);
 /* PCG iterations its[n*nsub + s] of the last solve, for the subdomains of this

@@ -29,7 +29,8 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_decompose", "osm_set_robin", "osm_assemble", "osm_upload_density", "osm_upload_density_device",
                "osm_solve", "osm_get_history", "osm_get_inner_iters", "osm_get_solution", "osm_get_local_solution",
                "osm_get_trace", "osm_get_csr", "osm_get_interface_map", "osm_get_interface_mass",
-               "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model", "osm_get_launch_count"]
+               "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model", "osm_get_launch_count", "osm_solve_batch",
+               "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution"]
 
 
 class MeshDesc(C.Structure):
@@ -50,6 +51,11 @@ class SolveOpts(C.Structure):
 class Report(C.Structure):
     _fields_ = [("outer_iters", C.c_int), ("converged", C.c_int), ("h_final", C.c_double), ("seconds", C.c_double),
                 ("inner_total", C.c_int64), ("inner_maxed", C.c_int)]
+
+
+class BatchReport(C.Structure):
+    _fields_ = [("B", C.c_int), ("outer_max", C.c_int), ("n_converged", C.c_int), ("inner_total", C.c_int64),
+                ("seconds", C.c_double)]
 
 
 class KernelTime(C.Structure):
@@ -85,6 +91,10 @@ _sigs = {
     "osm_get_kernel_timing": (C.c_int, [_P, C.POINTER(KernelTime), C.c_int, _pint]),
     "osm_get_traffic_model": (C.c_int, [_P, _pd, C.c_int]),
     "osm_get_launch_count": (C.c_int, [_P, _pi64]),
+    "osm_solve_batch": (C.c_int, [_P, C.c_int, _pd, C.POINTER(SolveOpts), C.POINTER(BatchReport)]),
+    "osm_get_batch_history": (C.c_int, [_P, C.c_int, _pd, C.c_int, _pint]),
+    "osm_get_batch_inner_iters": (C.c_int, [_P, C.c_int, _pi32, C.c_int, _pint]),
+    "osm_get_batch_local_solution": (C.c_int, [_P, C.c_int, C.c_int, _pd, _pi64]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -180,6 +190,39 @@ class Osm:
         st = _check(_lib.osm_solve(self._h, C.byref(opts), C.byref(rep)),
                     ok=(OSM_OK, OSM_NOT_CONVERGED, OSM_ERR_DIVERGED))
         return st, rep
+
+    def solve_batch(self, alpha_left, alpha_right, tol_outer=1e-8, max_outer=500, tol_inner=1e-10, max_inner=20000,
+                    warm_start=True):
+        """Batched-alpha solve: alpha_left/right are (B, nsub-1) arrays.  Returns the report."""
+        al = np.atleast_2d(np.asarray(alpha_left, dtype=np.float64))
+        ar = np.atleast_2d(np.asarray(alpha_right, dtype=np.float64))
+        B = al.shape[0]
+        a = np.ascontiguousarray(np.stack([al, ar], axis=1))  # [b][side][iface]
+        opts = SolveOpts(tol_outer, max_outer, tol_inner, max_inner, int(warm_start), 0)
+        rep = BatchReport()
+        _check(_lib.osm_solve_batch(self._h, B, _ptr(a, C.c_double), C.byref(opts), C.byref(rep)))
+        return rep
+
+    def batch_history(self, b):
+        n = C.c_int()
+        _check(_lib.osm_get_batch_history(self._h, b, None, 0, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(_lib.osm_get_batch_history(self._h, b, _ptr(out, C.c_double), n.value, C.byref(n)))
+        return out
+
+    def batch_inner_iters(self, b):
+        n = C.c_int()
+        _check(_lib.osm_get_batch_inner_iters(self._h, b, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int32)
+        _check(_lib.osm_get_batch_inner_iters(self._h, b, _ptr(out, C.c_int32), n.value, C.byref(n)))
+        return out.reshape(-1, self.nsub)
+
+    def batch_local_solution(self, b, s):
+        n = C.c_int64(0)
+        _check(_lib.osm_get_batch_local_solution(self._h, b, s, None, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(_lib.osm_get_batch_local_solution(self._h, b, s, _ptr(out, C.c_double), C.byref(n)))
+        return out
 
     # -- readback
     def history(self):

@@ -110,6 +110,8 @@ struct KernelTimer {
   int64_t launches = 0;
 };
 
+struct BatchBuf;
+
 struct Ctx {
   // configuration
   osm_mesh_desc mesh{};
@@ -201,6 +203,11 @@ struct Ctx {
   bool timing = false;
   std::vector<KernelTimer> timers;
 
+  // batched-alpha solver (batch.cu), built lazily on the first osm_solve_batch
+  BatchBuf* batch = nullptr;
+  int64_t* batch_sub_blk0 = nullptr;
+  int32_t* batch_sub_nblk = nullptr;
+
   // traffic model of the last solve
   double traffic[6] = {0};
   mutable int64_t launches = 0;  // kernel launches issued by this context
@@ -228,6 +235,14 @@ void launch_glue(Ctx& c, int zero);
 void launch_resid(Ctx& c);
 void launch_iface_w(Ctx& c);
 void launch_iface_sum(Ctx& c);
+
+// ---- batched alpha (batch.cu)
+osm_status solve_batch(Ctx& c, int B, const double* alphas, const osm_solve_opts& o, osm_batch_report* rep);
+void batch_history(const Ctx& c, int b, double* h, int cap, int* n);
+void batch_inner(const Ctx& c, int b, int32_t* its, int cap, int* n);
+void batch_local_solution(Ctx& c, int b, int s, double* u, int64_t* n);
+void batch_free(Ctx& c);
+double fnorm2_of(Ctx& c);  // ||f||^2 of the glued global system (osm.cu)
 
 // timing helpers (osm.cu)
 void timer_begin(Ctx& c, int id);

@@ -86,6 +86,7 @@ static void drop_graph(Ctx& c) {
 
 static void free_assembly(Ctx& c) {
   drop_graph(c);
+  batch_free(c);
   for (auto& s : c.subs) {
     dfree(s.rowptr);
     dfree(s.col);
@@ -491,6 +492,8 @@ static double glued_residual2(Ctx& c, int zero, std::vector<int32_t>* iters_out)
   }
   return tot;
 }
+
+double fnorm2_of(Ctx& c) { return glued_residual2(c, 1, nullptr); }
 
 // ------------------------------------------------------------------ solve
 static constexpr int kCgChunk = 8;  // PCG iterations per enqueued chunk
@@ -1018,6 +1021,41 @@ osm_status osm_get_kernel_timing(osm_ctx* h, osm_kernel_time* out, int cap, int*
       out[i].launches = c.timers[i].launches;
       out[i].total_ms = c.timers[i].total_ms;
     }
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_solve_batch(osm_ctx* h, int B, const double* alphas, const osm_solve_opts* o, osm_batch_report* rep) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!o) fail(OSM_ERR_INVALID_ARG, "NULL options");
+  return solve_batch(c, B, alphas, *o, rep);
+  OSM_API_END
+}
+
+osm_status osm_get_batch_history(osm_ctx* h, int b, double* hist, int cap, int* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  batch_history(c, b, hist, cap, n);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_batch_inner_iters(osm_ctx* h, int b, int32_t* its, int cap, int* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  batch_inner(c, b, its, cap, n);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  batch_local_solution(c, b, s, u, n);
   return OSM_OK;
   OSM_API_END
 }

@@ -1,0 +1,82 @@
+"""Batched-alpha solve vs the oracle and vs the single-candidate CUDA path.
+
+Every candidate must follow exactly the single-candidate iteration: same parity bars as
+tests/test_gpu_parity.py (history 1e-8 h + 1e-14, u_s 1e-10 relative), and the inner PCG
+counts must equal the oracle's.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import mesh, schwarz
+
+from parity_util import history_ok, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+CFG = dict(nx=6, ny=5, nz=4, lx=1.0, ly=0.8, lz=0.6, order=2, nsub=3)
+CANDS = [(20.0, 20.0), (40.0, 8.0), (5.0, 60.0), (15.0, 15.0), (80.0, 2.0)]
+
+
+@pytest.fixture(scope="module")
+def run():
+    import paper_2112_03851_b200 as P
+
+    drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=21)
+    o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+    o.decompose(CFG["nsub"])
+    o.set_robin(np.full(2, 20.0), np.full(2, 20.0))
+    o.assemble()
+    o.upload_density(drho)
+    al = np.array([[a, a] for a, _ in CANDS])
+    ar = np.array([[b, b] for _, b in CANDS])
+    rep = o.solve_batch(al, ar, tol_outer=1e-8, max_outer=400)
+    box = mesh.Box(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+    prob = schwarz.build_problem(box, CFG["nsub"], drho=drho)
+    yield o, rep, prob, drho
+    o.close()
+
+
+@pytest.mark.parametrize("b", range(len(CANDS)))
+def test_candidate_matches_oracle(run, b):
+    o, rep, prob, _ = run
+    a1, a2 = CANDS[b]
+    orep = schwarz.schwarz(prob, schwarz.robin_operators(prob, [a1, a1], [a2, a2]), tol_outer=1e-8, max_outer=400)
+    h = o.batch_history(b)
+    ok, d = history_ok(h, orep.h)
+    assert ok, d.max()
+    assert len(h) == len(orep.h)
+    its = o.batch_inner_iters(b)
+    assert np.abs(its - np.array(orep.inner)).max() <= 1
+    for s in range(CFG["nsub"]):
+        assert rel_l2(o.batch_local_solution(b, s), orep.u[s]) <= 1e-10
+
+
+def test_candidate_matches_single_path(run):
+    o, rep, prob, _ = run
+    assert rep.B == len(CANDS) and rep.n_converged == len(CANDS)
+    for b in (0, 2):
+        a1, a2 = CANDS[b]
+        o.set_robin(np.full(2, a1), np.full(2, a2))
+        st, _ = o.solve(tol_outer=1e-8, max_outer=400)
+        h1 = o.history()
+        hb = o.batch_history(b)
+        assert len(h1) == len(hb)
+        assert np.all(np.abs(h1 - hb) <= 1e-8 * h1 + 1e-14)
+        for s in range(CFG["nsub"]):
+            assert rel_l2(o.batch_local_solution(b, s), o.local_solution(s)) <= 1e-12
+
+
+def test_batch_errors():
+    import paper_2112_03851_b200 as P
+
+    o = P.Osm(4, 4, 4, 1, 1, 1, 1)
+    o.decompose(2)
+    o.set_robin([10.0], [10.0])
+    o.assemble()
+    o.upload_density(np.ones(64))
+    with pytest.raises(P.OsmError):
+        o.solve_batch(np.zeros((2, 1)), np.zeros((2, 1)))  # alpha = 0 on both sides: ILL_POSED
+    with pytest.raises(P.OsmError):
+        o.solve_batch(np.ones((65, 1)), np.ones((65, 1)))  # B > 64
+    o.close()

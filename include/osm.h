@@ -216,6 +216,23 @@ osm_status osm_get_kernel_timing(osm_ctx* ctx, osm_kernel_time* out, int cap, in
  * entries, out[4] = structural nnz (local), out[5] = local rows. */
 osm_status osm_get_traffic_model(osm_ctx* ctx, double* out, int n);
 
+/* Host-only distribution plan (no GPU needed): subdomains [s_begin, s_end) of `rank`, and
+ * its interface sides in the order the library uses them.  Per Schwarz iteration the
+ * library exchanges, for every remote side: [g | u] (2 n_Gamma doubles) both ways with
+ * `peer`; then the right slab of the interface (side 1) sends its interface-row
+ * residual (n_Gamma doubles) to the left slab (side 0), which owns those rows of h(n);
+ * then an allgather of one residual partial per subdomain (summed in subdomain order).
+ * n_Gamma = (o ny - 1)(o nz - 1).  INVALID_ARG as osm_decompose. */
+typedef struct osm_plan_side {
+  int iface;  /* interface i, between slabs i and i+1 */
+  int side;   /* 0: owner slab is the left slab (its right plane), 1: the right slab */
+  int sub;    /* owning subdomain */
+  int remote; /* neighbour slab on another rank */
+  int peer;   /* rank of the neighbour slab */
+} osm_plan_side;
+osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, int* s_end, osm_plan_side* sides,
+                    int cap, int* nsides);
+
 /* Number of this library's kernel launches on the context's stream since
  * creation (every kernel of setup, solve and readback). */
 osm_status osm_get_launch_count(osm_ctx* ctx, int64_t* n);

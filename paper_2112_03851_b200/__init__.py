@@ -30,7 +30,8 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_solve", "osm_get_history", "osm_get_inner_iters", "osm_get_solution", "osm_get_local_solution",
                "osm_get_trace", "osm_get_csr", "osm_get_interface_map", "osm_get_interface_mass",
                "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model", "osm_get_launch_count", "osm_solve_batch",
-               "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution"]
+               "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
+               "osm_plan"]
 
 
 class MeshDesc(C.Structure):
@@ -51,6 +52,10 @@ class SolveOpts(C.Structure):
 class Report(C.Structure):
     _fields_ = [("outer_iters", C.c_int), ("converged", C.c_int), ("h_final", C.c_double), ("seconds", C.c_double),
                 ("inner_total", C.c_int64), ("inner_maxed", C.c_int)]
+
+
+class PlanSide(C.Structure):
+    _fields_ = [("iface", C.c_int), ("side", C.c_int), ("sub", C.c_int), ("remote", C.c_int), ("peer", C.c_int)]
 
 
 class BatchReport(C.Structure):
@@ -95,6 +100,7 @@ _sigs = {
     "osm_get_batch_history": (C.c_int, [_P, C.c_int, _pd, C.c_int, _pint]),
     "osm_get_batch_inner_iters": (C.c_int, [_P, C.c_int, _pi32, C.c_int, _pint]),
     "osm_get_batch_local_solution": (C.c_int, [_P, C.c_int, C.c_int, _pd, _pi64]),
+    "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -116,6 +122,16 @@ def _check(st, ok=(OSM_OK,)):
 
 def _ptr(a, ct):
     return a.ctypes.data_as(C.POINTER(ct))
+
+
+def plan(nx, nsub, nranks, rank):
+    """Host-only distribution plan: (s_begin, s_end, [dict(iface, side, sub, remote, peer), ...])."""
+    sb, se, n = C.c_int(), C.c_int(), C.c_int()
+    _check(_lib.osm_plan(nx, nsub, nranks, rank, C.byref(sb), C.byref(se), None, 0, C.byref(n)))
+    arr = (PlanSide * max(1, n.value))()
+    _check(_lib.osm_plan(nx, nsub, nranks, rank, C.byref(sb), C.byref(se), arr, n.value, C.byref(n)))
+    return sb.value, se.value, [dict(iface=a.iface, side=a.side, sub=a.sub, remote=a.remote, peer=a.peer)
+                                for a in arr[:n.value]]
 
 
 def abi_version():

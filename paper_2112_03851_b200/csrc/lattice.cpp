@@ -345,6 +345,25 @@ void interface_mass(int order, int64_t ny, int64_t nz, double hy, double hz, std
   for (int64_t r = 0; r < n; ++r) rowptr[r + 1] += rowptr[r];
 }
 
+void plan_rank(int nsub, int nranks, int rank, int& s_begin, int& s_end, std::vector<PlanSide>& sides) {
+  s_begin = (int)((int64_t)rank * nsub / nranks);
+  s_end = (int)((int64_t)(rank + 1) * nsub / nranks);
+  sides.clear();
+  for (int s = s_begin; s < s_end; ++s)
+    for (int plane = 0; plane < 2; ++plane) {  // 0: left plane, 1: right plane
+      const bool has = plane == 0 ? s > 0 : s < nsub - 1;
+      if (!has) continue;
+      const int nbr = plane == 0 ? s - 1 : s + 1;
+      PlanSide p;
+      p.iface = plane == 0 ? s - 1 : s;
+      p.which = plane == 0 ? 1 : 0;
+      p.sub = s;
+      p.remote = !(nbr >= s_begin && nbr < s_end);
+      p.peer = (int)((int64_t)nbr * nranks / nsub);
+      sides.push_back(p);
+    }
+}
+
 std::vector<int64_t> partition_x(int64_t nx, int nsub) {
   std::vector<int64_t> c(nsub + 1, 0);
   int64_t base = nx / nsub, rem = nx % nsub;

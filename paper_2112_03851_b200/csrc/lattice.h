@@ -61,4 +61,15 @@ void interface_mass(int order, int64_t ny, int64_t nz, double hy, double hz, std
 // Cell starts c_0..c_S of the x-slabs (widths differ by <= 1, remainder to the left).
 std::vector<int64_t> partition_x(int64_t nx, int nsub);
 
+// Distribution plan of one rank (host only, no CUDA): subdomain s goes to rank
+// floor(s * nranks / nsub); every slab plane that touches another slab is a "side".
+struct PlanSide {
+  int iface;   // interface index i (between slabs i and i+1)
+  int which;   // 0: this slab is the left slab of the interface (its right plane), 1: the right slab
+  int sub;     // global subdomain id owning the side
+  int remote;  // neighbour on another rank
+  int peer;    // rank of the neighbour slab
+};
+void plan_rank(int nsub, int nranks, int rank, int& s_begin, int& s_end, std::vector<PlanSide>& sides);
+
 }  // namespace osm

@@ -282,18 +282,20 @@ static void assemble(Ctx& c) {
     const Sub& S = c.subs[ls];
     for (int64_t k = S.n; k < S.npad; ++k) islot[S.row0 + k] = -2;
   }
-  for (int ls = 0; ls < nloc; ++ls) {
-    Sub& S = c.subs[ls];
-    for (int which_plane = 0; which_plane < 2; ++which_plane) {  // 0: left plane, 1: right plane
-      const bool has = which_plane == 0 ? S.s > 0 : S.s < c.nsub - 1;
-      if (!has) continue;
+  {
+    int sb, se;
+    std::vector<PlanSide> plan;
+    plan_rank(c.nsub, c.nranks, c.rank, sb, se, plan);
+    for (const PlanSide& ps : plan) {
+      const int ls = ps.sub - c.s_begin;
+      Sub& S = c.subs[ls];
+      const int which_plane = ps.which == 1 ? 0 : 1;  // the right slab of an interface owns its left plane
       Side sd;
       sd.sub = ls;
-      sd.iface = which_plane == 0 ? S.s - 1 : S.s;
-      sd.which = which_plane == 0 ? 1 : 0;  // a left plane means this slab is the right slab of the interface
-      const int nbr = which_plane == 0 ? S.s - 1 : S.s + 1;
-      sd.remote = !(nbr >= c.s_begin && nbr < c.s_end);
-      sd.peer = (int)((int64_t)nbr * c.nranks / c.nsub);
+      sd.iface = ps.iface;
+      sd.which = ps.which;
+      sd.remote = ps.remote != 0;
+      sd.peer = ps.peer;
       const int64_t I = which_plane == 0 ? (int64_t)o * S.g.c0 : (int64_t)o * S.g.c1;
       std::vector<int32_t> mc(nG), mg(nG);
       const int k = (int)c.sides.size();
@@ -773,8 +775,10 @@ osm_status osm_decompose(osm_ctx* h, int nsub) {
   free_assembly(c);
   c.nsub = nsub;
   c.cstart = partition_x(c.mesh.nx, nsub);
-  c.s_begin = (int)((int64_t)c.rank * nsub / c.nranks);
-  c.s_end = (int)((int64_t)(c.rank + 1) * nsub / c.nranks);
+  {
+    std::vector<PlanSide> plan;
+    plan_rank(nsub, c.nranks, c.rank, c.s_begin, c.s_end, plan);
+  }
   c.robin_set = nsub == 1;
   c.alpha_left.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
   c.alpha_right.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
@@ -1020,6 +1024,27 @@ osm_status osm_get_kernel_timing(osm_ctx* h, osm_kernel_time* out, int cap, int*
       std::strncpy(out[i].name, c.timers[i].name.c_str(), sizeof(out[i].name) - 1);
       out[i].launches = c.timers[i].launches;
       out[i].total_ms = c.timers[i].total_ms;
+    }
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, int* s_end, osm_plan_side* sides,
+                     int cap, int* nsides) {
+  OSM_API_BEGIN
+  if (!s_begin || !s_end || !nsides) fail(OSM_ERR_INVALID_ARG, "NULL output");
+  if (nranks < 1 || rank < 0 || rank >= nranks || nsub < 1 || nsub > nx || nsub % nranks != 0)
+    fail(OSM_ERR_INVALID_ARG, "need 1 <= nsub <= nx, nsub % nranks == 0, 0 <= rank < nranks");
+  std::vector<PlanSide> plan;
+  plan_rank(nsub, nranks, rank, *s_begin, *s_end, plan);
+  *nsides = (int)plan.size();
+  if (sides)
+    for (int k = 0; k < std::min(cap, *nsides); ++k) {
+      sides[k].iface = plan[k].iface;
+      sides[k].side = plan[k].which;
+      sides[k].sub = plan[k].sub;
+      sides[k].remote = plan[k].remote;
+      sides[k].peer = plan[k].peer;
     }
   return OSM_OK;
   OSM_API_END

@@ -7,7 +7,10 @@ One "step" = one full Schwarz solve to h <= 1e-8 (every row of SURVEY 8(a): load
 update from the resident density, warm-start residuals, batched PCG to 1e-10,
 Robin traces, exchange, glued residual) on the BASELINE config C3 (P2, 64^3
 cells on the paper's 250 x 250 x 15 km box, Chicxulub-like density, 8 x-slab
-subdomains).  value = DOF_global x outer iterations / second (whole job).
+subdomains, two-sided OO2 transmission).  value = DOF x PCG iterations / second
+summed over subdomains (SURVEY 8(d) DOF.iter/s form (ii): the throughput of the
+hot loop, whole job); time_to_tol_s and DOF x outer-iterations / s (form (i)) are
+reported beside it.
 For N > 1 launch with torchrun (one rank per GPU, NCCL); the 8 subdomains are
 split over the ranks (strong scaling at fixed S).
 """
@@ -29,7 +32,7 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
-UNIT = "DOF*iter/s"
+UNIT = "DOF*CG-iter/s"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
@@ -88,12 +91,12 @@ class ClockSampler(threading.Thread):
 
 
 # ----------------------------------------------------------------------------- oracle sample (CPU)
-def oracle_sample(cfg, drho, alpha, iters):
+def oracle_sample(cfg, drho, iters):
     """Times the CPU oracle (oracle/, as it stands) on a bounded sample of the workload.
 
     Sample: `iters` Jacobi-PCG iterations of the oracle on interior subdomain 1 (Robin-augmented
-    K_1, cold start, rhs = b_1), single thread.  Returns (seconds per CG iteration, rows of the slab,
-    threads used).  Assembly of the sample is not timed.
+    K_1 of the config's transmission, cold start, rhs = b_1), single thread.  Returns (seconds per
+    CG iteration, rows of the slab, threads used).  Assembly of the sample is not timed.
     """
     from threadpoolctl import threadpool_limits
 
@@ -102,8 +105,8 @@ def oracle_sample(cfg, drho, alpha, iters):
     box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
     s = 1 if cfg["nsub"] > 2 else 0
     prob = schwarz.build_problem(box, cfg["nsub"], drho=drho, only=[s], monolithic=False)
-    al, ar = synth.alphas(cfg, alpha)
-    A = schwarz.robin_operators(prob, al, ar)
+    pl, ql, pr, qr = synth.robin(cfg)
+    A = schwarz.robin_operators(prob, pl, pr, ql, qr)
     Ks = schwarz.subdomain_operator(prob, s, A)
     b = prob.subs[s].b
     with threadpool_limits(limits=1):
@@ -115,28 +118,22 @@ def oracle_sample(cfg, drho, alpha, iters):
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, cfg, drho, rank):
+    """Reference arm: the CPU oracle as it stands, one host core, bounded sample per step."""
     if rank != 0:
         return
-    fz = cfg.get("frozen")
-    if not fz:
-        print(json.dumps({"impl": "reference", "unavailable": f"no frozen iteration counts for {args.config}"}))
-        return
     vals = []
-    sample_iters = args.ref_iters
     for k in range(args.warmup + args.steps):
-        t_iter, n_s, cores = oracle_sample(cfg, drho, cfg["alpha"], sample_iters)
-        t_solve = t_iter / n_s * fz["cg_work"]  # CG time of the whole solve, scaled by DOF x CG-iterations
-        v = cfg["dof"] * fz["outer"] / t_solve
+        t_iter, n_s, cores = oracle_sample(cfg, drho, args.ref_iters)
         if k >= args.warmup:
-            vals.append((v, t_solve))
+            vals.append((n_s / t_iter, t_iter))
     v = statistics.median([a for a, _ in vals])
     t = statistics.median([b for _, b in vals])
-    sample = (f"{sample_iters} oracle Jacobi-PCG iterations on subdomain 1 of {args.config} (scipy CSR, 1 thread), "
-              f"extrapolated by the workload's DOF x CG-iteration count {fz['cg_work']:.4g} and {fz['outer']} outer "
-              f"iterations (identical in oracle and GPU path, tests/test_gpu_parity.py); glued-residual SpMVs not timed")
+    sample = (f"{args.ref_iters} oracle Jacobi-PCG iterations on subdomain 1 of {args.config} (scipy CSR, 1 thread) "
+              f"per step; DOF x CG-iterations / s measured directly")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
+            "warmup": args.warmup, "ms_per_step": t * args.ref_iters * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, cfg),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -146,7 +143,10 @@ def config_block(args, cfg):
     return {"workload": f"{args.config}: P{cfg['order']} {cfg['nx']}x{cfg['ny']}x{cfg['nz']} Kuhn box "
                         f"{cfg['lx']/1e3:g}x{cfg['ly']/1e3:g}x{cfg['lz']/1e3:g} km, {cfg['field']} density, "
                         f"{cfg['nsub']} x-slab subdomains",
-            "dof": cfg["dof"], "nsub": cfg["nsub"], "alpha": cfg["alpha"], "tol_outer": 1e-8, "tol_inner": 1e-10,
+            "dof": cfg["dof"], "nsub": cfg["nsub"],
+            "transmission": ({"kind": "OO2 two-sided", "p1_p2_q1_q2": cfg["robin"]} if cfg.get("robin") is not None
+                             else {"kind": "OO0", "alpha": cfg["alpha"]}),
+            "tol_outer": 1e-8, "tol_inner": 1e-10,
             "l2": "no flush: CG working set >> 126 MB L2 (939 MB per CG iteration at C3 on 1 GPU)",
             "parallelism": f"{cfg['nsub']} subdomains over {args.gpus} GPU(s)"}
 
@@ -170,8 +170,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = dict(synth.CONFIGS[args.config])
-    if args.alpha is not None:
-        cfg["alpha"] = tuple(float(v) for v in args.alpha.split(":")) if ":" in args.alpha else float(args.alpha)
+    if args.alpha is not None:  # p | p1:p2 (OO0) | p1:p2:q1:q2 (OO2)
+        v = [float(t) for t in args.alpha.split(":")]
+        cfg["robin"] = tuple(v) if len(v) == 4 else None
+        if len(v) < 4:
+            cfg["alpha"] = v[0] if len(v) == 1 else tuple(v)
     o_ = cfg["order"]
     cfg["dof"] = (o_ * cfg["nx"] - 1) * (o_ * cfg["ny"] - 1) * (o_ * cfg["nz"] - 1)
     drho = synth.density(cfg)
@@ -203,7 +206,7 @@ def main():
                 nranks=world, device=local_rank, nccl_uid=uid, stream=stream.cuda_stream)
     osm.decompose(cfg["nsub"])
     S = cfg["nsub"]
-    osm.set_robin(*synth.alphas(cfg))
+    osm.set_robin2(*synth.robin(cfg))
     t_setup = time.perf_counter()
     osm.assemble()
     torch.cuda.synchronize()
@@ -250,7 +253,7 @@ def main():
         dist.all_reduce(w)
         cg_work = float(w.item())
     ms_step = ms / args.steps
-    value = cfg["dof"] * outer / (ms / 1e3)
+    value = cg_work / (ms / 1e3)  # DOF x CG-iterations per second, whole job
 
     # Dominant kernel roofline (k_cg_spmv): CUDA events around every launch on the library
     # stream, recorded during instrumented solves run right after the timed region (per-launch
@@ -290,11 +293,11 @@ def main():
     phi = torch.empty(int(np.prod(osm.lattice)), dtype=torch.float64).pin_memory() if rank == 0 else None
     barrier()
     t0 = time.perf_counter()
-    e2e_outer = 0
+    e2e_cg_work = 0.0
     for _ in range(args.e2e_steps):
         osm.upload_density(h_drho.numpy())
         st2, rep2 = osm.solve(tol_outer=1e-8, max_outer=1000)
-        e2e_outer += rep2.outer_iters
+        e2e_cg_work += local_cg_work(osm, S, rank, world)
         osm.solution(out=phi.numpy() if phi is not None else None)
     barrier()
     t_e2e = time.perf_counter() - t0
@@ -302,7 +305,10 @@ def main():
         t = torch.tensor([t_e2e], device=f"cuda:{local_rank}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
-    e2e = {"value": cfg["dof"] * e2e_outer / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(drho.nbytes),
+        w = torch.tensor([e2e_cg_work], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(w)
+        e2e_cg_work = float(w.item())
+    e2e = {"value": e2e_cg_work / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(drho.nbytes),
            "d2h_bytes_per_step": int(np.prod(osm.lattice)) * 8, "steps": args.e2e_steps,
            "path": "osm_upload_density(host pinned) + osm_solve + osm_get_solution(host pinned)"}
 
@@ -313,17 +319,16 @@ def main():
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        t_iter, n_s, cores = oracle_sample(cfg, drho, cfg["alpha"], args.ref_iters)
-        t_solve = t_iter / n_s * (cg_work / args.steps)
-        cpu = {"value": cfg["dof"] * (outer / args.steps) / t_solve, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{args.ref_iters} oracle Jacobi-PCG iterations on subdomain 1 (scipy CSR, 1 thread), "
-                         f"extrapolated with this run's DOF x CG-iteration count and outer count; glued-residual "
-                         f"SpMVs not timed", "seconds_per_cg_iteration": t_iter, "sample_rows": n_s}
+        t_iter, n_s, cores = oracle_sample(cfg, drho, args.ref_iters)
+        cpu = {"value": n_s / t_iter, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{args.ref_iters} oracle Jacobi-PCG iterations on subdomain 1 of {args.config} "
+                         f"(scipy CSR, 1 thread)", "seconds_per_cg_iteration": t_iter, "sample_rows": n_s,
+               "time_to_tol_s_extrapolated": t_iter / n_s * (cg_work / args.steps)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
-            "cg_dof_iter_per_s": cg_work / (ms / 1e3), "setup_s": t_setup,
+            "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)

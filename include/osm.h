@@ -135,6 +135,14 @@ osm_status osm_decompose(osm_ctx* ctx, int nsub);
  * called between solves; the Robin term is re-applied on the device. */
 osm_status osm_set_robin(osm_ctx* ctx, const double* alpha_left, const double* alpha_right);
 
+/* OO2 transmission ("A^(s) := p^(s) + q^(s) d^2_tau", optimized in Table 1
+ * rows oo2_*; sign reading SURVEY Q25: symbol Lambda = p + q k^2, i.e. the operator
+ * p - q d^2_tau, weak form int_Gamma p u v + q grad_tau u . grad_tau v = p M_Gamma + q S_Gamma).
+ * p_left[i], q_left[i]: side 0 (slab left of interface i); p_right, q_right: side 1.
+ * ILL_POSED if any coefficient < 0 or p = 0 on both sides.  osm_set_robin == q = 0. */
+osm_status osm_set_robin2(osm_ctx* ctx, const double* p_left, const double* q_left, const double* p_right,
+                          const double* q_right);
+
 /* [device work] Builds, per local subdomain: the Neumann stiffness K_s^N
  * (structural pattern, Dirichlet rows/cols removed), the interface mass
  * M_Gamma, interface maps, the SELL-32 hot-path copy and the Jacobi diagonal.
@@ -203,6 +211,10 @@ osm_status osm_get_interface_map(osm_ctx* ctx, int iface, int side, int32_t* idx
 /* The interface mass matrix M_Gamma (n_Gamma rows, plane-point order, CSR). */
 osm_status osm_get_interface_mass(osm_ctx* ctx, int64_t* rowptr, int32_t* col, double* val, int64_t* nrows,
                                   int64_t* nnz);
+
+/* S_Gamma values (the OO2 tangential stiffness), aligned with osm_get_interface_mass's pattern.
+ * val == NULL: *nnz only. */
+osm_status osm_get_interface_stiffness(osm_ctx* ctx, double* val, int64_t* nnz);
 
 /* Device-timing instrumentation: events around every launch of the named
  * kernels, on the library stream.  Reset on enable. */

@@ -207,6 +207,68 @@ def basis_values(order: int, lam: np.ndarray) -> np.ndarray:
     return out
 
 
+def tri_stiffness(order: int, Y: np.ndarray) -> np.ndarray:
+    """int_T grad_tau phi_a . grad_tau phi_b on the plane triangle with vertices Y (3 x 2).
+
+    Basis order as tri_mass (P2: v0, v1, v2, e01, e12, e02); degree-2 exact 3-point rule
+    (barycentric (2/3, 1/6, 1/6) and permutations, weights |T|/3).
+    """
+    Jm = (Y[1:] - Y[0]).T
+    Jinv = np.linalg.inv(Jm)
+    g = np.empty((3, 2))
+    g[1:] = Jinv
+    g[0] = -g[1:].sum(axis=0)
+    area = abs(np.linalg.det(Jm)) / 2.0
+    if order == 1:
+        Kt = area * g @ g.T
+        return np.triu(Kt) + np.triu(Kt, 1).T  # upper triangle mirrored: exactly symmetric
+    edges = [(0, 1), (1, 2), (0, 2)]
+    pts = np.array([[2 / 3, 1 / 6, 1 / 6], [1 / 6, 2 / 3, 1 / 6], [1 / 6, 1 / 6, 2 / 3]])
+    Kt = np.zeros((6, 6))
+    for lam in pts:
+        gr = np.empty((6, 2))
+        for i in range(3):
+            gr[i] = (4.0 * lam[i] - 1.0) * g[i]
+        for e, (i, j) in enumerate(edges):
+            gr[3 + e] = 4.0 * (lam[i] * g[j] + lam[j] * g[i])
+        Kt += (area / 3.0) * gr @ gr.T
+    return np.triu(Kt) + np.triu(Kt, 1).T  # upper triangle mirrored: exactly symmetric
+
+
+def interface_stiffness(box: Box) -> "scipy.sparse.csr_matrix":
+    """S_Gamma = int_Gamma grad_tau phi_i . grad_tau phi_j on the free interior points of an x = const
+    plane (same triangles and ordering as interface_mass).  The weak form of the OO2 tangential term:
+    A = p - q d^2/dtau^2 ("A^(s) := p^(s) + q^(s) d^2_tau"; sign reading SURVEY Q25,
+    Lambda = p + q k^2) gives int_Gamma (p u v + q grad_tau u . grad_tau v)."""
+    return _plane_assemble(box, lambda o, tri_pts: tri_stiffness(o, tri_pts))
+
+
+def _plane_assemble(box: Box, elem):
+    o = box.order
+    hy, hz = box.h[1], box.h[2]
+    _, Ny, Nz = box.lattice
+    nJ, nK = Ny - 2, Nz - 2
+    tris = [np.array([[0, 0], [1, 0], [1, 1]]), np.array([[0, 0], [0, 1], [1, 1]])]
+    rows, cols, vals = [], [], []
+    for ck in range(box.nz):
+        for cj in range(box.ny):
+            for tri in tris:
+                Et = elem(o, tri * np.array([hy, hz]))
+                pts = tri if o == 1 else np.concatenate([2 * tri, [tri[0] + tri[1], tri[1] + tri[2], tri[0] + tri[2]]])
+                Jp = o * cj + pts[:, 0]
+                Kp = o * ck + pts[:, 1]
+                free = (Jp >= 1) & (Jp <= Ny - 2) & (Kp >= 1) & (Kp <= Nz - 2)
+                gid = (Jp - 1) + nJ * (Kp - 1)
+                for a in range(len(pts)):
+                    for b in range(len(pts)):
+                        if free[a] and free[b]:
+                            rows.append(gid[a])
+                            cols.append(gid[b])
+                            vals.append(Et[a, b])
+    n = nJ * nK
+    return csr_from_triplets(n, n, rows, cols, vals)
+
+
 def interface_mass(box: Box) -> "scipy.sparse.csr_matrix":
     """M_Gamma on the free interior points of an x = const plane.
 

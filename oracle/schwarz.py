@@ -34,6 +34,7 @@ class Problem:
     nsub: int
     subs: list
     MG: sp.csr_matrix  # interface mass M_Gamma (identical on every interface)
+    SG: sp.csr_matrix  # interface tangential stiffness S_Gamma (OO2 term)
     K: sp.csr_matrix  # monolithic K (for the glued residual and the monolithic solve)
     f: np.ndarray  # monolithic load
 
@@ -63,22 +64,28 @@ def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=
         subs[i].right = l
         subs[i + 1].left = r
     MG = fe.interface_mass(box)
+    SG = fe.interface_stiffness(box)
     if not monolithic:
-        return Problem(box, nsub, subs, MG, None, None)
+        return Problem(box, nsub, subs, MG, SG, None, None)
     K = fe.assemble_stiffness(box, full)
     f = fe.assemble_load_function(box, full, load_fn, quad) if load_fn is not None else fe.assemble_load(box, full, drho)
-    return Problem(box, nsub, subs, MG, K, f)
+    return Problem(box, nsub, subs, MG, SG, K, f)
 
 
-def robin_operators(prob: Problem, alpha_left, alpha_right):
+def robin_operators(prob: Problem, alpha_left, alpha_right, q_left=None, q_right=None):
     """Transmission operators A[(i, side)] on interface i: side 0 = left slab (A^(1)), 1 = right (A^(2)).
 
-    OO0 reading: A^(s) = alpha_s M_Gamma (weak Robin term).
+    OO0: A^(s) = p_s M_Gamma (weak Robin term, p = alpha).
+    OO2: A^(s) = p_s M_Gamma + q_s S_Gamma.
     """
     A = {}
     for i in range(prob.nsub - 1):
         A[(i, 0)] = alpha_left[i] * prob.MG
         A[(i, 1)] = alpha_right[i] * prob.MG
+        if q_left is not None and q_left[i] != 0:
+            A[(i, 0)] = A[(i, 0)] + q_left[i] * prob.SG
+        if q_right is not None and q_right[i] != 0:
+            A[(i, 1)] = A[(i, 1)] + q_right[i] * prob.SG
     return A
 
 

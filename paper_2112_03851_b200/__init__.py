@@ -31,7 +31,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_trace", "osm_get_csr", "osm_get_interface_map", "osm_get_interface_mass",
                "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model", "osm_get_launch_count", "osm_solve_batch",
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
-               "osm_plan"]
+               "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness"]
 
 
 class MeshDesc(C.Structure):
@@ -100,6 +100,8 @@ _sigs = {
     "osm_get_batch_history": (C.c_int, [_P, C.c_int, _pd, C.c_int, _pint]),
     "osm_get_batch_inner_iters": (C.c_int, [_P, C.c_int, _pi32, C.c_int, _pint]),
     "osm_get_batch_local_solution": (C.c_int, [_P, C.c_int, C.c_int, _pd, _pi64]),
+    "osm_set_robin2": (C.c_int, [_P, _pd, _pd, _pd, _pd]),
+    "osm_get_interface_stiffness": (C.c_int, [_P, _pd, _pi64]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
 for _name, (_res, _args) in _sigs.items():
@@ -185,6 +187,20 @@ class Osm:
         if al.size != max(self.nsub - 1, 0) or ar.size != al.size:
             raise ValueError("need nsub-1 alphas per side")
         _check(_lib.osm_set_robin(self._h, _ptr(al, C.c_double), _ptr(ar, C.c_double)))
+
+    def set_robin2(self, p_left, q_left, p_right, q_right):
+        """OO2 transmission p M_Gamma + q S_Gamma per interface side (osm_set_robin2)."""
+        n = max(self.nsub - 1, 0)
+        arrs = [np.ascontiguousarray(np.broadcast_to(np.asarray(v, dtype=np.float64), (n,))) for v in
+                (p_left, q_left, p_right, q_right)]
+        _check(_lib.osm_set_robin2(self._h, *[_ptr(a, C.c_double) for a in arrs]))
+
+    def interface_stiffness(self):
+        nz = C.c_int64(0)
+        _check(_lib.osm_get_interface_stiffness(self._h, None, C.byref(nz)))
+        out = np.zeros(nz.value)
+        _check(_lib.osm_get_interface_stiffness(self._h, _ptr(out, C.c_double), C.byref(nz)))
+        return out
 
     def assemble(self):
         _check(_lib.osm_assemble(self._h))
@@ -342,7 +358,11 @@ def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None
     o = Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], rank, nranks, device,
             nccl_uid)
     o.decompose(cfg["nsub"])
-    if cfg["nsub"] > 1:
+    if cfg["nsub"] > 1 and alpha is None and cfg.get("robin") is not None:
+        n = cfg["nsub"] - 1
+        p1, p2, q1, q2 = cfg["robin"]
+        o.set_robin2(np.full(n, p1), np.full(n, q1), np.full(n, p2), np.full(n, q2))
+    elif cfg["nsub"] > 1:
         a = cfg.get("alpha") if alpha is None else alpha
         n = cfg["nsub"] - 1
         if np.isscalar(a):

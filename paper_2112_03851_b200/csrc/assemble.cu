@@ -92,9 +92,9 @@ __global__ void k_load(SlabGeom g, int64_t n, StencilDev T, const double* __rest
   b[row0 + iperm[i]] = s;
 }
 
-// Copy contract CSR rows into SELL-32 slices (column-major), remapping columns to
-// internal concatenated indices; padding = (val 0, col = own row).  Also dinv from K^N.
-__global__ void k_sell_build(int64_t npad, int64_t row0, int64_t slice0, const int32_t* __restrict__ perm,
+// Copy contract CSR rows into SELL-256 tiles (column-major over the tile), remapping
+// columns to internal concatenated indices; padding = (val 0, col = own row).  Also dinv from K^N.
+__global__ void k_sell_build(int64_t npad, int64_t row0, int64_t blk0, const int32_t* __restrict__ perm,
                              const int32_t* __restrict__ iperm, const int64_t* __restrict__ rowptr,
                              const int32_t* __restrict__ ccol, const double* __restrict__ cval,
                              const int64_t* __restrict__ soff, const int32_t* __restrict__ swidth,
@@ -102,16 +102,17 @@ __global__ void k_sell_build(int64_t npad, int64_t row0, int64_t slice0, const i
                              int32_t* __restrict__ flags) {
   const int64_t ri = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (ri >= npad) return;
-  const int64_t slice = slice0 + ri / kWarp;
-  const int lane = (int)(ri % kWarp);
-  const int64_t off = soff[slice] + lane;
-  const int w = swidth[slice];
+  const int64_t tile = blk0 + ri / kRowsPerBlock;
+  const int lane = (int)(ri % kRowsPerBlock);
+  const int64_t off = soff[tile] + lane;
+  const int w = swidth[tile];
   const int64_t grow = row0 + ri;
   const int c = perm[ri];
+  constexpr int64_t T = kRowsPerBlock;
   if (c < 0) {
     for (int k = 0; k < w; ++k) {
-      scol[off + (int64_t)kWarp * k] = (int32_t)grow;
-      sval[off + (int64_t)kWarp * k] = 0.0;
+      scol[off + T * k] = (int32_t)grow;
+      sval[off + T * k] = 0.0;
     }
     dinv[grow] = 0.0;
     return;
@@ -123,15 +124,15 @@ __global__ void k_sell_build(int64_t npad, int64_t row0, int64_t slice0, const i
   for (int k = 0; k < w; ++k) {
     if (k < len) {
       const int cc = ccol[beg + k];
-      scol[off + (int64_t)kWarp * k] = (int32_t)(row0 + iperm[cc]);
-      sval[off + (int64_t)kWarp * k] = cval[beg + k];
+      scol[off + T * k] = (int32_t)(row0 + iperm[cc]);
+      sval[off + T * k] = cval[beg + k];
       if (cc == c) {
         d = cval[beg + k];
         found = true;
       }
     } else {
-      scol[off + (int64_t)kWarp * k] = (int32_t)grow;
-      sval[off + (int64_t)kWarp * k] = 0.0;
+      scol[off + T * k] = (int32_t)grow;
+      sval[off + T * k] = 0.0;
     }
   }
   if (!found || !(d > 0.0)) atomicOr(flags, 1);
@@ -141,9 +142,10 @@ __global__ void k_sell_build(int64_t npad, int64_t row0, int64_t slice0, const i
 // For each M_Gamma entry (g, g2) of a side: the SELL position of K_s entry (map[g], map[g2]).
 __global__ void k_fold_build(int64_t nG, const int32_t* __restrict__ map_c, const int32_t* __restrict__ mrow,
                              const int32_t* __restrict__ mcol, const double* __restrict__ mval,
+                             const double* __restrict__ sval, double* __restrict__ fold_s,
                              const int64_t* __restrict__ rowptr, const int32_t* __restrict__ ccol,
                              const double* __restrict__ cval, const int32_t* __restrict__ iperm, int64_t row0,
-                             int64_t slice0, const int64_t* __restrict__ soff, int64_t fold0, int side_idx,
+                             int64_t blk0, const int64_t* __restrict__ soff, int64_t fold0, int side_idx,
                              int64_t* __restrict__ fold_pos, double* __restrict__ fold_m, double* __restrict__ fold_kn,
                              int32_t* __restrict__ fold_diag_row, int32_t* __restrict__ fold_side,
                              int32_t* __restrict__ flags) {
@@ -151,8 +153,8 @@ __global__ void k_fold_build(int64_t nG, const int32_t* __restrict__ map_c, cons
   if (gi >= nG) return;
   const int c = map_c[gi];
   const int ri = iperm[c];
-  const int64_t slice = slice0 + ri / kWarp;
-  const int lane = ri % kWarp;
+  const int64_t tile = blk0 + ri / kRowsPerBlock;
+  const int lane = ri % kRowsPerBlock;
   const int64_t beg = rowptr[c], end = rowptr[c + 1];
   for (int j = mrow[gi]; j < mrow[gi + 1]; ++j) {
     const int cc = map_c[mcol[j]];
@@ -167,25 +169,28 @@ __global__ void k_fold_build(int64_t nG, const int32_t* __restrict__ map_c, cons
       fold_pos[e] = -1;
       continue;
     }
-    fold_pos[e] = soff[slice] + (int64_t)kWarp * (lo - beg) + lane;
+    fold_pos[e] = soff[tile] + (int64_t)kRowsPerBlock * (lo - beg) + lane;
     fold_m[e] = mval[j];
+    fold_s[e] = sval[j];
     fold_kn[e] = cval[lo];
     fold_diag_row[e] = (cc == c) ? (int32_t)(row0 + ri) : -1;
     fold_side[e] = side_idx;
   }
 }
 
-// K_s = K_s^N + alpha_s M_Gamma on the interface rows, and the
-// Jacobi diagonal of the Robin-augmented rows.
-__global__ void k_fold_apply(int64_t nfold, const double* __restrict__ alpha_side, const int64_t* __restrict__ pos,
-                             const double* __restrict__ m, const double* __restrict__ kn,
+// K_s = K_s^N + (p_s M_Gamma + q_s S_Gamma) on the interface rows (OO2
+// PAPER.md:78), and the Jacobi diagonal of the Robin-augmented rows.
+__global__ void k_fold_apply(int64_t nfold, const double* __restrict__ alpha_side, const double* __restrict__ q_side,
+                             const int64_t* __restrict__ pos, const double* __restrict__ m,
+                             const double* __restrict__ sv, const double* __restrict__ kn,
                              const int32_t* __restrict__ diag_row, const int32_t* __restrict__ side,
                              double* __restrict__ sval, double* __restrict__ dinv, int32_t* __restrict__ flags) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= nfold) return;
   const int64_t p = pos[e];
   if (p < 0) return;
-  const double v = __dadd_rn(kn[e], __dmul_rn(alpha_side[side[e]], m[e]));
+  const double a = __dadd_rn(__dmul_rn(alpha_side[side[e]], m[e]), __dmul_rn(q_side[side[e]], sv[e]));
+  const double v = __dadd_rn(kn[e], a);
   sval[p] = v;
   const int dr = diag_row[e];
   if (dr >= 0) {
@@ -236,7 +241,7 @@ void launch_fill(const Ctx& c, const Sub& s) {
 }
 
 void launch_sell_build(const Ctx& c, const Sub& s, const int32_t*) {
-  k_sell_build<<<grid_for(s.npad), 256, 0, c.stream>>>(s.npad, s.row0, s.slice0, s.perm, s.iperm, s.rowptr, s.col,
+  k_sell_build<<<grid_for(s.npad), 256, 0, c.stream>>>(s.npad, s.row0, s.blk0, s.perm, s.iperm, s.rowptr, s.col,
                                                       s.val, c.sell_soff, c.sell_swidth, c.sell_val, c.sell_col,
                                                       c.dinv, c.d_flags);
   OSM_CHECK_LAUNCH();
@@ -245,17 +250,19 @@ void launch_sell_build(const Ctx& c, const Sub& s, const int32_t*) {
 
 void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s) {
   const int side_idx = (int)(&sd - c.sides.data());
-  k_fold_build<<<grid_for(c.nG), 256, 0, c.stream>>>(c.nG, sd.map_c, c.d_mrow, c.d_mcol, c.d_mval, s.rowptr, s.col,
-                                                    s.val, s.iperm, s.row0, s.slice0, c.sell_soff, sd.fold0, side_idx,
+  k_fold_build<<<grid_for(c.nG), 256, 0, c.stream>>>(c.nG, sd.map_c, c.d_mrow, c.d_mcol, c.d_mval, c.d_sval,
+                                                    c.fold_s, s.rowptr, s.col,
+                                                    s.val, s.iperm, s.row0, s.blk0, c.sell_soff, sd.fold0, side_idx,
                                                     c.fold_pos, c.fold_m, c.fold_kn, c.fold_diag_row, c.fold_side,
                                                     c.d_flags);
   OSM_CHECK_LAUNCH();
   ++c.launches;
 }
 
-void launch_fold_apply(const Ctx& c, const double* d_alpha_side) {
+void launch_fold_apply(const Ctx& c, const double* d_alpha_side, const double* d_q_side) {
   if (c.nfold == 0) return;
-  k_fold_apply<<<grid_for(c.nfold), 256, 0, c.stream>>>(c.nfold, d_alpha_side, c.fold_pos, c.fold_m, c.fold_kn,
+  k_fold_apply<<<grid_for(c.nfold), 256, 0, c.stream>>>(c.nfold, d_alpha_side, d_q_side, c.fold_pos, c.fold_m,
+                                                       c.fold_s, c.fold_kn,
                                                        c.fold_diag_row, c.fold_side, c.sell_val, c.dinv, c.d_flags);
   OSM_CHECK_LAUNCH();
   ++c.launches;

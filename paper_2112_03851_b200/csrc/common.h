@@ -29,7 +29,8 @@ struct Error : std::runtime_error {
 constexpr int kWarp = 32;
 constexpr int kSlicesPerBlock = 8;                       // warps per hot-path block
 constexpr int kRowsPerBlock = kWarp * kSlicesPerBlock;   // 256 rows per block
-constexpr int kThreads = kRowsPerBlock;                  // one thread per row in vector kernels
+constexpr int kThreads = kRowsPerBlock;                  // one thread per row in the SpMV kernels
+constexpr int kVecTiles = 4;                             // tiles per vector-kernel block (8 rows/thread)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }

@@ -31,14 +31,16 @@ struct StencilDev {
   int order;
 };
 
-// SELL-32 matrix over the concatenated internal rows of every local subdomain.
-// Slice k holds internal rows [32k, 32k+32); entry j of its row l sits at
-// soff[k] + 32 j + l (column major); padding entries have val 0, col = own row.
+// SELL-256 matrix over the concatenated internal rows of every local subdomain.
+// Tile t (= hot-path block t) holds internal rows [256t, 256t+256); entry j of its
+// row l sits at toff[t] + 256 j + l (column major over the tile), so entries
+// [j0, j1) of the whole tile are one contiguous range (bulk-copy friendly);
+// padding entries have val 0, col = own row.
 struct SellDev {
   const double* val;
   const int32_t* col;
-  const int64_t* soff;
-  const int32_t* swidth;
+  const int64_t* toff;
+  const int32_t* twidth;
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -51,6 +53,8 @@ struct SubState {
   double resid;    // interior part of sum (f - K u~)^2 for this subdomain
   int64_t blk0;    // first block (256 rows) of the subdomain
   int32_t nblk;    // number of blocks
+  int64_t vblk0;   // first vector block (up to kVecTiles tiles) of the subdomain
+  int32_t nvblk;   // number of vector blocks
   int32_t active;  // PCG still running
   int32_t iters;   // PCG iterations of the current inner solve
   int32_t status;  // 0 running, 1 converged, 2 max_inner, 3 breakdown
@@ -66,7 +70,8 @@ struct SideDev {
   const double* in;    // partner outbox (local) or receive buffer (remote) [g | u | w]
   double* unbr;        // neighbour trace u_t|Gamma (for gluing)
   double* wif;         // residual (f - K^N u~) at this side's plane rows
-  double alpha_own, alpha_sum;
+  double alpha_own, alpha_sum;  // p of this side, p_s + p_t
+  double q_own, q_sum;          // OO2 tangential coefficients (0 for OO0)
   int32_t sub;         // local subdomain index
   int32_t which;       // 0: this slab is the left slab of the interface (its right plane), 1: right slab
   int32_t slot0;       // first islot index of the side (= side * nG)
@@ -122,7 +127,8 @@ struct Ctx {
   int nsub = 0;
   std::vector<int64_t> cstart;  // slab cell starts
   int s_begin = 0, s_end = 0;   // local subdomains [s_begin, s_end)
-  std::vector<double> alpha_left, alpha_right;
+  std::vector<double> alpha_left, alpha_right;  // p^(1), p^(2) per interface
+  std::vector<double> q_left, q_right;          // q^(1), q^(2) per interface (OO2; 0 = OO0)
   bool robin_set = false, assembled = false, density_set = false;
   bool robin_dirty = true;
   double G = 6.672e-11;
@@ -137,9 +143,10 @@ struct Ctx {
   // interface mass (host + device), plane-point order
   int64_t nG = 0;
   std::vector<int32_t> h_mrow, h_mcol;
-  std::vector<double> h_mval;
+  std::vector<double> h_mval, h_sval;
   int32_t *d_mrow = nullptr, *d_mcol = nullptr;
   double* d_mval = nullptr;
+  double* d_sval = nullptr;  // S_Gamma values aligned with M_Gamma
 
   // subdomains and sides
   std::vector<Sub> subs;
@@ -152,12 +159,17 @@ struct Ctx {
   int64_t* sell_soff = nullptr;
   int32_t* sell_swidth = nullptr;
   int32_t* blk_sub = nullptr;  // block -> local subdomain
+  int32_t* vblk_sub = nullptr;    // vector block -> local subdomain
+  int32_t* vblk_tile0 = nullptr;  // vector block -> first tile
+  int32_t* vblk_ntile = nullptr;  // vector block -> tiles (<= kVecTiles)
+  int64_t nvblk_total = 0;
   int32_t* islot = nullptr;    // per internal row: -2 pad, -1 interior, >= 0 interface slot
 
   // Robin fold list (device): sell position, M value, K^N value, diag row (-1 if off-diagonal)
   int64_t nfold = 0;
   int64_t* fold_pos = nullptr;
   double* fold_m = nullptr;
+  double* fold_s = nullptr;
   double* fold_kn = nullptr;
   int32_t* fold_diag_row = nullptr;
   int32_t* fold_side = nullptr;
@@ -197,7 +209,8 @@ struct Ctx {
   double graph_tol = -1;
   int graph_maxit = -1;
   bool use_graph = true;
-  int sigma = 8192;  // SELL sorting window
+  int sigma = 32768;  // SELL sorting window (rows); SELL-256 padding 0.9% at C3
+  int spmv_variant = 2;  // 0: LDG rows, 2: LDG rows at 32 regs (default, 8 blocks/SM), 1: warp-specialized cp.async.bulk pipeline
 
   // instrumentation
   bool timing = false;
@@ -218,7 +231,7 @@ void launch_count(const Ctx& c, const Sub& s, int32_t* rowlen);
 void launch_fill(const Ctx& c, const Sub& s);
 void launch_sell_build(const Ctx& c, const Sub& s, const int32_t* d_slice_width_local);
 void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s);
-void launch_fold_apply(const Ctx& c, const double* d_alpha_side);
+void launch_fold_apply(const Ctx& c, const double* d_alpha_side, const double* d_q_side);
 void launch_load(const Ctx& c, const Sub& s, double fourpiG);
 void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned);
 void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract);
@@ -243,6 +256,8 @@ void batch_inner(const Ctx& c, int b, int32_t* its, int cap, int* n);
 void batch_local_solution(Ctx& c, int b, int s, double* u, int64_t* n);
 void batch_free(Ctx& c);
 double fnorm2_of(Ctx& c);  // ||f||^2 of the glued global system (osm.cu)
+
+void spmv_init_attributes();
 
 // timing helpers (osm.cu)
 void timer_begin(Ctx& c, int id);

@@ -145,6 +145,60 @@ std::vector<double> tri_mass_unit(int order) {
   return M;
 }
 
+// Plane-triangle stiffness (order P1/P2, basis order as tri_mass_unit) of the triangle with
+// vertices Y[3][2]: closed form, int lam_i lam_j = |T|(1 + d_ij)/12, int lam_i = |T|/3.
+std::vector<double> tri_stiffness(int order, const double Y[3][2]) {
+  const double J[2][2] = {{Y[1][0] - Y[0][0], Y[2][0] - Y[0][0]}, {Y[1][1] - Y[0][1], Y[2][1] - Y[0][1]}};
+  const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  const double area = std::fabs(det) / 2.0;
+  double g[3][2];
+  g[1][0] = J[1][1] / det;
+  g[1][1] = -J[0][1] / det;
+  g[2][0] = -J[1][0] / det;
+  g[2][1] = J[0][0] / det;
+  g[0][0] = -(g[1][0] + g[2][0]);
+  g[0][1] = -(g[1][1] + g[2][1]);
+  const int n = order == 1 ? 3 : 6;
+  std::vector<double> K(n * n);
+  if (order == 1) {
+    for (int a = 0; a < 3; ++a)
+      for (int b = a; b < 3; ++b) K[a * 3 + b] = K[b * 3 + a] = area * (g[a][0] * g[b][0] + g[a][1] * g[b][1]);
+    return K;
+  }
+  // grad phi_a = sum_m (A[a][m] + sum_k B[a][m][k] lam_k) grad lam_m
+  double A[6][3] = {}, B[6][3][3] = {};
+  for (int i = 0; i < 3; ++i) {
+    A[i][i] = -1.0;
+    B[i][i][i] = 4.0;
+  }
+  const int e[3][2] = {{0, 1}, {1, 2}, {0, 2}};
+  for (int k = 0; k < 3; ++k) {
+    B[3 + k][e[k][0]][e[k][1]] = 4.0;
+    B[3 + k][e[k][1]][e[k][0]] = 4.0;
+  }
+  auto lin = [](double a, const double* b, double ap, const double* bp) {
+    double sb = 0, sbp = 0, qd = 0;
+    for (int k = 0; k < 3; ++k) {
+      sb += b[k];
+      sbp += bp[k];
+      for (int l = 0; l < 3; ++l) qd += b[k] * bp[l] * (k == l ? 2.0 : 1.0) / 12.0;
+    }
+    return a * ap + (a * sbp + ap * sb) / 3.0 + qd;
+  };
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) {
+      double s = 0.0;
+      for (int m = 0; m < 3; ++m)
+        for (int nn = 0; nn < 3; ++nn) {
+          const double gg = g[m][0] * g[nn][0] + g[m][1] * g[nn][1];
+          if (gg == 0.0) continue;
+          s += gg * lin(A[a][m], B[a][m], A[b][nn], B[b][nn]);
+        }
+      K[a * 6 + b] = K[b * 6 + a] = area * s;
+    }
+  return K;
+}
+
 }  // namespace
 
 std::vector<std::array<int, 3>> tet_local_offsets(int t, int order) {
@@ -292,7 +346,7 @@ StencilTables build_stencil_tables(int order, const double h[3]) {
 }
 
 void interface_mass(int order, int64_t ny, int64_t nz, double hy, double hz, std::vector<int32_t>& rowptr,
-                    std::vector<int32_t>& col, std::vector<double>& val) {
+                    std::vector<int32_t>& col, std::vector<double>& val, std::vector<double>& sval) {
   const int64_t Ny = order * ny + 1, Nz = order * nz + 1;
   const int64_t nJ = Ny - 2, nK = Nz - 2, n = nJ * nK;
   const std::vector<double> Mu = tri_mass_unit(order);
@@ -301,12 +355,18 @@ void interface_mass(int order, int64_t ny, int64_t nz, double hy, double hz, std
   const int tris[2][3][2] = {{{0, 0}, {1, 0}, {1, 1}}, {{0, 0}, {0, 1}, {1, 1}}};
   struct Trip {
     int64_t r, c;
-    double v;
+    double v, s;
   };
   std::vector<Trip> trip;
   for (int64_t ck = 0; ck < nz; ++ck)
     for (int64_t cj = 0; cj < ny; ++cj)
       for (int t = 0; t < 2; ++t) {
+        double Y[3][2];
+        for (int a = 0; a < 3; ++a) {
+          Y[a][0] = tris[t][a][0] * hy;
+          Y[a][1] = tris[t][a][1] * hz;
+        }
+        const std::vector<double> St = tri_stiffness(order, Y);
         int pts[6][2];
         for (int a = 0; a < 3; ++a) {
           pts[a][0] = order * tris[t][a][0];
@@ -326,19 +386,25 @@ void interface_mass(int order, int64_t ny, int64_t nz, double hy, double hz, std
         }
         for (int a = 0; a < nl; ++a)
           for (int b = 0; b < nl; ++b)
-            if (fr[a] && fr[b]) trip.push_back({gid[a], gid[b], area * Mu[a * nl + b]});
+            if (fr[a] && fr[b]) trip.push_back({gid[a], gid[b], area * Mu[a * nl + b], St[a * nl + b]});
       }
   std::stable_sort(trip.begin(), trip.end(),
                    [](const Trip& p, const Trip& q) { return p.r != q.r ? p.r < q.r : p.c < q.c; });
   rowptr.assign(n + 1, 0);
   col.clear();
   val.clear();
+  sval.clear();
   for (size_t i = 0; i < trip.size();) {
     size_t j = i;
-    double s = 0.0;
-    while (j < trip.size() && trip[j].r == trip[i].r && trip[j].c == trip[i].c) s += trip[j++].v;
+    double s = 0.0, st = 0.0;
+    while (j < trip.size() && trip[j].r == trip[i].r && trip[j].c == trip[i].c) {
+      s += trip[j].v;
+      st += trip[j].s;
+      ++j;
+    }
     col.push_back((int32_t)trip[i].c);
     val.push_back(s);
+    sval.push_back(st);
     rowptr[trip[i].r + 1]++;
     i = j;
   }

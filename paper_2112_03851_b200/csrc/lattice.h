@@ -55,8 +55,10 @@ StencilTables build_stencil_tables(int order, const double h[3]);
 // Interface-plane mass matrix M_Gamma on the free interior points of an x = const
 // plane of the (Ny x Nz)-point lattice, CSR in plane-point order (j fastest).
 // Triangles: each (j,k) square split along its (j,k)-(j+1,k+1) diagonal.
+// Also the tangential stiffness S_Gamma = int grad_tau phi_i . grad_tau phi_j (the OO2 term),
+// with exactly the same pattern (sval aligned with val).
 void interface_mass(int order, int64_t ny, int64_t nz, double hy, double hz, std::vector<int32_t>& rowptr,
-                    std::vector<int32_t>& col, std::vector<double>& val);
+                    std::vector<int32_t>& col, std::vector<double>& val, std::vector<double>& sval);
 
 // Cell starts c_0..c_S of the x-slabs (widths differ by <= 1, remainder to the left).
 std::vector<int64_t> partition_x(int64_t nx, int nsub);

@@ -110,14 +110,19 @@ static void free_assembly(Ctx& c) {
   dfree(c.d_mrow);
   dfree(c.d_mcol);
   dfree(c.d_mval);
+  dfree(c.d_sval);
   dfree(c.sell_val);
   dfree(c.sell_col);
   dfree(c.sell_soff);
   dfree(c.sell_swidth);
   dfree(c.blk_sub);
+  dfree(c.vblk_sub);
+  dfree(c.vblk_tile0);
+  dfree(c.vblk_ntile);
   dfree(c.islot);
   dfree(c.fold_pos);
   dfree(c.fold_m);
+  dfree(c.fold_s);
   dfree(c.fold_kn);
   dfree(c.fold_diag_row);
   dfree(c.fold_side);
@@ -174,11 +179,12 @@ static void assemble(Ctx& c) {
   c.d_contribs = dupload(c, c.tables.contribs);
   c.d_load_begin = dupload(c, c.tables.load_begin);
   c.d_loads = dupload(c, c.tables.loads);
-  interface_mass(o, c.mesh.ny, c.mesh.nz, h[1], h[2], c.h_mrow, c.h_mcol, c.h_mval);
+  interface_mass(o, c.mesh.ny, c.mesh.nz, h[1], h[2], c.h_mrow, c.h_mcol, c.h_mval, c.h_sval);
   c.nG = (int64_t)c.h_mrow.size() - 1;
   c.d_mrow = dupload(c, c.h_mrow);
   c.d_mcol = dupload(c, c.h_mcol);
   c.d_mval = dupload(c, c.h_mval);
+  c.d_sval = dupload(c, c.h_sval);
   if (!c.d_flags) c.d_flags = dalloc<int32_t>(4);
   OSM_CUDA(cudaMemsetAsync(c.d_flags, 0, 4 * sizeof(int32_t), c.stream));
 
@@ -234,16 +240,16 @@ static void assemble(Ctx& c) {
       }
     }
     S.sell_entries = 0;
-    for (int64_t sl = 0; sl < S.nslice; ++sl) {
+    for (int64_t t = 0; t < S.nblk; ++t) {  // SELL-256 tiles = hot-path blocks
       int w = 0;
-      for (int l = 0; l < kWarp; ++l) {
-        const int32_t cr = perm[sl * kWarp + l];
+      for (int l = 0; l < kRowsPerBlock; ++l) {
+        const int32_t cr = perm[t * kRowsPerBlock + l];
         if (cr >= 0) w = std::max(w, len[cr]);
       }
       h_soff.push_back(sell_off);
       h_swidth.push_back(w);
-      sell_off += (int64_t)w * kWarp;
-      S.sell_entries += (int64_t)w * kWarp;
+      sell_off += (int64_t)w * kRowsPerBlock;
+      S.sell_entries += (int64_t)w * kRowsPerBlock;
     }
     S.perm = dupload(c, perm);
     S.iperm = dupload(c, iperm);
@@ -274,6 +280,21 @@ static void assemble(Ctx& c) {
   for (int ls = 0; ls < nloc; ++ls)
     for (int64_t k = 0; k < c.subs[ls].nblk; ++k) blk_sub[c.subs[ls].blk0 + k] = ls;
   c.blk_sub = dupload(c, blk_sub);
+  {
+    std::vector<int32_t> vs, vt, vn;
+    for (int ls = 0; ls < nloc; ++ls) {
+      Sub& S = c.subs[ls];
+      for (int64_t t = 0; t < S.nblk; t += kVecTiles) {
+        vs.push_back(ls);
+        vt.push_back((int32_t)(S.blk0 + t));
+        vn.push_back((int32_t)std::min<int64_t>(kVecTiles, S.nblk - t));
+      }
+    }
+    c.nvblk_total = (int64_t)vs.size();
+    c.vblk_sub = dupload(c, vs);
+    c.vblk_tile0 = dupload(c, vt);
+    c.vblk_ntile = dupload(c, vn);
+  }
 
   // --- interface sides
   const int64_t nG = c.nG;
@@ -338,6 +359,7 @@ static void assemble(Ctx& c) {
   c.nfold = nsides * mnnz;
   c.fold_pos = dalloc<int64_t>(c.nfold);
   c.fold_m = dalloc<double>(c.nfold);
+  c.fold_s = dalloc<double>(c.nfold);
   c.fold_kn = dalloc<double>(c.nfold);
   c.fold_diag_row = dalloc<int32_t>(c.nfold);
   c.fold_side = dalloc<int32_t>(c.nfold);
@@ -360,6 +382,10 @@ static void assemble(Ctx& c) {
     std::memset(&hst[ls], 0, sizeof(SubState));
     hst[ls].blk0 = c.subs[ls].blk0;
     hst[ls].nblk = (int32_t)c.subs[ls].nblk;
+    int64_t v0 = 0;
+    for (int j = 0; j < ls; ++j) v0 += ceil_div(c.subs[j].nblk, kVecTiles);
+    hst[ls].vblk0 = v0;
+    hst[ls].nvblk = (int32_t)ceil_div(c.subs[ls].nblk, kVecTiles);
   }
   OSM_CUDA(cudaMemcpyAsync(c.st, hst.data(), sizeof(SubState) * nloc, cudaMemcpyHostToDevice, c.stream));
   if (c.h_st) cudaFreeHost(c.h_st);
@@ -404,22 +430,28 @@ static void apply_robin(Ctx& c) {
     return;
   }
   if (!c.robin_set) fail(OSM_ERR_STATE, "osm_set_robin must be called before solving with nsub > 1");
-  std::vector<double> a(nsides);
+  std::vector<double> a(nsides), qv(nsides);
   for (int k = 0; k < nsides; ++k) {
     const Side& sd = c.sides[k];
     const double al = c.alpha_left[sd.iface], ar = c.alpha_right[sd.iface];
+    const double ql = c.q_left[sd.iface], qr = c.q_right[sd.iface];
     a[k] = sd.which == 0 ? al : ar;
+    qv[k] = sd.which == 0 ? ql : qr;
     c.h_sides[k].alpha_own = a[k];
     c.h_sides[k].alpha_sum = al + ar;
+    c.h_sides[k].q_own = qv[k];
+    c.h_sides[k].q_sum = ql + qr;
   }
   double* d_a = dupload(c, a);
+  double* d_q = dupload(c, qv);
   OSM_CUDA(cudaMemsetAsync(c.d_flags, 0, 4 * sizeof(int32_t), c.stream));
-  launch_fold_apply(c, d_a);
+  launch_fold_apply(c, d_a, d_q);
   OSM_CUDA(cudaMemcpyAsync(c.d_sides, c.h_sides.data(), sizeof(SideDev) * nsides, cudaMemcpyHostToDevice, c.stream));
   int32_t flags[4];
   OSM_CUDA(cudaMemcpyAsync(flags, c.d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c.stream));
   OSM_CUDA(cudaStreamSynchronize(c.stream));
   dfree(d_a);
+  dfree(d_q);
   if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
   c.robin_dirty = false;
 }
@@ -726,6 +758,8 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[1], cudaEventDisableTiming));
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
+    if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);
+    spmv_init_attributes();
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
@@ -782,25 +816,44 @@ osm_status osm_decompose(osm_ctx* h, int nsub) {
   c.robin_set = nsub == 1;
   c.alpha_left.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
   c.alpha_right.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
+  c.q_left.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
+  c.q_right.assign(nsub > 1 ? nsub - 1 : 0, 0.0);
   return OSM_OK;
   OSM_API_END
 }
 
-osm_status osm_set_robin(osm_ctx* h, const double* al, const double* ar) {
-  OSM_API_BEGIN
-  Ctx& c = ctx_of(h);
+static void set_robin(Ctx& c, const double* al, const double* ql, const double* ar, const double* qr) {
   if (c.nsub < 1) fail(OSM_ERR_STATE, "osm_decompose must precede osm_set_robin");
   const int ni = c.nsub - 1;
   if (ni > 0 && (!al || !ar)) fail(OSM_ERR_INVALID_ARG, "NULL alpha array");
   for (int i = 0; i < ni; ++i) {
-    if (!(al[i] >= 0) || !(ar[i] >= 0) || !std::isfinite(al[i]) || !std::isfinite(ar[i]))
-      fail(OSM_ERR_ILL_POSED, "Robin alpha must be finite and >= 0");
-    if (al[i] == 0 && ar[i] == 0) fail(OSM_ERR_ILL_POSED, "alpha = 0 on both sides of an interface");
+    const double pl = al[i], pr = ar[i], l = ql ? ql[i] : 0.0, r = qr ? qr[i] : 0.0;
+    for (double v : {pl, pr, l, r})
+      if (!(v >= 0) || !std::isfinite(v)) fail(OSM_ERR_ILL_POSED, "Robin coefficients must be finite and >= 0");
+    if (pl == 0 && pr == 0 && l == 0 && r == 0) fail(OSM_ERR_ILL_POSED, "zero transmission on both sides of an interface");
+    if (pl == 0 && pr == 0) fail(OSM_ERR_ILL_POSED, "p = 0 on both sides of an interface");
   }
   c.alpha_left.assign(al, al + ni);
   c.alpha_right.assign(ar, ar + ni);
+  c.q_left.assign(ni, 0.0);
+  c.q_right.assign(ni, 0.0);
+  if (ql) c.q_left.assign(ql, ql + ni);
+  if (qr) c.q_right.assign(qr, qr + ni);
   c.robin_set = true;
   c.robin_dirty = true;
+}
+
+osm_status osm_set_robin(osm_ctx* h, const double* al, const double* ar) {
+  OSM_API_BEGIN
+  set_robin(ctx_of(h), al, nullptr, ar, nullptr);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_set_robin2(osm_ctx* h, const double* pl, const double* ql, const double* pr, const double* qr) {
+  OSM_API_BEGIN
+  if (!ql || !qr) fail(OSM_ERR_INVALID_ARG, "NULL q array");
+  set_robin(ctx_of(h), pl, ql, pr, qr);
   return OSM_OK;
   OSM_API_END
 }
@@ -996,6 +1049,20 @@ osm_status osm_get_interface_mass(osm_ctx* h, int64_t* rowptr, int32_t* col, dou
   }
   *nrows = c.nG;
   *nnz = m;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_get_interface_stiffness(osm_ctx* h, double* val, int64_t* nnz) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!nnz) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  if (!c.assembled) fail(OSM_ERR_STATE, "not assembled");
+  if (val) {
+    if (*nnz < (int64_t)c.h_sval.size()) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+    std::copy(c.h_sval.begin(), c.h_sval.end(), val);
+  }
+  *nnz = (int64_t)c.h_sval.size();
   return OSM_OK;
   OSM_API_END
 }

@@ -98,15 +98,17 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// y_row = sum_j A[row, j] x[j] for the lane's row of a SELL-32 slice, entries in
-// column order (sequential per row, deterministic).  Software-pipelined: the
-// value/column chunk k+1 is requested before the gathers of chunk k are consumed,
-// so every warp keeps two chunks of streaming loads in flight.  The slice width
-// is warp-uniform, so the tail predicates never diverge.
+// ---------------------------------------------------------------- SELL-256 row products
+// y_row = sum_j A[row, j] x[j] for row threadIdx.x of tile blk, entries in column order
+// (sequential per row: deterministic, identical in both variants below).
+
+// Variant 0 (LDG): each thread streams its row's values/columns with non-allocating loads,
+// software-pipelined so chunk k+1 is requested before the gathers of chunk k are consumed.
 template <int CH>
-__device__ __forceinline__ double sell_row(const SellDev& A, int64_t slice, int lane, const double* __restrict__ x) {
-  const int w = A.swidth[slice];
-  const int64_t base = A.soff[slice] + lane;
+__device__ __forceinline__ double tile_row_ldg(const SellDev& A, int64_t blk, const double* __restrict__ x) {
+  constexpr int T = kRowsPerBlock;
+  const int w = A.twidth[blk];
+  const int64_t base = A.toff[blk] + threadIdx.x;
   const double* vp = A.val + base;
   const int32_t* cp = A.col + base;
   double s = 0.0;
@@ -114,8 +116,8 @@ __device__ __forceinline__ double sell_row(const SellDev& A, int64_t slice, int 
   int32_t c[CH];
 #pragma unroll
   for (int j = 0; j < CH; ++j) {
-    v[j] = j < w ? ld_stream(vp + 32 * j) : 0.0;
-    c[j] = j < w ? ld_stream(cp + 32 * j) : 0;
+    v[j] = j < w ? ld_stream(vp + T * j) : 0.0;
+    c[j] = j < w ? ld_stream(cp + T * j) : 0;
   }
   for (int k = 0; k < w; k += CH) {
     double xv[CH];
@@ -126,8 +128,8 @@ __device__ __forceinline__ double sell_row(const SellDev& A, int64_t slice, int 
     const int kn = k + CH;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
-      vn[j] = (kn + j < w) ? ld_stream(vp + 32 * (kn + j)) : 0.0;
-      cn[j] = (kn + j < w) ? ld_stream(cp + 32 * (kn + j)) : 0;
+      vn[j] = (kn + j < w) ? ld_stream(vp + T * (int64_t)(kn + j)) : 0.0;
+      cn[j] = (kn + j < w) ? ld_stream(cp + T * (int64_t)(kn + j)) : 0;
     }
 #pragma unroll
     for (int j = 0; j < CH; ++j)
@@ -141,31 +143,152 @@ __device__ __forceinline__ double sell_row(const SellDev& A, int64_t slice, int 
   return s;
 }
 
-constexpr int kChunk = 4;
+// Variant 1 (bulk async copy): one elected thread streams the tile's value/column chunks
+// (CH entries x 256 rows, contiguous) into an NST-stage shared-memory ring with
+// cp.async.bulk completing on mbarriers (SASS UBLKCP); all warps only read shared memory
+// and gather x.  The copy engine keeps the HBM stream in flight independently of the
+// warps' gather latency.  Every thread of the block must call this (block barriers).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialized pipeline: warps 0..7 consume (row = threadIdx.x < 256), warp 8 produces.
+// full[st]: the stage's bytes have landed (tx count); empty[st]: all 8 consumer warps are done.
+constexpr int kBulkCH = 4;   // entries per stage
+constexpr int kBulkNST = 2;  // stages (24 KB ring: leaves L1 room for the x window)
+constexpr int kBulkStageBytes = kBulkCH * kRowsPerBlock * 12;
+constexpr int kBulkSmem = kBulkNST * kBulkStageBytes + 2 * kBulkNST * 8;
+constexpr int kBulkThreads = kRowsPerBlock + 32;
+
+__device__ __forceinline__ double tile_row_bulk(const SellDev& A, int64_t blk, const double* __restrict__ x,
+                                                unsigned char* smem) {
+  constexpr int T = kRowsPerBlock;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkNST * kBulkStageBytes);
+  uint64_t* empty = full + kBulkNST;
+  const int w = A.twidth[blk];
+  const int64_t off = A.toff[blk];
+  const int nch = (w + kBulkCH - 1) / kBulkCH;
+  if (threadIdx.x == T) {
+    for (int i = 0; i < kBulkNST; ++i) {
+      mbar_init_n(&full[i], 1);
+      mbar_init_n(&empty[i], kSlicesPerBlock);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x >= T) {  // producer warp: one elected lane streams the chunks
+    if (threadIdx.x == T) {
+      for (int ch = 0; ch < nch; ++ch) {
+        const int st = ch % kBulkNST;
+        if (ch >= kBulkNST) mbar_wait(&empty[st], (uint32_t)(((ch / kBulkNST) - 1) & 1));
+        const int kk = min(kBulkCH, w - ch * kBulkCH);
+        double* sv = reinterpret_cast<double*>(smem + st * kBulkStageBytes);
+        int32_t* sc = reinterpret_cast<int32_t*>(smem + st * kBulkStageBytes + kBulkCH * T * 8);
+        const uint32_t bv = (uint32_t)kk * T * 8, bc = (uint32_t)kk * T * 4;
+        mbar_expect(&full[st], bv + bc);
+        bulk_g2s(sv, A.val + off + (int64_t)ch * kBulkCH * T, bv, &full[st]);
+        bulk_g2s(sc, A.col + off + (int64_t)ch * kBulkCH * T, bc, &full[st]);
+      }
+    }
+    return 0.0;
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch % kBulkNST;
+    mbar_wait(&full[st], (uint32_t)((ch / kBulkNST) & 1));
+    const double* sv = reinterpret_cast<const double*>(smem + st * kBulkStageBytes);
+    const int32_t* sc = reinterpret_cast<const int32_t*>(smem + st * kBulkStageBytes + kBulkCH * T * 8);
+    const int kk = min(kBulkCH, w - ch * kBulkCH);
+    if (kk == kBulkCH) {
+      int32_t cj[kBulkCH];
+      double vj[kBulkCH], xv[kBulkCH];
+#pragma unroll
+      for (int j = 0; j < kBulkCH; ++j) {
+        cj[j] = sc[j * T + threadIdx.x];
+        vj[j] = sv[j * T + threadIdx.x];
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);  // stage data is in registers now
+#pragma unroll
+      for (int j = 0; j < kBulkCH; ++j) xv[j] = __ldg(x + cj[j]);
+#pragma unroll
+      for (int j = 0; j < kBulkCH; ++j) s = fma(vj[j], xv[j], s);
+    } else {
+      for (int j = 0; j < kk; ++j) s = fma(sv[j * T + threadIdx.x], __ldg(x + sc[j * T + threadIdx.x]), s);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  return s;
+}
+
+// V = 0: LDG rows; V = 2: LDG rows with registers capped at 32 (8 blocks / 64 warps per SM);
+// V = 1: warp-specialized bulk-copy pipeline.
+template <int V>
+__device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
+                                           unsigned char* smem) {
+  if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
+  return tile_row_ldg<4>(A, blk, x);
+}
+#define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, (V) == 2 ? 8 : 1)
 
 // ---------------------------------------------------------------- PCG kernels
 
 // q = K_s p ; p.q -> alpha = rho / (p.q)
-__global__ void __launch_bounds__(kThreads) k_cg_spmv(SellDev A, const int32_t* __restrict__ blk_sub,
+template <int V>
+__global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restrict__ blk_sub,
                                                       SubState* __restrict__ st, const double* __restrict__ p,
                                                       double* __restrict__ q, double* __restrict__ part,
                                                       int64_t stride, int32_t* __restrict__ nactive) {
-  __shared__ double sm[kSlicesPerBlock * 1];
+  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  __shared__ double sm[NW * 1];
+  extern __shared__ __align__(128) unsigned char dsm[];
   pdl_enter();
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   if (!st[ls].active) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t slice = blk * kSlicesPerBlock + warp;
-  const int64_t row = slice * kWarp + lane;
-  const double y = sell_row<kChunk>(A, slice, lane, p);
-  q[row] = y;
-  double v[1] = {p[row] * y};
-  block_sum<1>(v, sm);
+  const bool has_row = threadIdx.x < kRowsPerBlock;
+  const int64_t row = blk * kRowsPerBlock + threadIdx.x;
+  const double y = tile_row<V>(A, blk, p, dsm);
+  double v[1] = {0.0};
+  if (has_row) {
+    q[row] = y;
+    v[0] = p[row] * y;
+  }
+  block_sum<1, NW>(v, sm);
   SubState& S = st[ls];
   if (publish<1>(v, part, stride, blk, &S.cnt, S.nblk)) {
     double t[1];
-    gather_partials<1>(t, part, stride, S.blk0, S.nblk, sm);
+    gather_partials<1, NW>(t, part, stride, S.blk0, S.nblk, sm);
     if (threadIdx.x == 0) {
       const double pq = t[0];
       S.cnt = 0;
@@ -181,39 +304,58 @@ __global__ void __launch_bounds__(kThreads) k_cg_spmv(SellDev A, const int32_t* 
 }
 
 // x += alpha p ; r -= alpha q ; z = D^{-1} r ; r.z, r.r ; stop test ||r|| <= tol ||rhs||; beta.
-// 128 threads x 2 rows (16-byte loads) per 256-row block.
+// Vector blocks: up to kVecTiles tiles (1024 rows) of one subdomain, 128 threads x 8 rows,
+// all loads of a thread issued before any use (memory-level parallelism), one reduction
+// and one counter update per 1024 rows.
 constexpr int kVecThreads = kRowsPerBlock / 2;
-__global__ void __launch_bounds__(kVecThreads) k_cg_update(const int32_t* __restrict__ blk_sub, SubState* __restrict__ st,
-                                                           double* __restrict__ x, double* __restrict__ r,
-                                                           const double* __restrict__ p, const double* __restrict__ q,
+__global__ void __launch_bounds__(kVecThreads) k_cg_update(const int32_t* __restrict__ vblk_sub,
+                                                           const int32_t* __restrict__ vblk_tile0,
+                                                           const int32_t* __restrict__ vblk_ntile,
+                                                           SubState* __restrict__ st, double* __restrict__ x,
+                                                           double* __restrict__ r, const double* __restrict__ p,
+                                                           const double* __restrict__ q,
                                                            const double* __restrict__ dinv, double* __restrict__ part,
                                                            int64_t stride, double tol, int maxit,
                                                            int32_t* __restrict__ nactive) {
   __shared__ double sm[(kVecThreads / 32) * 2];
   pdl_enter();
-  const int64_t blk = blockIdx.x;
-  const int ls = blk_sub[blk];
+  const int64_t vb = blockIdx.x;
+  const int ls = vblk_sub[vb];
   if (!st[ls].active) return;
-  const int64_t i2 = blk * kVecThreads + threadIdx.x;  // index of the row pair
+  const int nt = vblk_ntile[vb];
+  const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;  // row-pair index
   const double a = st[ls].alpha;
-  const double2 pv = reinterpret_cast<const double2*>(p)[i2];
-  const double2 qv = reinterpret_cast<const double2*>(q)[i2];
-  double2 xv = reinterpret_cast<const double2*>(x)[i2];
-  double2 rv = reinterpret_cast<const double2*>(r)[i2];
-  const double2 dv = reinterpret_cast<const double2*>(dinv)[i2];
-  xv.x = fma(a, pv.x, xv.x);
-  xv.y = fma(a, pv.y, xv.y);
-  rv.x = fma(-a, qv.x, rv.x);
-  rv.y = fma(-a, qv.y, rv.y);
-  reinterpret_cast<double2*>(x)[i2] = xv;
-  reinterpret_cast<double2*>(r)[i2] = rv;
-  const double z0 = dv.x * rv.x, z1 = dv.y * rv.y;
-  double v[2] = {rv.x * z0 + rv.y * z1, rv.x * rv.x + rv.y * rv.y};
+  double2 pv[kVecTiles], qv[kVecTiles], xv[kVecTiles], rv[kVecTiles], dv[kVecTiles];
+#pragma unroll
+  for (int j = 0; j < kVecTiles; ++j)
+    if (j < nt) {
+      const int64_t i2 = p0 + (int64_t)j * kVecThreads;
+      pv[j] = reinterpret_cast<const double2*>(p)[i2];
+      qv[j] = reinterpret_cast<const double2*>(q)[i2];
+      xv[j] = reinterpret_cast<const double2*>(x)[i2];
+      rv[j] = reinterpret_cast<const double2*>(r)[i2];
+      dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
+    }
+  double v[2] = {0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < kVecTiles; ++j)
+    if (j < nt) {
+      const int64_t i2 = p0 + (int64_t)j * kVecThreads;
+      xv[j].x = fma(a, pv[j].x, xv[j].x);
+      xv[j].y = fma(a, pv[j].y, xv[j].y);
+      rv[j].x = fma(-a, qv[j].x, rv[j].x);
+      rv[j].y = fma(-a, qv[j].y, rv[j].y);
+      reinterpret_cast<double2*>(x)[i2] = xv[j];
+      reinterpret_cast<double2*>(r)[i2] = rv[j];
+      const double z0 = dv[j].x * rv[j].x, z1 = dv[j].y * rv[j].y;
+      v[0] += rv[j].x * z0 + rv[j].y * z1;
+      v[1] += rv[j].x * rv[j].x + rv[j].y * rv[j].y;
+    }
   block_sum<2, kVecThreads / 32>(v, sm);
   SubState& S = st[ls];
-  if (publish<2>(v, part, stride, blk, &S.cnt, S.nblk)) {
+  if (publish<2>(v, part, stride, vb, &S.cnt, S.nvblk)) {
     double t[2];
-    gather_partials<2, kVecThreads / 32>(t, part, stride, S.blk0, S.nblk, sm);
+    gather_partials<2, kVecThreads / 32>(t, part, stride, S.vblk0, S.nvblk, sm);
     if (threadIdx.x == 0) {
       S.cnt = 0;
       const double rz = t[0], rr = t[1];
@@ -235,52 +377,71 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(const int32_t* __rest
   }
 }
 
-// p = D^{-1} r + beta p  (128 threads x 2 rows per 256-row block)
-__global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restrict__ blk_sub,
+// p = D^{-1} r + beta p  (vector blocks as k_cg_update)
+__global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restrict__ vblk_sub,
+                                                        const int32_t* __restrict__ vblk_tile0,
+                                                        const int32_t* __restrict__ vblk_ntile,
                                                         const SubState* __restrict__ st, const double* __restrict__ r,
                                                         const double* __restrict__ dinv, double* __restrict__ p) {
   pdl_enter();
-  const int64_t blk = blockIdx.x;
-  const int ls = blk_sub[blk];
+  const int64_t vb = blockIdx.x;
+  const int ls = vblk_sub[vb];
   if (!st[ls].active) return;
-  const int64_t i2 = blk * kVecThreads + threadIdx.x;
+  const int nt = vblk_ntile[vb];
+  const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;
   const double beta = st[ls].beta;
-  const double2 rv = reinterpret_cast<const double2*>(r)[i2];
-  const double2 dv = reinterpret_cast<const double2*>(dinv)[i2];
-  double2 pv = reinterpret_cast<const double2*>(p)[i2];
-  pv.x = fma(beta, pv.x, dv.x * rv.x);
-  pv.y = fma(beta, pv.y, dv.y * rv.y);
-  reinterpret_cast<double2*>(p)[i2] = pv;
+  double2 rv[kVecTiles], dv[kVecTiles], pv[kVecTiles];
+#pragma unroll
+  for (int j = 0; j < kVecTiles; ++j)
+    if (j < nt) {
+      const int64_t i2 = p0 + (int64_t)j * kVecThreads;
+      rv[j] = reinterpret_cast<const double2*>(r)[i2];
+      dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
+      pv[j] = reinterpret_cast<const double2*>(p)[i2];
+    }
+#pragma unroll
+  for (int j = 0; j < kVecTiles; ++j)
+    if (j < nt) {
+      pv[j].x = fma(beta, pv[j].x, dv[j].x * rv[j].x);
+      pv[j].y = fma(beta, pv[j].y, dv[j].y * rv[j].y);
+      reinterpret_cast<double2*>(p)[p0 + (int64_t)j * kVecThreads] = pv[j];
+    }
 }
 
 // Warm start: rhs = b + P^T lambda ; r = rhs - K_s x ; z = D^{-1} r ; p = z ;
 // rho = r.z, ||r||^2, ||rhs||^2 ; zero rhs -> x = 0 after 0 iterations.
-__global__ void __launch_bounds__(kThreads) k_warm(SellDev A, const int32_t* __restrict__ blk_sub,
+template <int V>
+__global__ void OSM_SPMV_BOUNDS(V) k_warm(SellDev A, const int32_t* __restrict__ blk_sub,
                                                    SubState* __restrict__ st, const double* __restrict__ x,
                                                    const double* __restrict__ b, const int32_t* __restrict__ islot,
                                                    const double* __restrict__ lam_all, const double* __restrict__ dinv,
                                                    double* __restrict__ r, double* __restrict__ p,
                                                    double* __restrict__ part, int64_t stride, double tol,
                                                    int32_t* __restrict__ nactive) {
-  __shared__ double sm[kSlicesPerBlock * 3];
+  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  __shared__ double sm[NW * 3];
+  extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t slice = blk * kSlicesPerBlock + warp;
-  const int64_t row = slice * kWarp + lane;
-  const double ax = sell_row<kChunk>(A, slice, lane, x);
-  const int sl = islot[row];
-  const double rhs = sl >= 0 ? b[row] + lam_all[sl] : b[row];
-  const double rv = rhs - ax;
-  const double z = dinv[row] * rv;
-  r[row] = rv;
-  p[row] = z;
-  double v[3] = {rv * z, rv * rv, rhs * rhs};
-  block_sum<3>(v, sm);
+  const int64_t row = blk * kRowsPerBlock + threadIdx.x;
+  const double ax = tile_row<V>(A, blk, x, dsm);
+  double v[3] = {0.0, 0.0, 0.0};
+  if (threadIdx.x < kRowsPerBlock) {
+    const int sl = islot[row];
+    const double rhs = sl >= 0 ? b[row] + lam_all[sl] : b[row];
+    const double rv = rhs - ax;
+    const double z = dinv[row] * rv;
+    r[row] = rv;
+    p[row] = z;
+    v[0] = rv * z;
+    v[1] = rv * rv;
+    v[2] = rhs * rhs;
+  }
+  block_sum<3, NW>(v, sm);
   SubState& S = st[ls];
   if (publish<3>(v, part, stride, blk, &S.cnt, S.nblk)) {
     double t[3];
-    gather_partials<3>(t, part, stride, S.blk0, S.nblk, sm);
+    gather_partials<3, NW>(t, part, stride, S.blk0, S.nblk, sm);
     if (threadIdx.x == 0) {
       S.cnt = 0;
       S.rho = t[0];
@@ -310,17 +471,19 @@ __global__ void __launch_bounds__(kThreads) k_zero_if(const int32_t* __restrict_
 
 // ---------------------------------------------------------------- Schwarz interface kernels
 
-// Robin data to send: g_{s->t} = (alpha_s + alpha_t) M_Gamma u_s|Gamma - lambda_s ;
-// also the trace u_s|Gamma for gluing.  Discrete form of PAPER.md:64-71.
+// Robin data to send: g_{s->t} = (A_s + A_t) u_s|Gamma - lambda_s with
+// A = p M_Gamma + q S_Gamma (OO0: q = 0); also the trace u_s|Gamma for gluing.  Discrete
+// form of PAPER.md:64-71.
 __global__ void k_trace(const SideDev* __restrict__ sides, int64_t nG, const int32_t* __restrict__ mrow,
                         const int32_t* __restrict__ mcol, const double* __restrict__ mval,
-                        const double* __restrict__ x) {
+                        const double* __restrict__ sval, const double* __restrict__ x) {
   const SideDev S = sides[blockIdx.y];
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= nG) return;
   double mu = 0.0;
-  for (int j = mrow[g]; j < mrow[g + 1]; ++j) mu = fma(mval[j], x[S.map[mcol[j]]], mu);
-  S.out[g] = S.alpha_sum * mu - S.lam[g];
+  for (int j = mrow[g]; j < mrow[g + 1]; ++j)
+    mu = fma(fma(S.alpha_sum, mval[j], S.q_sum * sval[j]), x[S.map[mcol[j]]], mu);
+  S.out[g] = mu - S.lam[g];
   S.out[nG + g] = x[S.map[g]];
 }
 
@@ -349,26 +512,31 @@ __global__ void __launch_bounds__(kThreads) k_glue(int64_t nrows, const int32_t*
 
 // Glued residual, subdomain part: w = b - K_s u~ ; interior rows add w^2 to
 // the subdomain's sum, interface rows keep w for the Robin correction and the owner sum.
-__global__ void __launch_bounds__(kThreads) k_resid(SellDev A, const int32_t* __restrict__ blk_sub,
+template <int V>
+__global__ void OSM_SPMV_BOUNDS(V) k_resid(SellDev A, const int32_t* __restrict__ blk_sub,
                                                     SubState* __restrict__ st, const double* __restrict__ ut,
                                                     const double* __restrict__ b, const int32_t* __restrict__ islot,
                                                     double* __restrict__ wif_all, double* __restrict__ part,
                                                     int64_t stride) {
-  __shared__ double sm[kSlicesPerBlock * 1];
+  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  __shared__ double sm[NW * 1];
+  extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t slice = blk * kSlicesPerBlock + warp;
-  const int64_t row = slice * kWarp + lane;
-  const double w = b[row] - sell_row<kChunk>(A, slice, lane, ut);
-  const int sl = islot[row];
-  if (sl >= 0) wif_all[sl] = w;
-  double v[1] = {sl == -1 ? w * w : 0.0};
-  block_sum<1>(v, sm);
+  const int64_t row = blk * kRowsPerBlock + threadIdx.x;
+  const double ax = tile_row<V>(A, blk, ut, dsm);
+  double v[1] = {0.0};
+  if (threadIdx.x < kRowsPerBlock) {
+    const double w = b[row] - ax;
+    const int sl = islot[row];
+    if (sl >= 0) wif_all[sl] = w;
+    v[0] = sl == -1 ? w * w : 0.0;
+  }
+  block_sum<1, NW>(v, sm);
   SubState& S = st[ls];
   if (publish<1>(v, part, stride, blk, &S.cnt, S.nblk)) {
     double t[1];
-    gather_partials<1>(t, part, stride, S.blk0, S.nblk, sm);
+    gather_partials<1, NW>(t, part, stride, S.blk0, S.nblk, sm);
     if (threadIdx.x == 0) {
       S.cnt = 0;
       S.resid = t[0];
@@ -376,16 +544,17 @@ __global__ void __launch_bounds__(kThreads) k_resid(SellDev A, const int32_t* __
   }
 }
 
-// Interface rows: w = b - K^N u~ = (b - K_s u~) + alpha_own M u~|Gamma ; publish w in the outbox.
+// Interface rows: w = b - K^N u~ = (b - K_s u~) + A_own u~|Gamma ; publish w in the outbox.
 __global__ void k_iface_w(const SideDev* __restrict__ sides, int64_t nG, const int32_t* __restrict__ mrow,
                           const int32_t* __restrict__ mcol, const double* __restrict__ mval,
-                          const double* __restrict__ ut) {
+                          const double* __restrict__ sval, const double* __restrict__ ut) {
   const SideDev S = sides[blockIdx.y];
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= nG) return;
   double mu = 0.0;
-  for (int j = mrow[g]; j < mrow[g + 1]; ++j) mu = fma(mval[j], ut[S.map[mcol[j]]], mu);
-  const double w = fma(S.alpha_own, mu, S.wif[g]);
+  for (int j = mrow[g]; j < mrow[g + 1]; ++j)
+    mu = fma(fma(S.alpha_own, mval[j], S.q_own * sval[j]), ut[S.map[mcol[j]]], mu);
+  const double w = S.wif[g] + mu;
   S.wif[g] = w;
   S.out[2 * nG + g] = w;
 }
@@ -419,10 +588,27 @@ SellDev sell_of(const Ctx& c) { return SellDev{c.sell_val, c.sell_col, c.sell_so
 
 }  // namespace
 
+static int spmv_smem(const Ctx& c) { return c.spmv_variant == 1 ? kBulkSmem : 0; }
+
+void spmv_init_attributes() {
+  static bool done = false;
+  if (done) return;
+  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
+  OSM_CUDA(cudaFuncSetAttribute(k_warm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
+  OSM_CUDA(cudaFuncSetAttribute(k_resid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
+  done = true;
+}
+
 void launch_warm(Ctx& c, double tol, int) {
   timer_begin(c, T_WARM);
-  k_warm<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot, c.lam_all,
-                                                            c.dinv, c.r, c.p, c.part, c.nblk_total, tol, c.d_nactive);
+  if (c.spmv_variant == 1)
+    k_warm<1><<<(unsigned)c.nblk_total, kBulkThreads, spmv_smem(c), c.stream>>>(
+        sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot, c.lam_all, c.dinv, c.r, c.p, c.part, c.nblk_total, tol,
+        c.d_nactive);
+  else
+    k_warm<0><<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
+                                                                 c.lam_all, c.dinv, c.r, c.p, c.part, c.nblk_total,
+                                                                 tol, c.d_nactive);
   OSM_CHECK_LAUNCH();
   ++c.launches;
   timer_end(c, T_WARM);
@@ -435,11 +621,12 @@ void launch_zero_if(Ctx& c) {
 }
 
 template <typename... KArgs, typename... Args>
-static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsigned block, Args... args) {
+static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                       Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = c.stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -451,25 +638,33 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
 
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
-  launch_pdl(c, k_cg_spmv, (unsigned)c.nblk_total, kThreads, sell_of(c), (const int32_t*)c.blk_sub, c.st,
-             (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
+  if (c.spmv_variant == 1)
+    launch_pdl(c, k_cg_spmv<1>, (unsigned)c.nblk_total, kBulkThreads, (size_t)kBulkSmem, sell_of(c),
+               (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
+  else if (c.spmv_variant == 2)
+    launch_pdl(c, k_cg_spmv<2>, (unsigned)c.nblk_total, kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub,
+               c.st, (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
+  else
+    launch_pdl(c, k_cg_spmv<0>, (unsigned)c.nblk_total, kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub,
+               c.st, (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
   ++c.launches;
   timer_end(c, T_SPMV);
 }
 
 void launch_cg_update(Ctx& c, double tol, int maxit) {
   timer_begin(c, T_UPDATE);
-  launch_pdl(c, k_cg_update, (unsigned)c.nblk_total, kVecThreads, (const int32_t*)c.blk_sub, c.st, c.x, c.r,
-             (const double*)c.p, (const double*)c.q, (const double*)c.dinv, c.part, c.nblk_total, tol, maxit,
-             c.d_nactive);
+  launch_pdl(c, k_cg_update, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+             (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
+             (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive);
   ++c.launches;
   timer_end(c, T_UPDATE);
 }
 
 void launch_cg_dir(Ctx& c) {
   timer_begin(c, T_DIR);
-  launch_pdl(c, k_cg_dir, (unsigned)c.nblk_total, kVecThreads, (const int32_t*)c.blk_sub, (const SubState*)c.st,
-             (const double*)c.r, (const double*)c.dinv, c.p);
+  launch_pdl(c, k_cg_dir, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+             (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, (const SubState*)c.st, (const double*)c.r,
+             (const double*)c.dinv, c.p);
   ++c.launches;
   timer_end(c, T_DIR);
 }
@@ -477,7 +672,7 @@ void launch_cg_dir(Ctx& c) {
 void launch_trace(Ctx& c) {
   if (c.sides.empty()) return;
   dim3 grid((unsigned)ceil_div(c.nG, 256), (unsigned)c.sides.size());
-  k_trace<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG, c.d_mrow, c.d_mcol, c.d_mval, c.x);
+  k_trace<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG, c.d_mrow, c.d_mcol, c.d_mval, c.d_sval, c.x);
   OSM_CHECK_LAUNCH();
   ++c.launches;
 }
@@ -499,8 +694,13 @@ void launch_glue(Ctx& c, int zero) {
 
 void launch_resid(Ctx& c) {
   timer_begin(c, T_RESID);
-  k_resid<<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot,
-                                                             c.wif_all, c.part, c.nblk_total);
+  if (c.spmv_variant == 1)
+    k_resid<1><<<(unsigned)c.nblk_total, kBulkThreads, spmv_smem(c), c.stream>>>(sell_of(c), c.blk_sub, c.st, c.ut, c.b,
+                                                                             c.islot, c.wif_all, c.part,
+                                                                             c.nblk_total);
+  else
+    k_resid<0><<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot,
+                                                                  c.wif_all, c.part, c.nblk_total);
   OSM_CHECK_LAUNCH();
   ++c.launches;
   timer_end(c, T_RESID);
@@ -509,7 +709,7 @@ void launch_resid(Ctx& c) {
 void launch_iface_w(Ctx& c) {
   if (c.sides.empty()) return;
   dim3 grid((unsigned)ceil_div(c.nG, 256), (unsigned)c.sides.size());
-  k_iface_w<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG, c.d_mrow, c.d_mcol, c.d_mval, c.ut);
+  k_iface_w<<<grid, 256, 0, c.stream>>>(c.d_sides, c.nG, c.d_mrow, c.d_mcol, c.d_mval, c.d_sval, c.ut);
   OSM_CHECK_LAUNCH();
   ++c.launches;
 }

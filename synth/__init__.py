@@ -82,13 +82,25 @@ def alpha_candidates(alpha0: float, B: int = 64, seed: int = 2112):
 CONFIGS = {
     "C1": dict(nx=8, ny=8, nz=8, lx=1.0, ly=1.0, lz=1.0, order=1, nsub=2, field="ball", alpha=20.0),
     "C2": dict(nx=32, ny=32, nz=32, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=2, field="ball", alpha=56.0),
-    # C3 alpha: two-sided OO0 (Table 1 'oo0_unsymmetric' form), (alpha_1, alpha_2) in 1/m,
-    # frozen from the GPU alpha scans in profiles/alpha_scan_C3.md (best: 159 outer iterations to 1e-8).
+    # C3 transmission: two-sided OO2 (Table 1 'oo2_unsymmetric' form; Table 2's label
+    # 'synch_cg_res_case1oo2', indicates OO2 for the timed runs): robin = (p1, p2, q1, q2)
+    # in (1/m, 1/m, m, m), frozen from the GPU scans in profiles/r01_oo2_scan*_C3.log (24 outer
+    # iterations to 1e-8).  The best two-sided OO0 pair (0.1, 5e-4) needs 159 (profiles/r01_alpha_scan3).
     "C3": dict(nx=64, ny=64, nz=64, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
-               order=2, nsub=8, field="chicxulub", alpha=(0.1, 5.0e-4)),
+               order=2, nsub=8, field="chicxulub", alpha=(0.1, 5.0e-4), robin=(5.0e-4, 1.0e-4, 2000.0, 2000.0)),
     "C5": dict(nx=192, ny=192, nz=192, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
                order=2, nsub=8, field="chicxulub", alpha=None),
 }
+
+
+def robin(cfg: dict):
+    """(p_left, q_left, p_right, q_right) per interface: OO2 when cfg has 'robin', else OO0 from 'alpha'."""
+    n = max(cfg["nsub"] - 1, 0)
+    if cfg.get("robin") is not None:
+        p1, p2, q1, q2 = cfg["robin"]
+        return np.full(n, p1), np.full(n, q1), np.full(n, p2), np.full(n, q2)
+    al, ar = alphas(cfg)
+    return al, np.zeros(n), ar, np.zeros(n)
 
 
 def alphas(cfg: dict, alpha=None):

@@ -4,10 +4,10 @@ import numpy as np
 from oracle import mesh, schwarz
 
 
-def oracle_run(cfg, drho, alpha_l, alpha_r, tol_outer=1e-8, max_outer=500, tol_inner=1e-10, warm=True):
+def oracle_run(cfg, drho, alpha_l, alpha_r, tol_outer=1e-8, max_outer=500, tol_inner=1e-10, warm=True, q=None):
     box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
     prob = schwarz.build_problem(box, cfg["nsub"], drho=drho)
-    A = schwarz.robin_operators(prob, alpha_l, alpha_r)
+    A = schwarz.robin_operators(prob, alpha_l, alpha_r, *(q if q is not None else (None, None)))
     rep = schwarz.schwarz(prob, A, tol_outer=tol_outer, max_outer=max_outer, tol_inner=tol_inner, warm_start=warm)
     return prob, rep
 

@@ -24,7 +24,15 @@ CASES = {
     "p2_ragged_S3_unsym": (dict(nx=10, ny=5, nz=4, lx=1.0, ly=0.6, lz=0.5, order=2, nsub=3), "random", 30.0, 12.0),
     "p1_thin_S4": (dict(nx=12, ny=9, nz=3, lx=250e3, ly=250e3, lz=15e3, order=1, nsub=4), "chicxulub", 3e-4, 4e-4),
     "p2_single": (dict(nx=5, ny=4, nz=6, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=1), "random", None, None),
+    # OO2 two-sided (Table 1 oo2_unsymmetric form): (p1, q1), (p2, q2)
+    "p2_oo2_S3": (dict(nx=8, ny=5, nz=4, lx=1.0, ly=0.7, lz=0.5, order=2, nsub=3), "random", (10.0, 0.05), (3.0, 0.2)),
+    "p1_oo2_thin_S4": (dict(nx=12, ny=9, nz=3, lx=250e3, ly=250e3, lz=15e3, order=1, nsub=4), "chicxulub",
+                       (1e-4, 1e3), (3e-4, 2e2)),
 }
+
+
+def _pq(a):
+    return (a, 0.0) if not isinstance(a, tuple) else a
 
 
 def _field(cfg, kind):
@@ -42,7 +50,8 @@ def _gpu(cfg, drho, al, ar):
     o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
     o.decompose(cfg["nsub"])
     if cfg["nsub"] > 1:
-        o.set_robin(np.full(cfg["nsub"] - 1, al), np.full(cfg["nsub"] - 1, ar))
+        (pl, ql), (pr, qr) = _pq(al), _pq(ar)
+        o.set_robin2(pl, ql, pr, qr)
     o.assemble()
     o.upload_density(drho)
     return o
@@ -53,7 +62,8 @@ def case(request):
     cfg, kind, al, ar = CASES[request.param]
     drho = _field(cfg, kind)
     S = cfg["nsub"]
-    prob, rep = oracle_run(cfg, drho, [al] * (S - 1), [ar] * (S - 1))
+    (pl, ql), (pr, qr) = _pq(al), _pq(ar)
+    prob, rep = oracle_run(cfg, drho, [pl] * (S - 1), [pr] * (S - 1), q=([ql] * (S - 1), [qr] * (S - 1)))
     o = _gpu(cfg, drho, al, ar)
     st, grep = o.solve(tol_outer=1e-8, max_outer=500)
     yield dict(name=request.param, cfg=cfg, prob=prob, rep=rep, o=o, st=st, grep=grep, al=al, ar=ar)
@@ -81,6 +91,10 @@ def test_interface_maps_and_mass(case):
         M = prob.MG
         assert np.array_equal(rp, M.indptr.astype(np.int64)) and np.array_equal(col, M.indices.astype(np.int32))
         assert np.abs(val - M.data).max() <= 1e-13 * np.abs(M.data).max()
+        sv = o.interface_stiffness()
+        Sg = prob.SG
+        assert np.array_equal(Sg.indptr, M.indptr) and np.array_equal(Sg.indices, M.indices)
+        assert np.abs(sv - Sg.data).max() <= 1e-13 * np.abs(Sg.data).max()
 
 
 def test_history_and_inner_counts(case):

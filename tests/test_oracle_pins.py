@@ -299,6 +299,44 @@ def test_interface_mass_quadratic_form():
         assert abs(fe.tri_mass(order, 0.37).sum() - 0.37) < 1e-15
 
 
+def test_interface_stiffness_quadratic_form():
+    """OO2 plane operator: v^T S v = int |grad_tau v_h|^2 by quadrature of the FE function's own
+    gradient (finite differences of the basis expansion are not used: the gradient of a random
+    quadratic q interpolated exactly); S symmetric bitwise; unconstrained row sums zero."""
+    rng = np.random.default_rng(9)
+    bary, w = quadrature.tri_rule(6)
+    for order in (1, 2):
+        box = mesh.Box(2, 3, 4, 1.0, 0.6, 0.9, order)
+        S = fe.interface_stiffness(box)
+        assert (S != S.T).nnz == 0
+        M = fe.interface_mass(box)
+        assert np.array_equal(S.indptr, M.indptr) and np.array_equal(S.indices, M.indices)  # same pattern
+        # element level: energy of an exactly represented polynomial on one triangle
+        Y = np.array([[0.0, 0.0], [0.3, 0.0], [0.3, 0.2]])
+        Kt = fe.tri_stiffness(order, Y)
+        assert np.allclose(Kt.sum(axis=1), 0, atol=1e-14)
+        c = rng.standard_normal(6)
+        q = lambda y, z: c[0] + c[1] * y + c[2] * z + (c[3] * y * y + c[4] * y * z + c[5] * z * z) * (order == 2)  # noqa
+        gq = lambda y, z: np.stack([c[1] + (2 * c[3] * y + c[4] * z) * (order == 2),  # noqa
+                                    c[2] + (c[4] * y + 2 * c[5] * z) * (order == 2)], axis=-1)
+        nodes = Y if order == 1 else np.concatenate([Y, [(Y[0] + Y[1]) / 2, (Y[1] + Y[2]) / 2, (Y[0] + Y[2]) / 2]])
+        v = q(nodes[:, 0], nodes[:, 1])
+        X = bary @ Y
+        g = gq(X[:, 0], X[:, 1])
+        exact = 0.5 * 0.3 * 0.2 * np.sum(w * np.sum(g * g, axis=1))
+        assert abs(v @ Kt @ v - exact) <= 1e-13 * max(1.0, exact)
+
+
+def test_oo2_schwarz_equals_monolithic():
+    """OO2 transmission (p M + q S) keeps the fixed point: Schwarz = monolithic."""
+    prob = _prob(6, 2, 3)
+    A = schwarz.robin_operators(prob, [10.0, 10.0], [3.0, 3.0], [0.05, 0.05], [0.2, 0.2])
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-10, tol_inner=1e-12)
+    assert rep.converged
+    us = schwarz.monolithic(prob)
+    assert np.linalg.norm(rep.ut - us) / np.linalg.norm(us) < 1e-8
+
+
 @pytest.mark.parametrize("n,err", list(zip(GOLD["manufactured_p2_l2"]["n"][:2], GOLD["manufactured_p2_l2"]["err"][:2])))
 def test_manufactured_p2(n, err):
     """P2 L2 error and order 3 for u = sin sin sin (BASELINE north_star 'optimal L2 order')."""

@@ -35,24 +35,27 @@ drho = synth.density(cfg)
 
 
 def parse(s):
-    if ":" in s:
-        l, r = s.split(":")
-        return float(l), float(r)
-    return float(s), float(s)
+    """p | p1:p2 | p1:p2:q1:q2 (OO2)."""
+    v = [float(t) for t in s.split(":")]
+    if len(v) == 1:
+        return v[0], v[0], 0.0, 0.0
+    if len(v) == 2:
+        return v[0], v[1], 0.0, 0.0
+    return v[0], v[1], v[2], v[3]
 
 
-al0, ar0 = parse(a.alphas[0])
+al0, ar0, _, _ = parse(a.alphas[0])
 o = P.setup(cfg, drho, alpha=(np.full(cfg["nsub"] - 1, al0), np.full(cfg["nsub"] - 1, ar0)))
 rows = []
 for s in a.alphas:
-    al, ar = parse(s)
-    o.set_robin(np.full(cfg["nsub"] - 1, al), np.full(cfg["nsub"] - 1, ar))
+    al, ar, ql, qr = parse(s)
+    o.set_robin2(al, ql, ar, qr)
     t = time.time()
     st, rep = o.solve(tol_outer=a.tol, max_outer=a.max_outer)
     h = o.history()
     m = len(h) // 2
     rate = float((h[-1] / h[m]) ** (1.0 / max(1, len(h) - 1 - m))) if len(h) > 4 else None
-    rows.append(dict(alpha_l=al, alpha_r=ar, status=st, outer=rep.outer_iters, inner_total=rep.inner_total,
+    rows.append(dict(alpha_l=al, alpha_r=ar, q_l=ql, q_r=qr, status=st, outer=rep.outer_iters, inner_total=rep.inner_total,
                      h=rep.h_final, rate=rate, seconds=time.time() - t))
     print(json.dumps(rows[-1]), flush=True)
 best = min(rows, key=lambda r: (r["status"] != 0, r["outer"] if r["status"] == 0 else r["rate"]))

@@ -249,6 +249,32 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * creation (every kernel of setup, solve and readback). */
 osm_status osm_get_launch_count(osm_ctx* ctx, int64_t* n);
 
+/* ---- Transmission-coefficient optimisation (host only, no GPU needed) ----
+ * Fourier convergence rate of the two-subdomain OSM on R^2, f = 0: with
+ * Lambda_s(k) = p_s + q_s k^2 (sign reading SURVEY Q25),
+ *   rho(k) = |(Lambda_1 - k)/(Lambda_1 + k)| |(Lambda_2 - k)/(Lambda_2 + k)|.
+ * osm_rate_max: max over nsamp geometric samples of [kmin, kmax] (PAPER.md:82 cost), and its argmax.
+ * osm_rate_curve: rho at n given frequencies (Fig. "Fourier convergence rate"). */
+osm_status osm_rate_max(double p1, double q1, double p2, double q2, double kmin, double kmax, int nsamp, double* rho,
+                        double* kargmax);
+osm_status osm_rate_curve(double p1, double q1, double p2, double q2, const double* k, int n, double* rho);
+
+/* CMA-ES (population lambda = 25 in the paper).  Standard
+ * (mu/mu_w, lambda) updates with cumulative step-size adaptation and rank-one + rank-mu covariance
+ * adaptation.  ask: the caller supplies lambda x n standard normal draws z (row-major) and gets
+ * x_k = m + sigma C^{1/2} z_k (symmetric square root).  tell: lambda costs (non-finite = worst; ties
+ * broken by sample index).  should_stop: 1 = max_iter reached, 2 = spread of the best cost over the
+ * last 10 + ceil(30 n / lambda) generations < ftol (7200 / 5e-11), 3 = sigma sqrt(max
+ * eig C) < 1e-14.  The handle owns its state; osm_cmaes_destroy frees it. */
+typedef struct osm_cmaes osm_cmaes;
+osm_status osm_cmaes_create(int n, int lambda, const double* mean, double sigma0, osm_cmaes** out);
+void osm_cmaes_destroy(osm_cmaes* es);
+osm_status osm_cmaes_ask(osm_cmaes* es, const double* z, double* x);
+osm_status osm_cmaes_tell(osm_cmaes* es, const double* f);
+osm_status osm_cmaes_state(osm_cmaes* es, double* mean, double* sigma, double* cov, double* best_x, double* best_f,
+                           int* generation);
+osm_status osm_cmaes_should_stop(osm_cmaes* es, int max_iter, double ftol, int* stop);
+
 #ifdef __cplusplus
 }
 #endif

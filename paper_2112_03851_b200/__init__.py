@@ -31,7 +31,9 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_trace", "osm_get_csr", "osm_get_interface_map", "osm_get_interface_mass",
                "osm_set_kernel_timing", "osm_get_kernel_timing", "osm_get_traffic_model", "osm_get_launch_count", "osm_solve_batch",
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
-               "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness"]
+               "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
+               "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
+               "osm_cmaes_should_stop"]
 
 
 class MeshDesc(C.Structure):
@@ -102,6 +104,14 @@ _sigs = {
     "osm_get_batch_local_solution": (C.c_int, [_P, C.c_int, C.c_int, _pd, _pi64]),
     "osm_set_robin2": (C.c_int, [_P, _pd, _pd, _pd, _pd]),
     "osm_get_interface_stiffness": (C.c_int, [_P, _pd, _pi64]),
+    "osm_rate_max": (C.c_int, [C.c_double] * 6 + [C.c_int, _pd, _pd]),
+    "osm_rate_curve": (C.c_int, [C.c_double] * 4 + [_pd, C.c_int, _pd]),
+    "osm_cmaes_create": (C.c_int, [C.c_int, C.c_int, _pd, C.c_double, C.POINTER(_P)]),
+    "osm_cmaes_destroy": (None, [_P]),
+    "osm_cmaes_ask": (C.c_int, [_P, _pd, _pd]),
+    "osm_cmaes_tell": (C.c_int, [_P, _pd]),
+    "osm_cmaes_state": (C.c_int, [_P, _pd, _pd, _pd, _pd, _pd, _pint]),
+    "osm_cmaes_should_stop": (C.c_int, [_P, C.c_int, C.c_double, _pint]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
 for _name, (_res, _args) in _sigs.items():
@@ -134,6 +144,71 @@ def plan(nx, nsub, nranks, rank):
     _check(_lib.osm_plan(nx, nsub, nranks, rank, C.byref(sb), C.byref(se), arr, n.value, C.byref(n)))
     return sb.value, se.value, [dict(iface=a.iface, side=a.side, sub=a.sub, remote=a.remote, peer=a.peer)
                                 for a in arr[:n.value]]
+
+
+def rate_max(p1, q1, p2, q2, kmin, kmax, nsamp=10000):
+    """Fourier convergence-rate cost max_k rho(k) (osm_rate_max): (rho_max, argmax k)."""
+    r, k = C.c_double(), C.c_double()
+    _check(_lib.osm_rate_max(p1, q1, p2, q2, kmin, kmax, nsamp, C.byref(r), C.byref(k)))
+    return r.value, k.value
+
+
+def rate_curve(p1, q1, p2, q2, k):
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    out = np.zeros_like(k)
+    _check(_lib.osm_rate_curve(p1, q1, p2, q2, _ptr(k, C.c_double), k.size, _ptr(out, C.c_double)))
+    return out
+
+
+class CMAES:
+    """Native CMA-ES (osm_cmaes_*): ask(z) with caller-supplied standard normals, tell(f)."""
+
+    def __init__(self, mean, sigma0, lam=25):
+        m = np.ascontiguousarray(mean, dtype=np.float64)
+        self.n, self.lam = m.size, lam
+        h = _P()
+        _check(_lib.osm_cmaes_create(self.n, lam, _ptr(m, C.c_double), float(sigma0), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.osm_cmaes_destroy(self._h)
+            self._h = None
+
+    def ask(self, z):
+        z = np.ascontiguousarray(z, dtype=np.float64).reshape(self.lam, self.n)
+        x = np.zeros((self.lam, self.n))
+        _check(_lib.osm_cmaes_ask(self._h, _ptr(z, C.c_double), _ptr(x, C.c_double)))
+        return x
+
+    def tell(self, f):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        _check(_lib.osm_cmaes_tell(self._h, _ptr(f, C.c_double)))
+
+    def state(self):
+        m, bx, cov = np.zeros(self.n), np.zeros(self.n), np.zeros((self.n, self.n))
+        sig, bf, g = C.c_double(), C.c_double(), C.c_int()
+        _check(_lib.osm_cmaes_state(self._h, _ptr(m, C.c_double), C.byref(sig), _ptr(cov, C.c_double),
+                                    _ptr(bx, C.c_double), C.byref(bf), C.byref(g)))
+        return dict(mean=m, sigma=sig.value, C=cov, best_x=bx, best_f=bf.value, generation=g.value)
+
+    def should_stop(self, max_iter=7200, ftol=5e-11):
+        st = C.c_int()
+        _check(_lib.osm_cmaes_should_stop(self._h, max_iter, ftol, C.byref(st)))
+        return st.value
+
+
+def cmaes_minimize(fun, mean, sigma0, z_stream, lam=25, max_iter=7200, ftol=5e-11):
+    """ask/tell loop with the native CMA-ES; z_stream(g) -> lambda x n standard normals."""
+    es = CMAES(mean, sigma0, lam)
+    g = 0
+    while True:
+        X = es.ask(z_stream(g))
+        es.tell([fun(x) for x in X])
+        g += 1
+        if es.should_stop(max_iter, ftol):
+            break
+    return es
 
 
 def abi_version():

@@ -41,6 +41,9 @@ struct SellDev {
   const int32_t* col;
   const int64_t* toff;
   const int32_t* twidth;
+  const uint16_t* vidx;  // value-indexed copy (variant 3): dictionary index per entry
+  const int16_t* cidx;   // column offset col - row per entry
+  const double* dict;    // distinct values
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -209,8 +212,21 @@ struct Ctx {
   double graph_tol = -1;
   int graph_maxit = -1;
   bool use_graph = true;
-  int sigma = 32768;  // SELL sorting window (rows); SELL-256 padding 0.9% at C3
-  int spmv_variant = 2;  // 0: LDG rows, 2: LDG rows at 32 regs (default, 8 blocks/SM), 1: warp-specialized cp.async.bulk pipeline
+  int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
+  int spmv_variant = 3;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
+                         // pipeline, 3: value-indexed SELL (16-bit value index + 16-bit column offset; default)
+
+  // value-indexed SELL (vi.cu)
+  bool vi_ok = false;
+  uint16_t* vi_idx = nullptr;
+  int16_t* vi_col = nullptr;
+  double* vi_dict = nullptr;
+  int64_t vi_ndict = 0, vi_nbase = 0;
+  struct FoldTuple {
+    int32_t side;
+    double kn, m, s;
+  };
+  std::vector<FoldTuple> vi_fold_tuples;
 
   // instrumentation
   bool timing = false;
@@ -222,7 +238,7 @@ struct Ctx {
   int32_t* batch_sub_nblk = nullptr;
 
   // traffic model of the last solve
-  double traffic[6] = {0};
+  double traffic[8] = {0};
   mutable int64_t launches = 0;  // kernel launches issued by this context
 };
 
@@ -258,6 +274,10 @@ void batch_free(Ctx& c);
 double fnorm2_of(Ctx& c);  // ||f||^2 of the glued global system (osm.cu)
 
 void spmv_init_attributes();
+void vi_build(Ctx& c);
+void vi_free(Ctx& c);
+void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side);
+int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)
 
 // timing helpers (osm.cu)
 void timer_begin(Ctx& c, int id);

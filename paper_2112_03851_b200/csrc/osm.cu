@@ -87,6 +87,7 @@ static void drop_graph(Ctx& c) {
 static void free_assembly(Ctx& c) {
   drop_graph(c);
   batch_free(c);
+  vi_free(c);
   for (auto& s : c.subs) {
     dfree(s.rowptr);
     dfree(s.col);
@@ -228,7 +229,17 @@ static void assemble(Ctx& c) {
     perm.assign(S.npad, -1);
     iperm.assign(S.n, -1);
     std::vector<int32_t> idx;
-    const int64_t sigma = std::max(kRowsPerBlock, c.sigma);
+    // sigma: fixed by OSM_SIGMA, else the largest power of two (<= 32768) that keeps every column
+    // offset col - row of the internal order within int16 (offset <= sigma + stencil reach), so
+    // the value-indexed copy can use 16-bit offsets; 32768 when no such sigma >= 1024 exists.
+    int64_t sigma = c.sigma;
+    if (sigma <= 0) {
+      const int64_t reach = 2 * S.g.nI * S.g.nJ + 2 * S.g.nI + 2;
+      sigma = 32768;
+      while (sigma > 1024 && sigma + reach > 32767) sigma /= 2;
+      if (sigma + reach > 32767) sigma = 32768;
+    }
+    sigma = std::max<int64_t>(kRowsPerBlock, sigma);
     for (int64_t w0 = 0; w0 < S.n; w0 += sigma) {
       const int64_t w1 = std::min<int64_t>(S.n, w0 + sigma);
       idx.resize(w1 - w0);
@@ -367,6 +378,7 @@ static void assemble(Ctx& c) {
     c.sides[k].fold0 = k * mnnz;
     launch_fold_build(c, c.sides[k], c.subs[c.sides[k].sub]);
   }
+  vi_build(c);  // value-indexed hot copy (from the unfolded K^N values)
 
   // --- reductions and device side table
   c.part = dalloc<double>(3 * c.nblk_total);
@@ -452,6 +464,7 @@ static void apply_robin(Ctx& c) {
   OSM_CUDA(cudaStreamSynchronize(c.stream));
   dfree(d_a);
   dfree(d_q);
+  vi_apply_robin(c, a, qv);
   if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
   c.robin_dirty = false;
 }
@@ -653,11 +666,15 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   // traffic model: algorithmic bytes per CG iteration per subdomain x its iterations
   for (double& t : c.traffic) t = 0;
   const int nloc = c.s_end - c.s_begin;
+  const bool vi = spmv_variant_of(c) == 3;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
     for (size_t k = S.s; k < c.inner.size(); k += c.nsub) its += std::max(0, c.inner[k]);
-    c.traffic[0] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);
+    // SpMV bytes in the format launched: fp64 SELL 12 B/entry (+ CSR-equivalent 4 B/row) or
+    // value-indexed 4 B/entry (index + offset; the dictionary is L1-resident); vectors p, q 16 B/row
+    c.traffic[0] += (double)its * ((vi ? 4.0 * S.nnz : 12.0 * S.nnz + 4.0 * (S.n + 1)) + 16.0 * S.n);
+    c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
     c.traffic[1] += (double)its * 56.0 * S.n;
     c.traffic[2] += (double)its * 32.0 * S.n;
     c.traffic[3] += (double)(S.sell_entries - S.nnz);
@@ -1165,7 +1182,7 @@ osm_status osm_get_traffic_model(osm_ctx* h, double* out, int n) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
   if (!out) fail(OSM_ERR_INVALID_ARG, "NULL output");
-  for (int i = 0; i < std::min(n, 6); ++i) out[i] = c.traffic[i];
+  for (int i = 0; i < std::min(n, 8); ++i) out[i] = c.traffic[i];
   return OSM_OK;
   OSM_API_END
 }

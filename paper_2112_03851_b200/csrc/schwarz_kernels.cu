@@ -31,6 +31,16 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) {
+  unsigned short v;
+  asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int16_t ld_stream(const int16_t* p) {
+  short v;
+  asm("ld.global.nc.L1::no_allocate.s16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -248,15 +258,54 @@ __device__ __forceinline__ double tile_row_bulk(const SellDev& A, int64_t blk, c
   return s;
 }
 
+// Variant 3 (value-indexed): 2-byte dictionary index + 2-byte column offset per entry; the
+// dictionary (distinct values, tens to thousands) is read through L1; same pipelining as variant 0.
+template <int CH>
+__device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, const double* __restrict__ x) {
+  constexpr int T = kRowsPerBlock;
+  const int w = A.twidth[blk];
+  const int64_t base = A.toff[blk] + threadIdx.x;
+  const uint16_t* ip = A.vidx + base;
+  const int16_t* cp = A.cidx + base;
+  const double* xr = x + blk * T + threadIdx.x;
+  double s = 0.0;
+  uint16_t id[CH];
+  int16_t d[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    id[j] = j < w ? ld_stream(ip + T * j) : (uint16_t)0;
+    d[j] = j < w ? ld_stream(cp + T * j) : (int16_t)0;
+  }
+  for (int k = 0; k < w; k += CH) {
+    double xv[CH], vv[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      xv[j] = (k + j < w) ? __ldg(xr + d[j]) : 0.0;
+      vv[j] = (k + j < w) ? __ldg(A.dict + id[j]) : 0.0;
+    }
+    const int kn = k + CH;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      id[j] = (kn + j < w) ? ld_stream(ip + T * (int64_t)(kn + j)) : (uint16_t)0;
+      d[j] = (kn + j < w) ? ld_stream(cp + T * (int64_t)(kn + j)) : (int16_t)0;
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (k + j < w) s = fma(vv[j], xv[j], s);
+  }
+  return s;
+}
+
 // V = 0: LDG rows; V = 2: LDG rows with registers capped at 32 (8 blocks / 64 warps per SM);
-// V = 1: warp-specialized bulk-copy pipeline.
+// V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers).
 template <int V>
 __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
                                            unsigned char* smem) {
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
+  if constexpr (V == 3) return tile_row_vi<4>(A, blk, x);
   return tile_row_ldg<4>(A, blk, x);
 }
-#define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, (V) == 2 ? 8 : 1)
+#define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, ((V) == 2 || (V) == 3) ? 8 : 1)
 
 // ---------------------------------------------------------------- PCG kernels
 
@@ -581,11 +630,15 @@ __global__ void __launch_bounds__(kThreads) k_iface_sum(const SideDev* __restric
   }
 }
 
-SellDev sell_of(const Ctx& c) { return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth}; }
+SellDev sell_of(const Ctx& c) {
+  return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth, c.vi_idx, c.vi_col, c.vi_dict};
+}
 
 }  // namespace
 
-static int spmv_smem(const Ctx& c) { return c.spmv_variant == 1 ? kBulkSmem : 0; }
+int spmv_variant_of(const Ctx& c) { return (c.spmv_variant == 3 && !c.vi_ok) ? 2 : c.spmv_variant; }
+
+static int spmv_smem(const Ctx& c) { return spmv_variant_of(c) == 1 ? kBulkSmem : 0; }
 
 void spmv_init_attributes() {
   static bool done = false;
@@ -596,16 +649,22 @@ void spmv_init_attributes() {
   done = true;
 }
 
+template <int V>
+static void warm_v(Ctx& c, double tol) {
+  const unsigned thr = V == 1 ? kBulkThreads : kThreads;
+  k_warm<V><<<(unsigned)c.nblk_total, thr, spmv_smem(c), c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
+                                                                      c.lam_all, c.dinv, c.r, c.p, c.part,
+                                                                      c.nblk_total, tol, c.d_nactive);
+}
+
 void launch_warm(Ctx& c, double tol, int) {
   timer_begin(c, T_WARM);
-  if (c.spmv_variant == 1)
-    k_warm<1><<<(unsigned)c.nblk_total, kBulkThreads, spmv_smem(c), c.stream>>>(
-        sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot, c.lam_all, c.dinv, c.r, c.p, c.part, c.nblk_total, tol,
-        c.d_nactive);
-  else
-    k_warm<0><<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
-                                                                 c.lam_all, c.dinv, c.r, c.p, c.part, c.nblk_total,
-                                                                 tol, c.d_nactive);
+  switch (spmv_variant_of(c)) {
+    case 0: warm_v<0>(c, tol); break;
+    case 1: warm_v<1>(c, tol); break;
+    case 2: warm_v<2>(c, tol); break;
+    default: warm_v<3>(c, tol); break;
+  }
   OSM_CHECK_LAUNCH();
   ++c.launches;
   timer_end(c, T_WARM);
@@ -633,17 +692,21 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
   OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
+template <int V>
+static void cg_spmv_v(Ctx& c) {
+  launch_pdl(c, k_cg_spmv<V>, (unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads,
+             (size_t)(V == 1 ? kBulkSmem : 0), sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
+             c.part, c.nblk_total, c.d_nactive);
+}
+
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
-  if (c.spmv_variant == 1)
-    launch_pdl(c, k_cg_spmv<1>, (unsigned)c.nblk_total, kBulkThreads, (size_t)kBulkSmem, sell_of(c),
-               (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
-  else if (c.spmv_variant == 2)
-    launch_pdl(c, k_cg_spmv<2>, (unsigned)c.nblk_total, kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub,
-               c.st, (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
-  else
-    launch_pdl(c, k_cg_spmv<0>, (unsigned)c.nblk_total, kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub,
-               c.st, (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive);
+  switch (spmv_variant_of(c)) {
+    case 0: cg_spmv_v<0>(c); break;
+    case 1: cg_spmv_v<1>(c); break;
+    case 2: cg_spmv_v<2>(c); break;
+    default: cg_spmv_v<3>(c); break;
+  }
   ++c.launches;
   timer_end(c, T_SPMV);
 }
@@ -689,15 +752,20 @@ void launch_glue(Ctx& c, int zero) {
   ++c.launches;
 }
 
+template <int V>
+static void resid_v(Ctx& c) {
+  k_resid<V><<<(unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, spmv_smem(c), c.stream>>>(
+      sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot, c.wif_all, c.part, c.nblk_total);
+}
+
 void launch_resid(Ctx& c) {
   timer_begin(c, T_RESID);
-  if (c.spmv_variant == 1)
-    k_resid<1><<<(unsigned)c.nblk_total, kBulkThreads, spmv_smem(c), c.stream>>>(sell_of(c), c.blk_sub, c.st, c.ut, c.b,
-                                                                             c.islot, c.wif_all, c.part,
-                                                                             c.nblk_total);
-  else
-    k_resid<0><<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot,
-                                                                  c.wif_all, c.part, c.nblk_total);
+  switch (spmv_variant_of(c)) {
+    case 0: resid_v<0>(c); break;
+    case 1: resid_v<1>(c); break;
+    case 2: resid_v<2>(c); break;
+    default: resid_v<3>(c); break;
+  }
   OSM_CHECK_LAUNCH();
   ++c.launches;
   timer_end(c, T_RESID);

@@ -41,9 +41,9 @@ struct SellDev {
   const int32_t* col;
   const int64_t* toff;
   const int32_t* twidth;
-  const uint16_t* vidx;  // value-indexed copy (variant 3): dictionary index per entry
-  const int16_t* cidx;   // column offset col - row per entry
-  const double* dict;    // distinct values
+  const uint32_t* packed;  // value-indexed copy (variant 3): (dict index << 16) | (uint16)(col - row),
+  const int64_t* poff;     //   4 entries of a row per uint4 (see vi.cu); per-tile word offsets
+  const double* dict;      // distinct values
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -221,6 +221,9 @@ struct Ctx {
   uint16_t* vi_idx = nullptr;
   int16_t* vi_col = nullptr;
   double* vi_dict = nullptr;
+  uint32_t* vi_packed = nullptr;
+  int64_t* vi_poff = nullptr;
+  int64_t vi_words = 0;
   int64_t vi_ndict = 0, vi_nbase = 0;
   struct FoldTuple {
     int32_t side;

@@ -31,16 +31,7 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) {
-  unsigned short v;
-  asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ int16_t ld_stream(const int16_t* p) {
-  short v;
-  asm("ld.global.nc.L1::no_allocate.s16 %0, [%1];" : "=h"(v) : "l"(p));
-  return v;
-}
+
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -258,40 +249,36 @@ __device__ __forceinline__ double tile_row_bulk(const SellDev& A, int64_t blk, c
   return s;
 }
 
-// Variant 3 (value-indexed): 2-byte dictionary index + 2-byte column offset per entry; the
-// dictionary (distinct values, tens to thousands) is read through L1; same pipelining as variant 0.
-template <int CH>
+// Variant 3 (value-indexed): each entry is one 32-bit word (dictionary index << 16 | 16-bit
+// column offset), 4 entries of a row per 16-byte load; the dictionary (tens to thousands of
+// distinct values) is read through L1.  The next group's load is issued before the current
+// group's gathers are consumed; the main loop has no per-entry predicates (widths are padded to
+// a multiple of 4 with zero-valued entries).
+__device__ __forceinline__ uint4 ld_stream4(const uint32_t* p) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p));
+  return v;
+}
 __device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, const double* __restrict__ x) {
   constexpr int T = kRowsPerBlock;
-  const int w = A.twidth[blk];
-  const int64_t base = A.toff[blk] + threadIdx.x;
-  const uint16_t* ip = A.vidx + base;
-  const int16_t* cp = A.cidx + base;
+  const int ng = (A.twidth[blk] + 3) >> 2;
+  const uint32_t* gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
   const double* xr = x + blk * T + threadIdx.x;
   double s = 0.0;
-  uint16_t id[CH];
-  int16_t d[CH];
-#pragma unroll
-  for (int j = 0; j < CH; ++j) {
-    id[j] = j < w ? ld_stream(ip + T * j) : (uint16_t)0;
-    d[j] = j < w ? ld_stream(cp + T * j) : (int16_t)0;
-  }
-  for (int k = 0; k < w; k += CH) {
-    double xv[CH], vv[CH];
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      xv[j] = (k + j < w) ? __ldg(xr + d[j]) : 0.0;
-      vv[j] = (k + j < w) ? __ldg(A.dict + id[j]) : 0.0;
-    }
-    const int kn = k + CH;
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      id[j] = (kn + j < w) ? ld_stream(ip + T * (int64_t)(kn + j)) : (uint16_t)0;
-      d[j] = (kn + j < w) ? ld_stream(cp + T * (int64_t)(kn + j)) : (int16_t)0;
-    }
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-      if (k + j < w) s = fma(vv[j], xv[j], s);
+  if (ng == 0) return s;
+  uint4 e = ld_stream4(gp);
+  for (int g = 0; g < ng; ++g) {
+    const double x0 = __ldg(xr + (int16_t)(e.x & 0xffffu)), x1 = __ldg(xr + (int16_t)(e.y & 0xffffu));
+    const double x2 = __ldg(xr + (int16_t)(e.z & 0xffffu)), x3 = __ldg(xr + (int16_t)(e.w & 0xffffu));
+    const double v0 = __ldg(A.dict + (e.x >> 16)), v1 = __ldg(A.dict + (e.y >> 16));
+    const double v2 = __ldg(A.dict + (e.z >> 16)), v3 = __ldg(A.dict + (e.w >> 16));
+    if (g + 1 < ng) e = ld_stream4(gp + 4 * (int64_t)T * (g + 1));
+    s = fma(v0, x0, s);
+    s = fma(v1, x1, s);
+    s = fma(v2, x2, s);
+    s = fma(v3, x3, s);
   }
   return s;
 }
@@ -302,7 +289,7 @@ template <int V>
 __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
                                            unsigned char* smem) {
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
-  if constexpr (V == 3) return tile_row_vi<4>(A, blk, x);
+  if constexpr (V == 3) return tile_row_vi(A, blk, x);
   return tile_row_ldg<4>(A, blk, x);
 }
 #define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, ((V) == 2 || (V) == 3) ? 8 : 1)
@@ -631,7 +618,7 @@ __global__ void __launch_bounds__(kThreads) k_iface_sum(const SideDev* __restric
 }
 
 SellDev sell_of(const Ctx& c) {
-  return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth, c.vi_idx, c.vi_col, c.vi_dict};
+  return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth, c.vi_packed, c.vi_poff, c.vi_dict};
 }
 
 }  // namespace

@@ -57,6 +57,28 @@ __global__ void k_vi_cols(int64_t ntile, const int64_t* __restrict__ toff, const
   }
 }
 
+// Packed layout: tile t holds rows 256 t + r; its entries are grouped by 4 (width padded to a
+// multiple of 4 with (zero value, offset 0) entries); group g of row r is the uint4 at
+// poff[t] + 4 (256 g + r) (in 32-bit words), entry = (value index << 16) | (uint16) offset.
+__global__ void k_vi_pack(int64_t ntile, const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
+                          const int64_t* __restrict__ poff, const uint16_t* __restrict__ vidx,
+                          const int16_t* __restrict__ cidx, uint32_t zero_idx, uint32_t* __restrict__ packed) {
+  const int64_t t = blockIdx.x;
+  if (t >= ntile) return;
+  const int r = threadIdx.x;
+  const int w = twidth[t];
+  const int w4 = (w + 3) & ~3;
+  const int64_t base = toff[t] + r;
+  for (int k = 0; k < w4; ++k) {
+    uint32_t e = zero_idx << 16;
+    if (k < w) {
+      const int64_t i = base + (int64_t)kRowsPerBlock * k;
+      e = ((uint32_t)vidx[i] << 16) | (uint32_t)(uint16_t)cidx[i];
+    }
+    packed[poff[t] + 4 * ((int64_t)kRowsPerBlock * (k >> 2) + r) + (k & 3)] = e;
+  }
+}
+
 __global__ void k_vi_fold_slots(int64_t nfold, const int64_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                 uint16_t* __restrict__ vidx) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -70,9 +92,13 @@ void vi_free(Ctx& c) {
   if (c.vi_idx) cudaFree(c.vi_idx);
   if (c.vi_col) cudaFree(c.vi_col);
   if (c.vi_dict) cudaFree(c.vi_dict);
+  if (c.vi_packed) cudaFree(c.vi_packed);
+  if (c.vi_poff) cudaFree(c.vi_poff);
   c.vi_idx = nullptr;
   c.vi_col = nullptr;
   c.vi_dict = nullptr;
+  c.vi_packed = nullptr;
+  c.vi_poff = nullptr;
   c.vi_ok = false;
   c.vi_fold_tuples.clear();
 }
@@ -85,11 +111,12 @@ void vi_build(Ctx& c) {
   if (n == 0) return;
   // 1. distinct K^N values
   double* tmp = nullptr;
-  OSM_CUDA(cudaMalloc(&tmp, sizeof(double) * n));
+  OSM_CUDA(cudaMalloc(&tmp, sizeof(double) * (n + 1)));
   OSM_CUDA(cudaMemcpyAsync(tmp, c.sell_val, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  OSM_CUDA(cudaMemsetAsync(tmp + n, 0, sizeof(double), c.stream));  // 0.0 is always in the dictionary
   thrust::device_ptr<double> tp(tmp);
-  thrust::sort(thrust::cuda::par.on(c.stream), tp, tp + n);
-  const int64_t nd = thrust::unique(thrust::cuda::par.on(c.stream), tp, tp + n) - tp;
+  thrust::sort(thrust::cuda::par.on(c.stream), tp, tp + n + 1);
+  const int64_t nd = thrust::unique(thrust::cuda::par.on(c.stream), tp, tp + n + 1) - tp;
   // 2. fold tuples (side, K^N, m, s) -> slots after the K^N values
   std::vector<int64_t> pos(c.nfold);
   std::vector<double> kn(c.nfold), m(c.nfold), sv(c.nfold);
@@ -163,6 +190,33 @@ void vi_build(Ctx& c) {
     vi_free(c);
     return;
   }
+  // 5. packed copy (4 entries of a row per 16-byte load); the 2-byte arrays are freed
+  std::vector<int32_t> tw(c.nblk_total);
+  OSM_CUDA(cudaMemcpy(tw.data(), c.sell_swidth, sizeof(int32_t) * c.nblk_total, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> poff(c.nblk_total);
+  int64_t words = 0;
+  for (int64_t t = 0; t < c.nblk_total; ++t) {
+    poff[t] = words;
+    words += (int64_t)((tw[t] + 3) & ~3) * kRowsPerBlock;
+  }
+  // index of 0.0 in the sorted dictionary
+  std::vector<double> hd(nd);
+  OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * nd, cudaMemcpyDeviceToHost));
+  const uint32_t zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
+  OSM_CUDA(cudaMalloc(&c.vi_poff, sizeof(int64_t) * c.nblk_total));
+  OSM_CUDA(cudaMemcpy(c.vi_poff, poff.data(), sizeof(int64_t) * c.nblk_total, cudaMemcpyHostToDevice));
+  OSM_CUDA(cudaMalloc(&c.vi_packed, sizeof(uint32_t) * std::max<int64_t>(1, words)));
+  k_vi_pack<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(c.nblk_total, c.sell_soff, c.sell_swidth,
+                                                                   c.vi_poff, c.vi_idx, c.vi_col, zero_idx,
+                                                                   c.vi_packed);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  cudaFree(c.vi_idx);
+  cudaFree(c.vi_col);
+  c.vi_idx = nullptr;
+  c.vi_col = nullptr;
+  c.vi_words = words;
   c.vi_ok = true;
 }
 

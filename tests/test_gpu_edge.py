@@ -1,0 +1,129 @@
+"""Edge and degenerate cases of the CUDA path (through the C ABI), each checked against the oracle
+or against the status contract of include/osm.h."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import mesh, schwarz
+
+from parity_util import history_ok, oracle_run, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _osm(nx, ny, nz, order, nsub, alpha=(10.0, 10.0), L=(1.0, 1.0, 1.0)):
+    import paper_2112_03851_b200 as P
+
+    o = P.Osm(nx, ny, nz, *L, order)
+    o.decompose(nsub)
+    if nsub > 1:
+        o.set_robin(np.full(nsub - 1, alpha[0]), np.full(nsub - 1, alpha[1]))
+    o.assemble()
+    return o
+
+
+def test_zero_density_one_iteration():
+    """delta rho = 0 -> Phi = 0 after one iteration, even with a warm start."""
+    o = _osm(6, 5, 4, 2, 3)
+    o.upload_density(np.zeros(120))
+    st, rep = o.solve()
+    assert st == 0 and rep.outer_iters == 1 and o.history()[0] == 0.0
+    assert not np.any(o.solution())
+    o.close()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_one_cell_slabs(order):
+    """nsub = nx: every slab one cell wide (each P1 slab is just its two planes)."""
+    cfg = dict(nx=5, ny=4, nz=3, lx=1.0, ly=0.9, lz=0.6, order=order, nsub=5)
+    drho = synth.random_field(5, 4, 3, seed=23)
+    o = _osm(5, 4, 3, order, 5, (8.0, 12.0), (1.0, 0.9, 0.6))
+    o.upload_density(drho)
+    st, _ = o.solve(max_outer=800)
+    prob, rep = oracle_run(cfg, drho, [8.0] * 4, [12.0] * 4, max_outer=800)
+    ok, d = history_ok(o.history(), rep.h)
+    assert st == 0 and ok and len(o.history()) == len(rep.h), d.max()
+    assert rel_l2(o.solution(), schwarz.full_lattice(prob, rep.ut)) <= 1e-10
+    o.close()
+
+
+@pytest.mark.parametrize("nsub", [1, 2])
+def test_smallest_grid(nsub):
+    """2^3 P1 cells: a single free DOF (u = 1/24 for f = 1, oracle pin p1_tiny)."""
+    from oracle.fe import G_NEWTON
+
+    o = _osm(2, 2, 2, 1, nsub)
+    o.upload_density(np.full(8, 1.0 / (4 * np.pi * G_NEWTON)))
+    st, _ = o.solve()
+    phi = o.solution()
+    assert st == 0
+    # lattice centre (1,1,1) of the 3^3 lattice; with 2 subdomains Phi is the Schwarz iterate at h <= 1e-8
+    assert abs(phi[13] - 1.0 / 24.0) <= (1e-14 if nsub == 1 else 1e-7) / 24.0
+    o.close()
+
+
+def test_status_contract():
+    import paper_2112_03851_b200 as P
+
+    with pytest.raises(P.OsmError) as e:
+        P.Osm(1, 4, 4, 1, 1, 1, 1)  # 2 lattice points in x: no interior
+    assert e.value.status == P.OSM_ERR_GRID_TOO_SMALL
+    with pytest.raises(P.OsmError) as e:
+        P.Osm(4, 4, 4, 1, 1, 1, 3)
+    assert e.value.status == P.OSM_ERR_INVALID_ARG
+    o = P.Osm(4, 4, 4, 1, 1, 1, 2)
+    with pytest.raises(P.OsmError) as e:
+        o.decompose(5)
+    assert e.value.status == P.OSM_ERR_INVALID_ARG
+    o.decompose(2)
+    with pytest.raises(P.OsmError) as e:
+        o.set_robin([-1.0], [1.0])
+    assert e.value.status == P.OSM_ERR_ILL_POSED
+    with pytest.raises(P.OsmError) as e:
+        o.set_robin([0.0], [0.0])
+    assert e.value.status == P.OSM_ERR_ILL_POSED
+    with pytest.raises(P.OsmError) as e:
+        o.solve()
+    assert e.value.status == P.OSM_ERR_STATE
+    o.set_robin([5.0], [5.0])
+    o.assemble()
+    with pytest.raises(P.OsmError) as e:
+        o.solve()  # no density yet
+    assert e.value.status == P.OSM_ERR_STATE
+    o.upload_density(np.ones(64))
+    st, rep = o.solve(max_outer=2)
+    assert st == P.OSM_NOT_CONVERGED and rep.outer_iters == 2 and not rep.converged
+    with pytest.raises(ValueError):
+        o.upload_density(np.ones(63))
+    o.close()
+
+
+def test_max_inner_reported():
+    """An inner solve capped by max_inner keeps its last iterate and is counted (DESIGN R2)."""
+    cfg = dict(nx=6, ny=6, nz=6, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=2)
+    drho = synth.ball(6, 6, 6)
+    o = _osm(6, 6, 6, 2, 2, (20.0, 20.0))
+    o.upload_density(drho)
+    st, rep = o.solve(max_outer=3, max_inner=5)
+    assert rep.inner_maxed > 0
+    prob, orep = oracle_run(cfg, drho, [20.0], [20.0], max_outer=3)
+    orep5 = schwarz.schwarz(prob, schwarz.robin_operators(prob, [20.0], [20.0]), max_outer=3, max_inner=5)
+    ok, d = history_ok(o.history(), orep5.h)
+    assert ok, d.max()
+    o.close()
+
+
+def test_resolve_after_reassembly_and_new_density():
+    """Solving twice, re-assembling and re-uploading give identical results (no stale state)."""
+    o = _osm(6, 4, 4, 2, 2, (15.0, 25.0))
+    d1 = synth.random_field(6, 4, 4, seed=1)
+    o.upload_density(d1)
+    o.solve()
+    h1 = o.history().copy()
+    o.upload_density(synth.random_field(6, 4, 4, seed=2))
+    o.solve()
+    o.assemble()
+    o.upload_density(d1)
+    o.solve()
+    assert np.array_equal(o.history(), h1)
+    o.close()

@@ -1,0 +1,107 @@
+"""Parity at BASELINE sizes, in the launch configuration bench.py times (value-indexed SpMV, graphs,
+PDL), on outputs the oracle can compute in seconds:
+
+C3 (P2 64^3 paper box, 8 subdomains, OO2): bit-exact CSR patterns and interface maps of sampled
+subdomains (0 = end slab, 3 = interior); the first outer iteration's subdomain solves (cold PCG to
+1e-10 on K_s = K^N + p M + q S with rhs = b_s) and the traces they produce on interface 0.
+
+C2 (P2 32^3 unit cube, 2 subdomains, ball density): the first 10 outer iterations (history, inner
+counts, u_s) against the full oracle Schwarz iteration; at convergence, the oracle's monolithic K
+gives ||f - K Phi_gpu|| / ||f|| equal to the reported h(N) <= 1e-8.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import linalg, mesh, schwarz
+
+from parity_util import history_ok, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c3():
+    import paper_2112_03851_b200 as P
+
+    cfg = dict(synth.CONFIGS["C3"])
+    drho = synth.density(cfg)
+    o = P.setup(cfg, drho)
+    st, rep = o.solve(tol_outer=1e-8, max_outer=1)
+    box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+    prob = schwarz.build_problem(box, cfg["nsub"], drho=drho, only=[0, 1, 3], monolithic=False)
+    yield cfg, o, prob
+    o.close()
+
+
+def test_c3_patterns_and_maps(c3):
+    cfg, o, prob = c3
+    for s in (0, 3):
+        rp, col, val = o.csr(s)
+        K = prob.subs[s].KN
+        assert np.array_equal(rp, K.indptr.astype(np.int64)) and np.array_equal(col, K.indices.astype(np.int32))
+        assert np.abs(val - K.data).max() <= 1e-13 * np.abs(K.data).max()
+    assert np.array_equal(o.interface_map(0, 0), prob.subs[0].right.astype(np.int32))
+    assert np.array_equal(o.interface_map(0, 1), prob.subs[1].left.astype(np.int32))
+    assert np.array_equal(o.interface_map(2, 1), prob.subs[3].left.astype(np.int32))
+    assert np.array_equal(o.interface_map(3, 0), prob.subs[3].right.astype(np.int32))
+
+
+def test_c3_first_iteration_solves_and_traces(c3):
+    cfg, o, prob = c3
+    p1, p2, q1, q2 = cfg["robin"]
+    S = cfg["nsub"]
+    A = schwarz.robin_operators(prob, [p1] * (S - 1), [p2] * (S - 1), [q1] * (S - 1), [q2] * (S - 1))
+    its = o.inner_iters()[0]
+    u = {}
+    for s in (0, 1):
+        Ks = schwarz.subdomain_operator(prob, s, A)
+        res = linalg.pcg(Ks, prob.subs[s].b, tol=1e-10, maxit=20000)
+        u[s] = res.x
+        assert abs(its[s] - res.iterations) <= 1, (s, its[s], res.iterations)
+        assert rel_l2(o.local_solution(s), res.x) <= 1e-10
+    # lambda^1 on interface 0: (A_0 + A_1) u_other|Gamma - 0
+    C = A[(0, 0)] + A[(0, 1)]
+    lam_left = np.asarray(C @ u[1][prob.subs[1].left]).ravel()
+    lam_right = np.asarray(C @ u[0][prob.subs[0].right]).ravel()
+    assert rel_l2(o.trace(0, 0), lam_left) <= 1e-9
+    assert rel_l2(o.trace(0, 1), lam_right) <= 1e-9
+
+
+@pytest.fixture(scope="module")
+def c2():
+    import paper_2112_03851_b200 as P
+
+    cfg = dict(synth.CONFIGS["C2"])
+    drho = synth.density(cfg)
+    o = P.setup(cfg, drho)
+    box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+    prob = schwarz.build_problem(box, cfg["nsub"], drho=drho)
+    yield cfg, o, prob
+    o.close()
+
+
+def test_c2_first_ten_outer_iterations(c2):
+    cfg, o, prob = c2
+    st, rep = o.solve(tol_outer=1e-300, max_outer=10, diverge_window=0)
+    A = schwarz.robin_operators(prob, [cfg["alpha"]], [cfg["alpha"]])
+    orep = schwarz.schwarz(prob, A, tol_outer=1e-300, max_outer=10, diverge_window=0)
+    ok, d = history_ok(o.history(), orep.h)
+    assert ok and len(orep.h) == 10, d.max()
+    assert np.abs(o.inner_iters() - np.array(orep.inner)).max() <= 1
+    for s in range(cfg["nsub"]):
+        assert rel_l2(o.local_solution(s), orep.u[s]) <= 1e-10
+
+
+def test_c2_converged_is_monolithic_solution(c2):
+    cfg, o, prob = c2
+    st, rep = o.solve(tol_outer=1e-8, max_outer=1000)
+    assert st == 0
+    phi = o.solution()
+    box = prob.box
+    Nx, Ny, Nz = box.lattice
+    K, J, I = np.meshgrid(np.arange(1, Nz - 1), np.arange(1, Ny - 1), np.arange(1, Nx - 1), indexing="ij")
+    ut = phi[box.lattice_id(I.ravel(), J.ravel(), K.ravel())]
+    h = schwarz.global_residual(prob, ut)
+    assert abs(h - o.history()[-1]) <= 1e-10 * h + 1e-14
+    assert h <= 1e-8

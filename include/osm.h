@@ -194,6 +194,12 @@ osm_status osm_get_inner_iters(osm_ctx* ctx, int32_t* its, int cap_outer, int* n
  * copies).  Gathered to rank 0; other ranks may pass NULL.  phi == NULL on
  * rank 0: *n = Nx*Ny*Nz. */
 osm_status osm_get_solution(osm_ctx* ctx, double* phi, int64_t* n);
+/* [collective] Gravity anomaly of the last solve:
+ * g_z = -dPhi_h/dz (m/s^2, z up, positive for excess mass below) of the glued FE potential on the
+ * plane z = z0 (0 <= z0 <= lz) at the cell-centre columns (x_c, y_c), nx*ny host doubles, x fastest,
+ * evaluated exactly in the Kuhn tet containing the point (ties between tets: lower axis first).
+ * Rank 0 receives it; gz == NULL on rank 0: *n = nx*ny. */
+osm_status osm_gravity_z(osm_ctx* ctx, double z0, double* gz, int64_t* n);
 /* Local subdomain iterate u_s (contract order, host).  u == NULL: *n = n_s. */
 osm_status osm_get_local_solution(osm_ctx* ctx, int s, double* u, int64_t* n);
 /* lambda_{s,Gamma} of interface `iface`, side 0/1 (owner rank only; host). */

@@ -33,7 +33,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
-               "osm_cmaes_should_stop"]
+               "osm_cmaes_should_stop", "osm_gravity_z"]
 
 
 class MeshDesc(C.Structure):
@@ -112,6 +112,7 @@ _sigs = {
     "osm_cmaes_tell": (C.c_int, [_P, _pd]),
     "osm_cmaes_state": (C.c_int, [_P, _pd, _pd, _pd, _pd, _pd, _pint]),
     "osm_cmaes_should_stop": (C.c_int, [_P, C.c_int, C.c_double, _pint]),
+    "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
 for _name, (_res, _args) in _sigs.items():
@@ -357,6 +358,16 @@ class Osm:
         if out.dtype != np.float64 or not out.flags.c_contiguous or out.size < n.value:
             raise ValueError("out must be a contiguous float64 array of the lattice size")
         _check(_lib.osm_get_solution(self._h, _ptr(out, C.c_double), C.byref(n)))
+        return out
+
+    def gravity_z(self, z0):
+        """[collective] g_z = -dPhi/dz on the plane z = z0 at the cell-centre columns (rank 0; else None)."""
+        n = C.c_int64(self.mesh.nx * self.mesh.ny)
+        if self.rank != 0:
+            _check(_lib.osm_gravity_z(self._h, float(z0), None, C.byref(n)))
+            return None
+        out = np.zeros(n.value)
+        _check(_lib.osm_gravity_z(self._h, float(z0), _ptr(out, C.c_double), C.byref(n)))
         return out
 
     def local_solution_size(self, s) -> int:

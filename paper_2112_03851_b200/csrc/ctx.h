@@ -277,6 +277,7 @@ void batch_free(Ctx& c);
 double fnorm2_of(Ctx& c);  // ||f||^2 of the glued global system (osm.cu)
 
 void spmv_init_attributes();
+void gravity_z(Ctx& c, double z0, double* d_out);  // gravity.cu (uses c.phi)
 void vi_build(Ctx& c);
 void vi_free(Ctx& c);
 void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side);

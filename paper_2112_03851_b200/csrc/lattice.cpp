@@ -249,6 +249,18 @@ void element_stiffness(int order, const double h[3], std::vector<double>& Ke, do
   }
 }
 
+void tet_bary_gradients(int t, const double h[3], std::vector<double>& out) {
+  int v[4][3];
+  tet_vertices(t, v);
+  double X[4][3], g[4][3], vol;
+  for (int a = 0; a < 4; ++a)
+    for (int d = 0; d < 3; ++d) X[a][d] = v[a][d] * h[d];
+  bary_gradients(X, g, vol);
+  out.assign(12, 0.0);
+  for (int a = 0; a < 4; ++a)
+    for (int d = 0; d < 3; ++d) out[a * 3 + d] = g[a][d];
+}
+
 StencilTables build_stencil_tables(int order, const double h[3]) {
   StencilTables T;
   T.order = order;

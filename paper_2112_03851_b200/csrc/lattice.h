@@ -52,6 +52,9 @@ void element_stiffness(int order, const double h[3], std::vector<double>& Ke, do
 
 StencilTables build_stencil_tables(int order, const double h[3]);
 
+// Physical barycentric gradients (4 x 3, row-major) of Kuhn tet t of a cell of size h.
+void tet_bary_gradients(int t, const double h[3], std::vector<double>& g);
+
 // Interface-plane mass matrix M_Gamma on the free interior points of an x = const
 // plane of the (Ny x Nz)-point lattice, CSR in plane-point order (j fastest).
 // Triangles: each (j,k) square split along its (j,k)-(j+1,k+1) diagonal.

@@ -944,6 +944,15 @@ osm_status osm_get_inner_iters(osm_ctx* h, int32_t* its, int cap_outer, int* n_o
   OSM_API_END
 }
 
+// Glued Phi of the last solve on the full lattice into c.phi (on rank 0 after the reduce).
+static void gather_phi(Ctx& c, int64_t N) {
+  if (!c.assembled) fail(OSM_ERR_STATE, "nothing solved");
+  if (!c.phi) c.phi = dalloc<double>(N);
+  OSM_CUDA(cudaMemsetAsync(c.phi, 0, sizeof(double) * N, c.stream));
+  for (const Sub& S : c.subs) launch_scatter_phi(c, S, c.nranks > 1 ? 1 : 0);
+  if (c.nranks > 1) OSM_NCCL(ncclReduce(c.phi, c.phi, N, ncclDouble, ncclSum, 0, c.comm, c.stream));
+}
+
 osm_status osm_get_solution(osm_ctx* h, double* phi, int64_t* n) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
@@ -954,16 +963,39 @@ osm_status osm_get_solution(osm_ctx* h, double* phi, int64_t* n) {
     *n = N;
     return OSM_OK;
   }
-  if (!c.assembled) fail(OSM_ERR_STATE, "nothing solved");
   if (c.rank == 0 && *n < N) fail(OSM_ERR_INVALID_ARG, "solution buffer too small");
-  if (!c.phi) c.phi = dalloc<double>(N);
-  OSM_CUDA(cudaMemsetAsync(c.phi, 0, sizeof(double) * N, c.stream));
-  for (const Sub& S : c.subs) launch_scatter_phi(c, S, c.nranks > 1 ? 1 : 0);
-  if (c.nranks > 1) OSM_NCCL(ncclReduce(c.phi, c.phi, N, ncclDouble, ncclSum, 0, c.comm, c.stream));
+  gather_phi(c, N);
   if (c.rank == 0 && phi)
     OSM_CUDA(cudaMemcpyAsync(phi, c.phi, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
   OSM_CUDA(cudaStreamSynchronize(c.stream));
   *n = N;
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_gravity_z(osm_ctx* h, double z0, double* gz, int64_t* n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
+  const int64_t M = c.mesh.nx * c.mesh.ny;
+  if (!gz && c.rank == 0) {
+    *n = M;
+    return OSM_OK;
+  }
+  if (!(z0 >= 0) || !(z0 <= c.mesh.lz)) fail(OSM_ERR_INVALID_ARG, "z0 outside [0, lz]");
+  if (c.rank == 0 && *n < M) fail(OSM_ERR_INVALID_ARG, "buffer too small");
+  const int o = c.mesh.order;
+  const int64_t N = (o * c.mesh.nx + 1) * (o * c.mesh.ny + 1) * (o * c.mesh.nz + 1);
+  gather_phi(c, N);
+  if (c.rank == 0) {
+    double* d = dalloc<double>(M);
+    gravity_z(c, z0, d);
+    OSM_CUDA(cudaMemcpyAsync(gz, d, sizeof(double) * M, cudaMemcpyDeviceToHost, c.stream));
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+    dfree(d);
+  }
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  *n = M;
   return OSM_OK;
   OSM_API_END
 }

@@ -127,3 +127,22 @@ def test_resolve_after_reassembly_and_new_density():
     o.solve()
     assert np.array_equal(o.history(), h1)
     o.close()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_gravity_anomaly_matches_oracle(order):
+    """NEXT-3: g_z = -dPhi/dz of the GPU solution vs the oracle's evaluation of the oracle's Phi."""
+    from oracle import gravity
+
+    cfg = dict(nx=6, ny=5, nz=4, lx=250e3, ly=250e3, lz=15e3, order=order, nsub=3)
+    drho = synth.chicxulub(6, 5, 4)
+    o = _osm(6, 5, 4, order, 3, (3e-4, 4e-4), (250e3, 250e3, 15e3))
+    o.upload_density(drho)
+    st, _ = o.solve(max_outer=800)
+    prob, rep = oracle_run(cfg, drho, [3e-4] * 2, [4e-4] * 2, max_outer=800)
+    phi_or = schwarz.full_lattice(prob, rep.ut)
+    for z0 in (0.0, 7.5e3, 15e3):
+        g = o.gravity_z(z0)
+        go = gravity.gravity_z(prob.box, phi_or, z0)
+        assert np.abs(g - go).max() <= 1e-9 * np.abs(go).max(), z0
+    o.close()

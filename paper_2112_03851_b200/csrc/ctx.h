@@ -44,6 +44,7 @@ struct SellDev {
   const uint32_t* packed;  // value-indexed copy (variant 3): (dict index << 16) | (uint16)(col - row),
   const int64_t* poff;     //   4 entries of a row per uint4 (see vi.cu); per-tile word offsets
   const double* dict;      // distinct values
+  int ndict;
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -212,9 +213,11 @@ struct Ctx {
   double graph_tol = -1;
   int graph_maxit = -1;
   bool use_graph = true;
+  int update_variant = 0;  // 0: k_cg_update at 96 regs, 1: capped for 8 blocks/SM
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
-  int spmv_variant = 3;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
-                         // pipeline, 3: value-indexed SELL (16-bit value index + 16-bit column offset; default)
+  int spmv_variant = 4;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
+                         // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary
+                         // in shared memory (default; falls back to 3, then 2, when it does not apply)
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;

@@ -776,6 +776,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
     if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);
+    if (const char* e = std::getenv("OSM_UPD")) c.update_variant = std::atoi(e);
     spmv_init_attributes();
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};

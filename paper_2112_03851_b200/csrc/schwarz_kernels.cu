@@ -283,16 +283,48 @@ __device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, con
   return s;
 }
 
+// Variant 4: variant 3 with the dictionary staged in shared memory at block start (dictionary
+// lookups leave the L1 tag path; used when the dictionary fits kSmemDict entries).
+constexpr int kSmemDict = 2048;
+__device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk, const double* __restrict__ x,
+                                                   const double* sdict) {
+  constexpr int T = kRowsPerBlock;
+  const int ng = (A.twidth[blk] + 3) >> 2;
+  const uint32_t* gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
+  const double* xr = x + blk * T + threadIdx.x;
+  double s = 0.0;
+  if (ng == 0) return s;
+  uint4 e = ld_stream4(gp);
+  for (int g = 0; g < ng; ++g) {
+    const double x0 = __ldg(xr + (int16_t)(e.x & 0xffffu)), x1 = __ldg(xr + (int16_t)(e.y & 0xffffu));
+    const double x2 = __ldg(xr + (int16_t)(e.z & 0xffffu)), x3 = __ldg(xr + (int16_t)(e.w & 0xffffu));
+    const double v0 = sdict[e.x >> 16], v1 = sdict[e.y >> 16], v2 = sdict[e.z >> 16], v3 = sdict[e.w >> 16];
+    if (g + 1 < ng) e = ld_stream4(gp + 4 * (int64_t)T * (g + 1));
+    s = fma(v0, x0, s);
+    s = fma(v1, x1, s);
+    s = fma(v2, x2, s);
+    s = fma(v3, x3, s);
+  }
+  return s;
+}
+
 // V = 0: LDG rows; V = 2: LDG rows with registers capped at 32 (8 blocks / 64 warps per SM);
-// V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers).
+// V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers);
+// V = 4: value-indexed rows, dictionary in shared memory.
 template <int V>
 __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
                                            unsigned char* smem) {
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
+  if constexpr (V == 4) {
+    double* sd = reinterpret_cast<double*>(smem);
+    for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];
+    __syncthreads();
+    return tile_row_vi_smem(A, blk, x, sd);
+  }
   return tile_row_ldg<4>(A, blk, x);
 }
-#define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, ((V) == 2 || (V) == 3) ? 8 : 1)
+#define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, ((V) >= 2) ? 8 : 1)
 
 // ---------------------------------------------------------------- PCG kernels
 
@@ -341,7 +373,8 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
 // all loads of a thread issued before any use (memory-level parallelism), one reduction
 // and one counter update per 1024 rows.
 constexpr int kVecThreads = kRowsPerBlock / 2;
-__global__ void __launch_bounds__(kVecThreads) k_cg_update(const int32_t* __restrict__ vblk_sub,
+template <int MINB>
+__global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* __restrict__ vblk_sub,
                                                            const int32_t* __restrict__ vblk_tile0,
                                                            const int32_t* __restrict__ vblk_ntile,
                                                            SubState* __restrict__ st, double* __restrict__ x,
@@ -618,14 +651,22 @@ __global__ void __launch_bounds__(kThreads) k_iface_sum(const SideDev* __restric
 }
 
 SellDev sell_of(const Ctx& c) {
-  return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth, c.vi_packed, c.vi_poff, c.vi_dict};
+  return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth, c.vi_packed, c.vi_poff, c.vi_dict,
+                 (int)c.vi_ndict};
 }
 
 }  // namespace
 
-int spmv_variant_of(const Ctx& c) { return (c.spmv_variant == 3 && !c.vi_ok) ? 2 : c.spmv_variant; }
+int spmv_variant_of(const Ctx& c) {
+  if (c.spmv_variant >= 3 && !c.vi_ok) return 2;
+  if (c.spmv_variant == 4 && c.vi_ndict > kSmemDict) return 3;
+  return c.spmv_variant;
+}
 
-static int spmv_smem(const Ctx& c) { return spmv_variant_of(c) == 1 ? kBulkSmem : 0; }
+static int spmv_smem(const Ctx& c) {
+  const int v = spmv_variant_of(c);
+  return v == 1 ? kBulkSmem : (v == 4 ? (int)(sizeof(double) * c.vi_ndict) : 0);
+}
 
 void spmv_init_attributes() {
   static bool done = false;
@@ -650,7 +691,8 @@ void launch_warm(Ctx& c, double tol, int) {
     case 0: warm_v<0>(c, tol); break;
     case 1: warm_v<1>(c, tol); break;
     case 2: warm_v<2>(c, tol); break;
-    default: warm_v<3>(c, tol); break;
+    case 3: warm_v<3>(c, tol); break;
+    default: warm_v<4>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
   ++c.launches;
@@ -681,8 +723,8 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
 
 template <int V>
 static void cg_spmv_v(Ctx& c) {
-  launch_pdl(c, k_cg_spmv<V>, (unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads,
-             (size_t)(V == 1 ? kBulkSmem : 0), sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
+  launch_pdl(c, k_cg_spmv<V>, (unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
+             sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
              c.part, c.nblk_total, c.d_nactive);
 }
 
@@ -692,7 +734,8 @@ void launch_cg_spmv(Ctx& c) {
     case 0: cg_spmv_v<0>(c); break;
     case 1: cg_spmv_v<1>(c); break;
     case 2: cg_spmv_v<2>(c); break;
-    default: cg_spmv_v<3>(c); break;
+    case 3: cg_spmv_v<3>(c); break;
+    default: cg_spmv_v<4>(c); break;
   }
   ++c.launches;
   timer_end(c, T_SPMV);
@@ -700,9 +743,14 @@ void launch_cg_spmv(Ctx& c) {
 
 void launch_cg_update(Ctx& c, double tol, int maxit) {
   timer_begin(c, T_UPDATE);
-  launch_pdl(c, k_cg_update, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
-             (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
-             (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive);
+  if (c.update_variant == 1)
+    launch_pdl(c, k_cg_update<8>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+               (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
+               (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive);
+  else
+    launch_pdl(c, k_cg_update<1>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+               (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
+               (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive);
   ++c.launches;
   timer_end(c, T_UPDATE);
 }
@@ -751,7 +799,8 @@ void launch_resid(Ctx& c) {
     case 0: resid_v<0>(c); break;
     case 1: resid_v<1>(c); break;
     case 2: resid_v<2>(c); break;
-    default: resid_v<3>(c); break;
+    case 3: resid_v<3>(c); break;
+    default: resid_v<4>(c); break;
   }
   OSM_CHECK_LAUNCH();
   ++c.launches;

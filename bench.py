@@ -261,23 +261,38 @@ def main():
     osm.set_kernel_timing(True)
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     traffic = dict(spmv_bytes=0.0, update_bytes=0.0, dir_bytes=0.0)
+    traffic_csr = 0.0
     ev2.record(stream)
     for _ in range(args.timing_steps):
         step()
         tm = osm.traffic_model()
         for k in traffic:
             traffic[k] += tm[k]
+        traffic_csr += tm["csr_equiv_bytes"]
     ev3.record(stream)
     torch.cuda.synchronize()
     ms_instr = ev2.elapsed_time(ev3)
     kt = osm.kernel_timing()
+    # the same instrumented solve with the fp64 SELL kernel (variant 2): the HBM-bound reference
+    # implementation of the same SpMV (bitwise-identical iterations), for the HBM roofline
+    active = osm.set_spmv_variant(2)
+    osm.set_kernel_timing(True)
+    step()
+    kt2 = osm.kernel_timing()
+    tm2 = osm.traffic_model()
+    default_variant = osm.set_spmv_variant(4)
     osm.set_kernel_timing(False)
     peak, peak_src = hbm_peak()
     spmv_launches, spmv_ms = kt["cg_spmv"]
     achieved = traffic["spmv_bytes"] / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
     tr = ncu_traffic()
     per_launch_alg = traffic["spmv_bytes"] / max(1, spmv_launches)
-    roofline = {"bound": "hbm", "kernel": "k_cg_spmv", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    fp64_ach = tm2["spmv_bytes"] / (kt2["cg_spmv"][1] / 1e3) / 1e9 if kt2["cg_spmv"][1] > 0 else None
+    roofline_fp64 = {"bound": "hbm", "kernel": "k_cg_spmv<2> (fp64 SELL-256)", "achieved": fp64_ach, "peak": peak,
+                     "unit": "GB/s", "frac": fp64_ach / peak if fp64_ach else None,
+                     "traffic": (ncu_traffic("fp64_sell_variant2_k_cg_spmv_r01b")),
+                     "us_per_launch": 1e3 * kt2["cg_spmv"][1] / max(1, kt2["cg_spmv"][0]), "variant": active}
+    roofline = {"bound": "hbm", "kernel": f"k_cg_spmv<{default_variant}>", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None,
                 "traffic": tr, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_launch_alg,
@@ -286,7 +301,12 @@ def main():
                 "instrumented_steps": args.timing_steps,
                 "cg_kernels_gbs": {k: (traffic[b] / (kt[k][1] / 1e3) / 1e9 if kt[k][1] > 0 else None)
                                    for k, b in (("cg_update", "update_bytes"), ("cg_dir", "dir_bytes"))},
-                "kernel_ms": {k: v[1] for k, v in kt.items()}, "kernel_launches": {k: v[0] for k, v in kt.items()}}
+                "kernel_ms": {k: v[1] for k, v in kt.items()}, "kernel_launches": {k: v[0] for k, v in kt.items()},
+                "us_per_launch": 1e3 * spmv_ms / max(1, spmv_launches),
+                "format": "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
+                          "offset) + 16 B per row (p, q); dictionary in shared memory",
+                "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
+                "limiter": "L1/TEX throughput (ncu: l1tex 79% of peak, dram 37%; profiles/r01c_ncu_cg_raw.csv)"}
 
     # e2e through the C ABI with host buffers: pinned drho H2D + solve + Phi D2H, every step
     h_drho = torch.from_numpy(drho).pin_memory()
@@ -329,7 +349,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "roofline": roofline, "roofline_fp64_sell": roofline_fp64, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)
     osm.close()

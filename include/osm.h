@@ -229,9 +229,10 @@ osm_status osm_get_kernel_timing(osm_ctx* ctx, osm_kernel_time* out, int cap, in
 
 /* Algorithmic HBM bytes of one PCG iteration of local subdomain-set work,
  * summed over this rank's subdomains weighted by their inner iteration counts in
- * the last solve: out[0] = SpMV kernel bytes, out[1] =
- * update kernel bytes, out[2] = direction kernel bytes, out[3] = SELL padding
- * entries, out[4] = structural nnz (local), out[5] = local rows. */
+ * the last solve: out[0] = SpMV kernel bytes (in the format of the
+ * SpMV variant that ran), out[1] = update kernel bytes, out[2] = direction kernel bytes,
+ * out[3] = SELL padding entries, out[4] = structural nnz (local), out[5] = local rows,
+ * out[6] = SpMV bytes of the CSR-equivalent fp64 format (12 nnz + 4 (n+1) + 16 n). n <= 8. */
 osm_status osm_get_traffic_model(osm_ctx* ctx, double* out, int n);
 
 /* Host-only distribution plan (no GPU needed): subdomains [s_begin, s_end) of `rank`, and
@@ -250,6 +251,14 @@ typedef struct osm_plan_side {
 } osm_plan_side;
 osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, int* s_end, osm_plan_side* sides,
                     int cap, int* nsides);
+
+/* SpMV implementation of the PCG kernels (all give bitwise-identical iterations):
+ * 0 fp64 SELL-256, LDG rows; 1 fp64 SELL-256, warp-specialized cp.async.bulk pipeline;
+ * 2 fp64 SELL-256, LDG rows at 32 registers; 3 value-indexed (16-bit dictionary index + 16-bit
+ * column offset); 4 = 3 with the dictionary in shared memory (default).  Variants 3/4 fall back
+ * to 2 when the matrix does not admit the value-indexed copy.  *active (may be NULL) receives the
+ * variant that will actually run.  INVALID_ARG for other values. */
+osm_status osm_set_spmv_variant(osm_ctx* ctx, int variant, int* active);
 
 /* Number of this library's kernel launches on the context's stream since
  * creation (every kernel of setup, solve and readback). */

@@ -33,7 +33,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
-               "osm_cmaes_should_stop", "osm_gravity_z"]
+               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant"]
 
 
 class MeshDesc(C.Structure):
@@ -112,6 +112,7 @@ _sigs = {
     "osm_cmaes_tell": (C.c_int, [_P, _pd]),
     "osm_cmaes_state": (C.c_int, [_P, _pd, _pd, _pd, _pd, _pd, _pint]),
     "osm_cmaes_should_stop": (C.c_int, [_P, C.c_int, C.c_double, _pint]),
+    "osm_set_spmv_variant": (C.c_int, [_P, C.c_int, _pint]),
     "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
@@ -427,16 +428,22 @@ class Osm:
         _check(_lib.osm_get_kernel_timing(self._h, arr, n.value, C.byref(n)))
         return {a.name.decode(): (a.launches, a.total_ms) for a in arr}
 
+    def set_spmv_variant(self, v: int) -> int:
+        """Select the SpMV implementation (include/osm.h); returns the variant that will run."""
+        a = C.c_int()
+        _check(_lib.osm_set_spmv_variant(self._h, int(v), C.byref(a)))
+        return a.value
+
     def launch_count(self) -> int:
         n = C.c_int64(0)
         _check(_lib.osm_get_launch_count(self._h, C.byref(n)))
         return n.value
 
     def traffic_model(self):
-        out = np.zeros(6)
-        _check(_lib.osm_get_traffic_model(self._h, _ptr(out, C.c_double), 6))
+        out = np.zeros(8)
+        _check(_lib.osm_get_traffic_model(self._h, _ptr(out, C.c_double), 8))
         return dict(spmv_bytes=out[0], update_bytes=out[1], dir_bytes=out[2], pad_entries=out[3], nnz=out[4],
-                    rows=out[5])
+                    rows=out[5], csr_equiv_bytes=out[6])
 
 
 def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None) -> Osm:

@@ -666,7 +666,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   // traffic model: algorithmic bytes per CG iteration per subdomain x its iterations
   for (double& t : c.traffic) t = 0;
   const int nloc = c.s_end - c.s_begin;
-  const bool vi = spmv_variant_of(c) == 3;
+  const bool vi = spmv_variant_of(c) >= 3;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1198,6 +1198,17 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
   Ctx& c = ctx_of(h);
   if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
   batch_local_solution(c, b, s, u, n);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (v < 0 || v > 4) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..4");
+  c.spmv_variant = v;
+  drop_graph(c);  // captured launches embed the old kernel
+  if (active) *active = spmv_variant_of(c);
   return OSM_OK;
   OSM_API_END
 }

@@ -221,6 +221,7 @@ struct Ctx {
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;
+  bool vi_per_side = false;  // fold slots per interface side (else per side kind)
   uint16_t* vi_idx = nullptr;
   int16_t* vi_col = nullptr;
   double* vi_dict = nullptr;
@@ -281,7 +282,7 @@ double fnorm2_of(Ctx& c);  // ||f||^2 of the glued global system (osm.cu)
 
 void spmv_init_attributes();
 void gravity_z(Ctx& c, double z0, double* d_out);  // gravity.cu (uses c.phi)
-void vi_build(Ctx& c);
+void vi_build(Ctx& c, bool per_side = false);
 void vi_free(Ctx& c);
 void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side);
 int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)

@@ -104,8 +104,10 @@ void vi_free(Ctx& c) {
 }
 
 // Builds the dictionary, the 16-bit value indices (fold positions -> tuple slots) and the int16
-// column offsets from the fp64 SELL arrays (K^N values, before any Robin fold).
-void vi_build(Ctx& c) {
+// column offsets from the fp64 SELL arrays.  Fold tuples are keyed by the side kind (0: left slab
+// of its interface, 1: right slab) -- shared by every interface, valid while p and q are uniform per
+// kind -- or, with per_side, by the individual side.
+void vi_build(Ctx& c, bool per_side) {
   vi_free(c);
   const int64_t n = c.sell_total;
   if (n == 0) return;
@@ -132,7 +134,8 @@ void vi_build(Ctx& c) {
   std::map<std::tuple<int32_t, double, double, double>, int32_t> tuples;
   std::vector<int32_t> slot(c.nfold, 0);
   for (int64_t e = 0; e < c.nfold; ++e) {
-    auto key = std::make_tuple(side[e], kn[e], m[e], sv[e]);
+    const int32_t key_side = per_side ? side[e] : c.sides[side[e]].which;
+    auto key = std::make_tuple(key_side, kn[e], m[e], sv[e]);
     auto it = tuples.find(key);
     if (it == tuples.end()) it = tuples.emplace(key, (int32_t)(nd + tuples.size())).first;
     slot[e] = it->second;
@@ -217,6 +220,7 @@ void vi_build(Ctx& c) {
   c.vi_idx = nullptr;
   c.vi_col = nullptr;
   c.vi_words = words;
+  c.vi_per_side = per_side;
   c.vi_ok = true;
 }
 
@@ -224,11 +228,34 @@ void vi_build(Ctx& c) {
 // as k_fold_apply rounds it.
 void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side) {
   if (!c.vi_ok || c.vi_fold_tuples.empty()) return;
+  // coefficients per tuple key: the side itself, or the side kind when uniform over interfaces
+  std::vector<double> pk(2, 0.0), qk(2, 0.0);
+  if (!c.vi_per_side) {
+    bool seen[2] = {false, false}, uniform = true;
+    for (size_t k = 0; k < c.sides.size(); ++k) {
+      const int w = c.sides[k].which;
+      if (!seen[w]) {
+        pk[w] = p_side[k];
+        qk[w] = q_side[k];
+        seen[w] = true;
+      } else if (pk[w] != p_side[k] || qk[w] != q_side[k]) {
+        uniform = false;
+      }
+    }
+    if (!uniform) {  // per-interface coefficients: rebuild with per-side slots
+      vi_build(c, true);
+      if (!c.vi_ok) return;
+      vi_apply_robin(c, p_side, q_side);
+      return;
+    }
+  }
   std::vector<double> tail(c.vi_fold_tuples.size());
   for (size_t t = 0; t < tail.size(); ++t) {
     const auto& T = c.vi_fold_tuples[t];
-    volatile double a = p_side[T.side] * T.m;  // no contraction: match __dmul_rn / __dadd_rn
-    volatile double b = q_side[T.side] * T.s;
+    const double pt = c.vi_per_side ? p_side[T.side] : pk[T.side];
+    const double qt = c.vi_per_side ? q_side[T.side] : qk[T.side];
+    volatile double a = pt * T.m;  // no contraction: match __dmul_rn / __dadd_rn
+    volatile double b = qt * T.s;
     volatile double ab = a + b;
     tail[t] = T.kn + ab;
   }

@@ -58,3 +58,23 @@ def test_variants_bitwise_identical(robin):
     prob, rep = oracle_run(CFG, drho, [robin[0]] * (S - 1), [robin[2]] * (S - 1), q=([robin[1]] * (S - 1), [robin[3]] * (S - 1)))
     ok, d = history_ok(ref[1], rep.h)
     assert ok and len(ref[1]) == len(rep.h), d.max()
+
+
+def test_value_indexed_nonuniform_interface_coefficients():
+    """Different (p, q) per interface force per-side dictionary slots; still bitwise equal to fp64."""
+    import paper_2112_03851_b200 as P
+
+    drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=19)
+    hs = []
+    for v in (2, 4):
+        o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+        o.decompose(CFG["nsub"])
+        o.set_robin2([10.0, 14.0], [0.05, 0.0], [3.0, 2.0], [0.2, 0.1])
+        o.assemble()
+        o.set_spmv_variant(v)
+        o.upload_density(drho)
+        st, _ = o.solve(max_outer=300)
+        assert st == 0
+        hs.append(o.history())
+        o.close()
+    assert np.array_equal(hs[0], hs[1])

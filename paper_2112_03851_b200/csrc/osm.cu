@@ -326,8 +326,8 @@ static void assemble(Ctx& c) {
       sd.sub = ls;
       sd.iface = ps.iface;
       sd.which = ps.which;
-      sd.remote = ps.remote != 0;
-      sd.peer = ps.peer;
+      sd.remote = ps.remote != 0 || c.force_remote;
+      sd.peer = c.force_remote ? c.rank : ps.peer;
       const int64_t I = which_plane == 0 ? (int64_t)o * S.g.c0 : (int64_t)o * S.g.c1;
       std::vector<int32_t> mc(nG), mg(nG);
       const int k = (int)c.sides.size();
@@ -354,9 +354,8 @@ static void assemble(Ctx& c) {
   const int nsides = (int)c.sides.size();
   for (int k = 0; k < nsides; ++k) {
     Side& sd = c.sides[k];
-    if (sd.remote) continue;
     for (int j = 0; j < nsides; ++j)
-      if (j != k && c.sides[j].iface == sd.iface) sd.partner = j;
+      if (j != k && c.sides[j].iface == sd.iface) sd.partner = j;  // -1 when the neighbour is on another rank
   }
   c.islot = dupload(c, islot);
   c.lam_all = dalloc<double>(nsides * nG);
@@ -473,11 +472,27 @@ static void apply_robin(Ctx& c) {
 // part 1: [g | u] both directions for every remote side; part 2: the right slab's
 // interface-row residual w to the owner (left slab).
 static void exchange(Ctx& c, int part) {
-  if (c.nranks == 1) return;
+  if (!c.comm) return;
   bool any = false;
   for (const Side& sd : c.sides) any = any || sd.remote;
   if (!any) return;
   const int64_t nG = c.nG;
+  if (c.force_remote) {
+    // every side talks to its own rank: NCCL matches the j-th send with the j-th receive, so each
+    // receive is posted into the partner of the j-th sender
+    OSM_NCCL(ncclGroupStart());
+    for (const Side& sd : c.sides) {
+      if (part == 1) OSM_NCCL(ncclSend(sd.out, 2 * nG, ncclDouble, c.rank, c.comm, c.stream));
+      else if (sd.which == 1) OSM_NCCL(ncclSend(sd.out + 2 * nG, nG, ncclDouble, c.rank, c.comm, c.stream));
+    }
+    for (const Side& sd : c.sides) {
+      const Side& dst = c.sides[sd.partner];
+      if (part == 1) OSM_NCCL(ncclRecv(dst.inbuf, 2 * nG, ncclDouble, c.rank, c.comm, c.stream));
+      else if (sd.which == 1) OSM_NCCL(ncclRecv(dst.inbuf + 2 * nG, nG, ncclDouble, c.rank, c.comm, c.stream));
+    }
+    OSM_NCCL(ncclGroupEnd());
+    return;
+  }
   OSM_NCCL(ncclGroupStart());
   for (const Side& sd : c.sides) {
     if (!sd.remote) continue;
@@ -496,7 +511,7 @@ static void exchange(Ctx& c, int part) {
 // Per-subdomain values (local, in subdomain order) -> all nsub values on every rank.
 static std::vector<double> allgather_sub(Ctx& c, const std::vector<double>& local, int width) {
   const int nloc = c.s_end - c.s_begin;
-  if (c.nranks == 1) return local;
+  if (!c.comm) return local;
   double* d = dalloc<double>((int64_t)c.nsub * width);
   OSM_CUDA(cudaMemcpyAsync(d + (int64_t)c.s_begin * width, local.data(), sizeof(double) * nloc * width,
                            cudaMemcpyHostToDevice, c.stream));
@@ -781,10 +796,15 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
+    if (const char* e = std::getenv("OSM_FORCE_REMOTE")) c.force_remote = std::atoi(e) != 0 && c.nranks == 1;
     if (c.nranks > 1) {
       ncclUniqueId id;
       std::memcpy(&id, d.nccl_uid, sizeof(id));
       OSM_NCCL(ncclCommInitRank(&c.comm, c.nranks, id, c.rank));
+    } else if (c.force_remote) {  // debug: a 1-rank communicator so the NCCL path runs on one GPU
+      ncclUniqueId id;
+      OSM_NCCL(ncclGetUniqueId(&id));
+      OSM_NCCL(ncclCommInitRank(&c.comm, 1, id, 0));
     }
   } catch (...) {
     osm_destroy(h);

@@ -244,7 +244,19 @@ static void assemble(Ctx& c) {
       const int64_t w1 = std::min<int64_t>(S.n, w0 + sigma);
       idx.resize(w1 - w0);
       std::iota(idx.begin(), idx.end(), (int32_t)w0);
-      std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+      if (c.sort_key == 0) {  // row length, descending (minimal SELL padding)
+        std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+      } else {  // lattice parity class (then length when sort_key == 2): same-class rows in spatial order
+        auto cls = [&](int32_t i) {
+          const int64_t I = S.g.I_lo + i % S.g.nI, t = i / S.g.nI, J = 1 + t % S.g.nJ, K = 1 + t / S.g.nJ;
+          return (int)((I % 2) + 2 * (J % 2) + 4 * (K % 2));
+        };
+        std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+          const int ca = cls(a), cb = cls(b);
+          if (ca != cb) return ca < cb;
+          return c.sort_key == 2 ? len[a] > len[b] : false;
+        });
+      }
       for (int64_t k = 0; k < w1 - w0; ++k) {
         perm[w0 + k] = idx[k];
         iperm[idx[k]] = (int32_t)(w0 + k);
@@ -792,6 +804,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
     if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);
     if (const char* e = std::getenv("OSM_UPD")) c.update_variant = std::atoi(e);
+    if (const char* e = std::getenv("OSM_SORT")) c.sort_key = std::atoi(e);
     spmv_init_attributes();
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};

@@ -156,6 +156,13 @@ osm_status osm_upload_density(osm_ctx* ctx, const double* drho, double G);
 /* Same, from a device pointer (nx*ny*nz doubles on the context's device). */
 osm_status osm_upload_density_device(osm_ctx* ctx, const double* drho_dev, double G);
 
+/* Load vector given directly in global free-DOF order (lattice ids increasing, Dirichlet points
+ * removed; n = (o nx - 1)(o ny - 1)(o nz - 1) host doubles), instead of a density (SURVEY 8(b)
+ * "escape hatch").  Each slab takes b_free at its points, halved on its interface planes (the two
+ * slab copies of an interface row share it), so the glued system is K u = b_free.
+ * INVALID_ARG on a size mismatch; STATE before osm_assemble. */
+osm_status osm_upload_load_vector(osm_ctx* ctx, const double* b_free, int64_t n);
+
 /* [collective] Runs the Schwarz iteration from u^0 = lambda^0 = 0.  Returns OK,
  * NOT_CONVERGED (max_outer reached), DIVERGED, or an error.  report may be NULL. */
 osm_status osm_solve(osm_ctx* ctx, const osm_solve_opts* opts, osm_report* report);

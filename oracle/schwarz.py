@@ -39,11 +39,14 @@ class Problem:
     f: np.ndarray  # monolithic load
 
 
-def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=None, monolithic=True) -> Problem:
+def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=None, monolithic=True,
+                  load_free=None) -> Problem:
     """Assemble every K_s^N, b_s, interface maps, M_Gamma and the monolithic K, f.
 
     ``only``: assemble just these subdomains (others are None); ``monolithic=False`` skips K, f
-    (used for bounded timing samples of large workloads).
+    (used for bounded timing samples of large workloads).  ``load_free``: a global free-DOF load
+    vector instead of a density: b_s takes it at the slab's points, halved on the slab's interface
+    planes (the library's osm_upload_load_vector rule), and f = load_free.
     """
     sls = slabs(box, nsub)
     full = slabs(box, 1)[0]
@@ -53,7 +56,9 @@ def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=
             subs.append(Subdomain(sl, None, None, None))
             continue
         KN = fe.assemble_stiffness(box, sl)
-        if load_fn is not None:
+        if load_free is not None:
+            b = None  # filled below from load_free
+        elif load_fn is not None:
             b = fe.assemble_load_function(box, sl, load_fn, quad)
         else:
             b = fe.assemble_load(box, sl, drho)
@@ -63,12 +68,26 @@ def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=
         l, r = interface_map(box, sls[i], sls[i + 1])
         subs[i].right = l
         subs[i + 1].left = r
+    if load_free is not None:
+        for sub in subs:
+            if sub.KN is None:
+                continue
+            b = np.asarray(load_free, dtype=np.float64)[sub.gidx].copy()
+            for idx in (sub.left, sub.right):
+                if idx is not None:
+                    b[idx] *= 0.5
+            sub.b = b
     MG = fe.interface_mass(box)
     SG = fe.interface_stiffness(box)
     if not monolithic:
         return Problem(box, nsub, subs, MG, SG, None, None)
     K = fe.assemble_stiffness(box, full)
-    f = fe.assemble_load_function(box, full, load_fn, quad) if load_fn is not None else fe.assemble_load(box, full, drho)
+    if load_free is not None:
+        f = np.asarray(load_free, dtype=np.float64).copy()
+    elif load_fn is not None:
+        f = fe.assemble_load_function(box, full, load_fn, quad)
+    else:
+        f = fe.assemble_load(box, full, drho)
     return Problem(box, nsub, subs, MG, SG, K, f)
 
 

@@ -33,7 +33,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
-               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant"]
+               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector"]
 
 
 class MeshDesc(C.Structure):
@@ -112,6 +112,7 @@ _sigs = {
     "osm_cmaes_tell": (C.c_int, [_P, _pd]),
     "osm_cmaes_state": (C.c_int, [_P, _pd, _pd, _pd, _pd, _pd, _pint]),
     "osm_cmaes_should_stop": (C.c_int, [_P, C.c_int, C.c_double, _pint]),
+    "osm_upload_load_vector": (C.c_int, [_P, _pd, C.c_int64]),
     "osm_set_spmv_variant": (C.c_int, [_P, C.c_int, _pint]),
     "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
@@ -287,6 +288,11 @@ class Osm:
         if d.size != self.mesh.nx * self.mesh.ny * self.mesh.nz:
             raise ValueError("density must have nx*ny*nz cells")
         _check(_lib.osm_upload_density(self._h, _ptr(d, C.c_double), float(G)))
+
+    def upload_load_vector(self, b_free):
+        """Global free-DOF load vector (osm_upload_load_vector); interface rows split half/half."""
+        b = np.ascontiguousarray(b_free, dtype=np.float64)
+        _check(_lib.osm_upload_load_vector(self._h, _ptr(b, C.c_double), b.size))
 
     def upload_density_device(self, ptr: int, G=6.672e-11):
         _check(_lib.osm_upload_density_device(self._h, C.c_void_p(ptr), float(G)))

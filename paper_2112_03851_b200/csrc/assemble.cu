@@ -92,6 +92,20 @@ __global__ void k_load(SlabGeom g, int64_t n, StencilDev T, const double* __rest
   b[row0 + iperm[i]] = s;
 }
 
+// Load from a global free-DOF vector (osm_upload_load_vector): b_s = b_free at the slab's points,
+// halved on the slab's interface planes (the two duplicates of an interface row share the load,
+// so b_s + b_t = b_free there and the glued system is the monolithic one).
+__global__ void k_load_free(SlabGeom g, int64_t n, int64_t Nx, const double* __restrict__ bfree,
+                            const int32_t* __restrict__ iperm, int64_t row0, double* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t I, J, K;
+  lattice_of(g, i, I, J, K);
+  const int64_t gi = (I - 1) + (Nx - 2) * ((J - 1) + (g.Ny - 2) * (K - 1));
+  const bool iface = (g.c0 > 0 && I == g.order * g.c0) || (g.c1 < g.nx && I == g.order * g.c1);
+  b[row0 + iperm[i]] = iface ? 0.5 * bfree[gi] : bfree[gi];
+}
+
 // Copy contract CSR rows into SELL-256 tiles (column-major over the tile), remapping
 // columns to internal concatenated indices; padding = (val 0, col = own row).  Also dinv from K^N.
 __global__ void k_sell_build(int64_t npad, int64_t row0, int64_t blk0, const int32_t* __restrict__ perm,
@@ -270,6 +284,13 @@ void launch_fold_apply(const Ctx& c, const double* d_alpha_side, const double* d
 
 void launch_load(const Ctx& c, const Sub& s, double fourpiG) {
   k_load<<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, tables_of(c), c.drho, fourpiG, s.iperm, s.row0, c.b);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+}
+
+void launch_load_free(const Ctx& c, const Sub& s, const double* d_bfree) {
+  k_load_free<<<grid_for(s.n), 256, 0, c.stream>>>(s.g, s.n, c.mesh.order * c.mesh.nx + 1, d_bfree, s.iperm, s.row0,
+                                                  c.b);
   OSM_CHECK_LAUNCH();
   ++c.launches;
 }

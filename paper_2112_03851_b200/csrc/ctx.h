@@ -258,6 +258,7 @@ void launch_sell_build(const Ctx& c, const Sub& s, const int32_t* d_slice_width_
 void launch_fold_build(const Ctx& c, const Side& sd, const Sub& s);
 void launch_fold_apply(const Ctx& c, const double* d_alpha_side, const double* d_q_side);
 void launch_load(const Ctx& c, const Sub& s, double fourpiG);
+void launch_load_free(const Ctx& c, const Sub& s, const double* d_bfree);
 void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned);
 void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract);
 

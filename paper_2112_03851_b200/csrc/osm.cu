@@ -933,6 +933,23 @@ static void upload_density(Ctx& c, const double* drho, bool device, double G) {
   c.density_set = true;
 }
 
+osm_status osm_upload_load_vector(osm_ctx* h, const double* b_free, int64_t n) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!c.assembled) fail(OSM_ERR_STATE, "osm_assemble must precede osm_upload_load_vector");
+  const int o = c.mesh.order;
+  const int64_t N = (o * c.mesh.nx - 1) * (o * c.mesh.ny - 1) * (o * c.mesh.nz - 1);
+  if (!b_free || n != N) fail(OSM_ERR_INVALID_ARG, "load vector must hold the global free DOFs");
+  double* d = dalloc<double>(N);
+  OSM_CUDA(cudaMemcpyAsync(d, b_free, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+  for (const Sub& S : c.subs) launch_load_free(c, S, d);
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  dfree(d);
+  c.density_set = true;
+  return OSM_OK;
+  OSM_API_END
+}
+
 osm_status osm_upload_density(osm_ctx* h, const double* drho, double G) {
   OSM_API_BEGIN
   upload_density(ctx_of(h), drho, false, G);

@@ -66,6 +66,24 @@ def chicxulub(nx, ny, nz, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2
     return np.ascontiguousarray(out.ravel(), dtype=np.float64)
 
 
+def manufactured_cell_average(nx, ny, nz, lx=1.0, ly=1.0, lz=1.0):
+    """Cell averages of f = 3 pi^2 sin(pi x/lx) sin(pi y/ly) sin(pi z/lz) (unit cube: f = -Delta u for
+    u = sin sin sin), closed form: the average of sin(pi x/L) over [a, b] is
+    L (cos(pi a/L) - cos(pi b/L)) / (pi (b - a)).  Returned as f values per cell (x fastest); divide by
+    4 pi G for a density."""
+    def avg(n, L):
+        e = np.arange(n + 1) * (L / n)
+        return L * (np.cos(np.pi * e[:-1] / L) - np.cos(np.pi * e[1:] / L)) / (np.pi * (L / n))
+    ax, ay, az = avg(nx, lx), avg(ny, ly), avg(nz, lz)
+    f = 3 * np.pi ** 2 * az[:, None, None] * ay[None, :, None] * ax[None, None, :]
+    return np.ascontiguousarray(f.ravel(), dtype=np.float64)
+
+
+def random_load(n, seed=0):
+    """i.i.d. N(0,1) global load vector (for osm_upload_load_vector parity)."""
+    return np.random.Generator(np.random.PCG64(seed)).standard_normal(n)
+
+
 def random_field(nx, ny, nz, seed=0, scale=1000.0):
     rng = np.random.Generator(np.random.PCG64(seed))
     return rng.normal(0.0, scale, size=nx * ny * nz).astype(np.float64)

@@ -460,3 +460,31 @@ def test_divergence_flag():
     except linalg.PrecondError:
         return  # negative alpha may already break the preconditioner: also an error path
     assert rep.diverged or not rep.converged
+
+
+def test_synth_manufactured_cell_average():
+    """The closed-form cell averages equal a high-order quadrature of f over each cell (input check)."""
+    n = 3
+    f = synth.manufactured_cell_average(n, n, n)
+    g, w = np.polynomial.legendre.leggauss(8)
+    t, wt = 0.5 * (g + 1) / n, 0.5 * w
+    ref = np.zeros((n, n, n))
+    for k in range(n):
+        for j in range(n):
+            for i in range(n):
+                xs, ys, zs = i / n + t, j / n + t, k / n + t
+                Z, Y, X = np.meshgrid(zs, ys, xs, indexing="ij")
+                W = wt[:, None, None] * wt[None, :, None] * wt[None, None, :]
+                ref[k, j, i] = np.sum(W * 3 * np.pi**2 * np.sin(np.pi * X) * np.sin(np.pi * Y) * np.sin(np.pi * Z))
+    assert np.allclose(f, ref.ravel(), rtol=1e-12)
+
+
+def test_load_free_split_is_monolithic():
+    """A global load split half/half on interface rows gives the monolithic solution (Schwarz fixed point)."""
+    box = mesh.Box(5, 4, 3, 1.0, 0.8, 0.6, 2)
+    b = synth.random_load(box.n_free, seed=3)
+    prob = schwarz.build_problem(box, 2, load_free=b)
+    rep = schwarz.schwarz(prob, schwarz.robin_operators(prob, [10.0], [10.0]), tol_outer=1e-11, tol_inner=1e-12)
+    us = schwarz.monolithic(prob)
+    assert np.linalg.norm(rep.ut - us) / np.linalg.norm(us) < 1e-9
+    assert sum(sub.b.sum() for sub in prob.subs) == pytest.approx(b.sum(), rel=1e-12)

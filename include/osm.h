@@ -183,6 +183,10 @@ typedef struct osm_batch_report {
 } osm_batch_report;
 osm_status osm_solve_batch(osm_ctx* ctx, int B, const double* alphas, const osm_solve_opts* opts,
                            osm_batch_report* report);
+/* OO2 batch: pq host array [b][4][iface]: (p_left, q_left, p_right, q_right) of interface i,
+ * i.e. pq[(b*4 + j)*(nsub-1) + i]; A_b = p M_Gamma + q S_Gamma per side (as osm_set_robin2). */
+osm_status osm_solve_batch2(osm_ctx* ctx, int B, const double* pq, const osm_solve_opts* opts,
+                            osm_batch_report* report);
 /* h_b(1..N_b) of candidate b of the last batched solve.  h == NULL: *n = N_b. */
 osm_status osm_get_batch_history(osm_ctx* ctx, int b, double* h, int cap, int* n);
 /* PCG iterations [n][s] (local subdomains) of candidate b.  its == NULL: *n = N_b * nsub_local. */

@@ -33,7 +33,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
-               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector"]
+               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector", "osm_solve_batch2"]
 
 
 class MeshDesc(C.Structure):
@@ -112,6 +112,7 @@ _sigs = {
     "osm_cmaes_tell": (C.c_int, [_P, _pd]),
     "osm_cmaes_state": (C.c_int, [_P, _pd, _pd, _pd, _pd, _pd, _pint]),
     "osm_cmaes_should_stop": (C.c_int, [_P, C.c_int, C.c_double, _pint]),
+    "osm_solve_batch2": (C.c_int, [_P, C.c_int, _pd, C.POINTER(SolveOpts), C.POINTER(BatchReport)]),
     "osm_upload_load_vector": (C.c_int, [_P, _pd, C.c_int64]),
     "osm_set_spmv_variant": (C.c_int, [_P, C.c_int, _pint]),
     "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
@@ -316,6 +317,17 @@ class Osm:
         opts = SolveOpts(tol_outer, max_outer, tol_inner, max_inner, int(warm_start), 0)
         rep = BatchReport()
         _check(_lib.osm_solve_batch(self._h, B, _ptr(a, C.c_double), C.byref(opts), C.byref(rep)))
+        return rep
+
+    def solve_batch2(self, p_left, q_left, p_right, q_right, tol_outer=1e-8, max_outer=500, tol_inner=1e-10,
+                     max_inner=20000, warm_start=True):
+        """OO2 batched solve: each argument is a (B, nsub-1) array (osm_solve_batch2)."""
+        arrs = [np.atleast_2d(np.asarray(v, dtype=np.float64)) for v in (p_left, q_left, p_right, q_right)]
+        B = arrs[0].shape[0]
+        pq = np.ascontiguousarray(np.stack(arrs, axis=1))  # [b][4][iface]
+        opts = SolveOpts(tol_outer, max_outer, tol_inner, max_inner, int(warm_start), 0)
+        rep = BatchReport()
+        _check(_lib.osm_solve_batch2(self._h, B, _ptr(pq, C.c_double), C.byref(opts), C.byref(rep)))
         return rep
 
     def batch_history(self, b):

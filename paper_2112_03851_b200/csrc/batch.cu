@@ -46,9 +46,13 @@ struct BatchDev {
   const int32_t* mrow;
   const int32_t* mcol;
   const double* mval;
+  const double* sval;       // S_Gamma values (OO2), aligned with mval
   const double* mdiag;      // [nG]
-  const double* alpha_own;  // [nsides][kB]
-  const double* alpha_sum;  // [nsides][kB]
+  const double* sdiag;      // [nG]
+  const double* alpha_own;  // p of the side, [nsides][kB]
+  const double* alpha_sum;  // p_s + p_t, [nsides][kB]
+  const double* q_own;      // q of the side (OO2), [nsides][kB]
+  const double* q_sum;      // q_s + q_t, [nsides][kB]
   const int32_t* side_which;   // [nsides]
   const int32_t* side_partner; // [nsides]
   const int32_t* cand_active;  // [kB]
@@ -67,8 +71,8 @@ struct BatchBuf {
   int32_t *blk_sub = nullptr, *blk_nrow = nullptr;
   int64_t* blk_row0 = nullptr;
   int32_t* mapg = nullptr;
-  double* mdiag = nullptr;
-  double *alpha_own = nullptr, *alpha_sum = nullptr;
+  double *mdiag = nullptr, *sdiag = nullptr;
+  double *alpha_own = nullptr, *alpha_sum = nullptr, *q_own = nullptr, *q_sum = nullptr;
   int32_t *side_which = nullptr, *side_partner = nullptr, *cand_active = nullptr;
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *ut = nullptr;
   double *lam = nullptr, *unbr = nullptr, *wif = nullptr, *out = nullptr;
@@ -86,10 +90,13 @@ struct BatchBuf {
 
 namespace {
 
-// dinv of K_b = K^N + alpha_b M on the fly
+// dinv of K_b = K^N + p_b M + q_b S on the fly (rounded like the single path's fold)
 __device__ __forceinline__ double dinv_b(const BatchDev& D, int64_t row, int sl, int b) {
   double d = D.dkn[row];
-  if (sl >= 0) d = __dadd_rn(d, __dmul_rn(D.alpha_own[(sl / D.nG) * kB + b], D.mdiag[sl % D.nG]));
+  if (sl >= 0) {
+    const int k = sl / (int)D.nG, g = sl % (int)D.nG;
+    d = __dadd_rn(d, __dadd_rn(__dmul_rn(D.alpha_own[k * kB + b], D.mdiag[g]), __dmul_rn(D.q_own[k * kB + b], D.sdiag[g])));
+  }
   return d > 0.0 ? 1.0 / d : 0.0;
 }
 
@@ -171,18 +178,20 @@ __global__ void __launch_bounds__(kBT) kb_spmm(BatchDev D, BState* __restrict__ 
       }
     }
     const int sl = D.islot[row];
-    if (MODE != MODE_RESID && sl >= 0) {  // + alpha_b M_Gamma X on the interface rows
+    if (MODE != MODE_RESID && sl >= 0) {  // + (p_b M_Gamma + q_b S_Gamma) X on the interface rows
       const int side = sl / (int)D.nG, g = sl % (int)D.nG;
+      const double p0 = D.alpha_own[side * kB + b0], p1 = D.alpha_own[side * kB + b1];
+      const double q0 = D.q_own[side * kB + b0], q1 = D.q_own[side * kB + b1];
       double m0 = 0.0, m1 = 0.0;
       for (int j = D.mrow[g]; j < D.mrow[g + 1]; ++j) {
-        const double mv = D.mval[j];
+        const double mv = D.mval[j], sv = D.sval[j];
         const int64_t cr = D.mapg[side * D.nG + D.mcol[j]];
         const double2 xv = reinterpret_cast<const double2*>(X + cr * kB)[lane];
-        m0 = fma(mv, xv.x, m0);
-        m1 = fma(mv, xv.y, m1);
+        m0 = fma(fma(p0, mv, q0 * sv), xv.x, m0);
+        m1 = fma(fma(p1, mv, q1 * sv), xv.y, m1);
       }
-      y0 = fma(D.alpha_own[side * kB + b0], m0, y0);
-      y1 = fma(D.alpha_own[side * kB + b1], m1, y1);
+      y0 += m0;
+      y1 += m1;
     }
     const int64_t e = row * kB;
     if (MODE == MODE_CG) {
@@ -385,10 +394,12 @@ __global__ void kb_trace(BatchDev D, const double* __restrict__ x, const double*
   const int64_t g = i / kB;
   const int b = (int)(i % kB);
   if (!D.cand_active[b]) return;
+  const double ps = D.alpha_sum[k * kB + b], qs = D.q_sum[k * kB + b];
   double mu = 0.0;
-  for (int j = D.mrow[g]; j < D.mrow[g + 1]; ++j) mu = fma(D.mval[j], x[(int64_t)D.mapg[k * D.nG + D.mcol[j]] * kB + b], mu);
+  for (int j = D.mrow[g]; j < D.mrow[g + 1]; ++j)
+    mu = fma(fma(ps, D.mval[j], qs * D.sval[j]), x[(int64_t)D.mapg[k * D.nG + D.mcol[j]] * kB + b], mu);
   double* o = out + (int64_t)k * 3 * D.nG * kB;
-  o[i] = D.alpha_sum[k * kB + b] * mu - lam[(int64_t)k * D.nG * kB + i];
+  o[i] = mu - lam[(int64_t)k * D.nG * kB + i];
   o[D.nG * kB + i] = x[(int64_t)D.mapg[k * D.nG + g] * kB + b];
 }
 
@@ -474,7 +485,7 @@ void batch_free(Ctx& c) {
   BatchBuf* B = c.batch;
   if (!B) return;
   void* ptrs[] = {B->rowptr, B->col, B->val, B->dkn, B->b, B->islot, B->blk_sub, B->blk_nrow, B->blk_row0, B->mapg,
-                  B->mdiag, B->alpha_own, B->alpha_sum, B->side_which, B->side_partner, B->cand_active, B->x, B->r,
+                  B->mdiag, B->sdiag, B->q_own, B->q_sum, B->alpha_own, B->alpha_sum, B->side_which, B->side_partner, B->cand_active, B->x, B->r,
                   B->p, B->q, B->ut, B->lam, B->unbr, B->wif, B->out, B->st, B->cnt, B->nact, B->d_nactive,
                   B->part, B->side_sum};
   for (void* p : ptrs)
@@ -569,13 +580,19 @@ static void batch_setup(Ctx& c) {
   up(mapg, B->mapg);
   up(which, B->side_which);
   up(partner, B->side_partner);
-  std::vector<double> md(std::max<int64_t>(1, nG), 0.0);
+  std::vector<double> md(std::max<int64_t>(1, nG), 0.0), sd(std::max<int64_t>(1, nG), 0.0);
   for (int64_t g = 0; g < nG; ++g)
     for (int j = c.h_mrow[g]; j < c.h_mrow[g + 1]; ++j)
-      if (c.h_mcol[j] == g) md[g] = c.h_mval[j];
+      if (c.h_mcol[j] == g) {
+        md[g] = c.h_mval[j];
+        sd[g] = c.h_sval[j];
+      }
   up(md, B->mdiag);
+  up(sd, B->sdiag);
   B->alpha_own = balloc<double>(std::max(1, nsides) * kB);
   B->alpha_sum = balloc<double>(std::max(1, nsides) * kB);
+  B->q_own = balloc<double>(std::max(1, nsides) * kB);
+  B->q_sum = balloc<double>(std::max(1, nsides) * kB);
   B->cand_active = balloc<int32_t>(kB);
   const int64_t nv = nrows * kB;
   B->x = balloc<double>(nv);
@@ -617,9 +634,13 @@ static BatchDev batch_view(const Ctx& c) {
   D.mrow = c.d_mrow;
   D.mcol = c.d_mcol;
   D.mval = c.d_mval;
+  D.sval = c.d_sval;
   D.mdiag = B->mdiag;
+  D.sdiag = B->sdiag;
   D.alpha_own = B->alpha_own;
   D.alpha_sum = B->alpha_sum;
+  D.q_own = B->q_own;
+  D.q_sum = B->q_sum;
   D.side_which = B->side_which;
   D.side_partner = B->side_partner;
   D.cand_active = B->cand_active;
@@ -628,18 +649,19 @@ static BatchDev batch_view(const Ctx& c) {
   return D;
 }
 
-osm_status solve_batch(Ctx& c, int nB, const double* alphas, const osm_solve_opts& o, osm_batch_report* rep) {
+osm_status solve_batch(Ctx& c, int nB, const double* pq, const osm_solve_opts& o, osm_batch_report* rep) {
   if (!c.assembled || !c.density_set) fail(OSM_ERR_STATE, "assemble and upload a density before osm_solve_batch");
   if (c.nranks != 1) fail(OSM_ERR_INVALID_ARG, "osm_solve_batch runs on a single rank");
   if (nB < 1 || nB > kB) fail(OSM_ERR_INVALID_ARG, "need 1 <= B <= 64");
-  if (c.nsub > 1 && !alphas) fail(OSM_ERR_INVALID_ARG, "NULL alphas");
+  if (c.nsub > 1 && !pq) fail(OSM_ERR_INVALID_ARG, "NULL coefficients");
   const int ni = c.nsub - 1;
-  for (int i = 0; i < nB * 2 * ni; ++i)
-    if (!(alphas[i] >= 0) || !std::isfinite(alphas[i])) fail(OSM_ERR_ILL_POSED, "alpha must be finite and >= 0");
+  // pq: [b][4][iface] = p_left, q_left, p_right, q_right
+  for (int i = 0; i < nB * 4 * ni; ++i)
+    if (!(pq[i] >= 0) || !std::isfinite(pq[i])) fail(OSM_ERR_ILL_POSED, "coefficients must be finite and >= 0");
   for (int bb = 0; bb < nB; ++bb)
     for (int i = 0; i < ni; ++i)
-      if (alphas[(bb * 2 + 0) * ni + i] == 0 && alphas[(bb * 2 + 1) * ni + i] == 0)
-        fail(OSM_ERR_ILL_POSED, "alpha = 0 on both sides of an interface");
+      if (pq[(bb * 4 + 0) * ni + i] == 0 && pq[(bb * 4 + 2) * ni + i] == 0)
+        fail(OSM_ERR_ILL_POSED, "p = 0 on both sides of an interface");
   const auto t0 = std::chrono::steady_clock::now();
   batch_setup(c);
   BatchBuf* B = c.batch;
@@ -648,14 +670,21 @@ osm_status solve_batch(Ctx& c, int nB, const double* alphas, const osm_solve_opt
   const int64_t nG = c.nG;
   // alpha per side per candidate
   std::vector<double> aown(std::max(1, nsides) * kB, 0.0), asum(std::max(1, nsides) * kB, 0.0);
+  std::vector<double> qown(std::max(1, nsides) * kB, 0.0), qsum(std::max(1, nsides) * kB, 0.0);
   for (int k = 0; k < nsides; ++k)
     for (int bb = 0; bb < nB; ++bb) {
-      const double al = alphas[(bb * 2 + 0) * ni + c.sides[k].iface], ar = alphas[(bb * 2 + 1) * ni + c.sides[k].iface];
-      aown[k * kB + bb] = c.sides[k].which == 0 ? al : ar;
-      asum[k * kB + bb] = al + ar;
+      const int i = c.sides[k].iface;
+      const double pl = pq[(bb * 4 + 0) * ni + i], ql = pq[(bb * 4 + 1) * ni + i];
+      const double pr = pq[(bb * 4 + 2) * ni + i], qr = pq[(bb * 4 + 3) * ni + i];
+      aown[k * kB + bb] = c.sides[k].which == 0 ? pl : pr;
+      qown[k * kB + bb] = c.sides[k].which == 0 ? ql : qr;
+      asum[k * kB + bb] = pl + pr;
+      qsum[k * kB + bb] = ql + qr;
     }
   OSM_CUDA(cudaMemcpyAsync(B->alpha_own, aown.data(), sizeof(double) * aown.size(), cudaMemcpyHostToDevice, c.stream));
   OSM_CUDA(cudaMemcpyAsync(B->alpha_sum, asum.data(), sizeof(double) * asum.size(), cudaMemcpyHostToDevice, c.stream));
+  OSM_CUDA(cudaMemcpyAsync(B->q_own, qown.data(), sizeof(double) * qown.size(), cudaMemcpyHostToDevice, c.stream));
+  OSM_CUDA(cudaMemcpyAsync(B->q_sum, qsum.data(), sizeof(double) * qsum.size(), cudaMemcpyHostToDevice, c.stream));
   // load vector in contract order (from the single-candidate internal b)
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];

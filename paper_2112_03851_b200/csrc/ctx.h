@@ -276,7 +276,7 @@ void launch_iface_w(Ctx& c);
 void launch_iface_sum(Ctx& c);
 
 // ---- batched alpha (batch.cu)
-osm_status solve_batch(Ctx& c, int B, const double* alphas, const osm_solve_opts& o, osm_batch_report* rep);
+osm_status solve_batch(Ctx& c, int B, const double* pq, const osm_solve_opts& o, osm_batch_report* rep);
 void batch_history(const Ctx& c, int b, double* h, int cap, int* n);
 void batch_inner(const Ctx& c, int b, int32_t* its, int cap, int* n);
 void batch_local_solution(Ctx& c, int b, int s, double* u, int64_t* n);

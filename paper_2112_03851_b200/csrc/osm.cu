@@ -1221,7 +1221,24 @@ osm_status osm_solve_batch(osm_ctx* h, int B, const double* alphas, const osm_so
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
   if (!o) fail(OSM_ERR_INVALID_ARG, "NULL options");
-  return solve_batch(c, B, alphas, *o, rep);
+  if (B < 1 || B > 64) fail(OSM_ERR_INVALID_ARG, "need 1 <= B <= 64");
+  const int ni = c.nsub - 1;
+  std::vector<double> pq((size_t)B * 4 * std::max(ni, 0), 0.0);  // OO0: q = 0
+  if (ni > 0 && !alphas) fail(OSM_ERR_INVALID_ARG, "NULL alphas");
+  for (int b = 0; b < B; ++b)
+    for (int i = 0; i < ni; ++i) {
+      pq[(b * 4 + 0) * ni + i] = alphas[(b * 2 + 0) * ni + i];
+      pq[(b * 4 + 2) * ni + i] = alphas[(b * 2 + 1) * ni + i];
+    }
+  return solve_batch(c, B, pq.data(), *o, rep);
+  OSM_API_END
+}
+
+osm_status osm_solve_batch2(osm_ctx* h, int B, const double* pq, const osm_solve_opts* o, osm_batch_report* rep) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!o) fail(OSM_ERR_INVALID_ARG, "NULL options");
+  return solve_batch(c, B, pq, *o, rep);
   OSM_API_END
 }
 

@@ -80,3 +80,28 @@ def test_batch_errors():
     with pytest.raises(P.OsmError):
         o.solve_batch(np.ones((65, 1)), np.ones((65, 1)))  # B > 64
     o.close()
+
+
+def test_oo2_batch_matches_oracle():
+    """osm_solve_batch2: each OO2 candidate (p1, q1, p2, q2) follows the oracle's iteration."""
+    import paper_2112_03851_b200 as P
+
+    drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=37)
+    cands = [(10.0, 0.05, 4.0, 0.2), (20.0, 0.0, 3.0, 0.1), (6.0, 0.1, 6.0, 0.1)]
+    o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+    o.decompose(CFG["nsub"])
+    o.set_robin(np.full(2, 20.0), np.full(2, 20.0))
+    o.assemble()
+    o.upload_density(drho)
+    arr = np.array(cands)
+    rep = o.solve_batch2(*[np.repeat(arr[:, j:j + 1], 2, axis=1) for j in (0, 1, 2, 3)], max_outer=400)
+    box = mesh.Box(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+    prob = schwarz.build_problem(box, CFG["nsub"], drho=drho)
+    for b, (p1, q1, p2, q2) in enumerate(cands):
+        orep = schwarz.schwarz(prob, schwarz.robin_operators(prob, [p1] * 2, [p2] * 2, [q1] * 2, [q2] * 2),
+                               tol_outer=1e-8, max_outer=400)
+        ok, d = history_ok(o.batch_history(b), orep.h)
+        assert ok and len(o.batch_history(b)) == len(orep.h), (b, d.max())
+        for s in range(CFG["nsub"]):
+            assert rel_l2(o.batch_local_solution(b, s), orep.u[s]) <= 1e-10
+    o.close()

@@ -215,7 +215,8 @@ struct Ctx {
   bool use_graph = true;
   bool force_remote = false;  // debug: every side goes through NCCL (peer = own rank), see osm_create
   int update_variant = 0;  // 0: k_cg_update at 96 regs, 1: capped for 8 blocks/SM
-  int sort_key = 2;  // SELL row order inside sigma windows: 0 length desc, 1 parity class, 2 class then length
+  int sort_key = 3;  // SELL row order inside sigma windows: 0 length desc, 1 parity class, 2 class then length,
+                    // 3 class, length, then (K, I, J) with J fastest (default)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
   int spmv_variant = 4;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
                          // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary

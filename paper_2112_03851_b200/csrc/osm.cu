@@ -12,13 +12,22 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "ctx.h"
 
 namespace osm {
 
 thread_local std::string g_last_error;
+
+// NVTX ranges (tracing) around the phases of a solve; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define OSM_NCCL(call)                                                                         \
   do {                                                                                         \
@@ -246,16 +255,16 @@ static void assemble(Ctx& c) {
       std::iota(idx.begin(), idx.end(), (int32_t)w0);
       if (c.sort_key == 0) {  // row length, descending (minimal SELL padding)
         std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
-      } else {  // lattice parity class (then length when sort_key == 2): same-class rows in spatial order
-        auto cls = [&](int32_t i) {
+      } else {  // lattice parity class (then length when sort_key >= 2): same-class rows in spatial order;
+                // sort_key 3 also orders a class by (K, I, J) so warps run along the long y axis and
+                // their gathers hit consecutive addresses of the neighbour class
+        auto key = [&](int32_t i) {
           const int64_t I = S.g.I_lo + i % S.g.nI, t = i / S.g.nI, J = 1 + t % S.g.nJ, K = 1 + t / S.g.nJ;
-          return (int)((I % 2) + 2 * (J % 2) + 4 * (K % 2));
+          const int cls = (int)((I % 2) + 2 * (J % 2) + 4 * (K % 2));
+          return std::make_tuple(cls, c.sort_key >= 2 ? -len[i] : 0, c.sort_key == 3 ? K : 0, c.sort_key == 3 ? I : 0,
+                                 c.sort_key == 3 ? J : 0);
         };
-        std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
-          const int ca = cls(a), cb = cls(b);
-          if (ca != cb) return ca < cb;
-          return c.sort_key == 2 ? len[a] > len[b] : false;
-        });
+        std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return key(a) < key(b); });
       }
       for (int64_t k = 0; k < w1 - w0; ++k) {
         perm[w0 + k] = idx[k];
@@ -618,6 +627,7 @@ static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
 }
 
 static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
+  NvtxRange nv_solve("osm_solve");
   if (!c.assembled) fail(OSM_ERR_STATE, "osm_assemble must precede osm_solve");
   if (!c.density_set) fail(OSM_ERR_STATE, "osm_upload_density must precede osm_solve");
   if (o.max_outer < 1 || o.max_inner < 1 || !(o.tol_outer > 0) || !(o.tol_inner > 0))
@@ -639,6 +649,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   int64_t inner_total = 0;
   int inner_maxed = 0;
   for (int n = 1; n <= o.max_outer; ++n) {
+    NvtxRange nv_outer("schwarz_iteration");
     if (!o.warm_start) OSM_CUDA(cudaMemsetAsync(c.x, 0, sizeof(double) * c.nrows_total, c.stream));
     OSM_CUDA(cudaMemsetAsync(c.d_nactive, 0, sizeof(int32_t), c.stream));
     launch_warm(c, o.tol_inner, o.warm_start);
@@ -646,6 +657,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[0], c.d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
     OSM_CUDA(cudaStreamSynchronize(c.stream));
     if (c.h_nactive[0] > 0) {
+      NvtxRange nv_pcg("batched_pcg");
       // batched masked PCG: enqueue chunks; poll the active count one chunk behind
       for (int ch = 0;; ++ch) {
         enqueue_cg_chunk(c, o.tol_inner, o.max_inner);
@@ -659,9 +671,13 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
         if ((int64_t)ch * kCgChunk > (int64_t)o.max_inner + 2 * kCgChunk) break;  // safety net
       }
     }
-    launch_trace(c);
-    exchange(c, 1);
-    launch_accept(c);
+    {
+      NvtxRange nv_x("trace_exchange");
+      launch_trace(c);
+      exchange(c, 1);
+      launch_accept(c);
+    }
+    NvtxRange nv_r("glued_residual");
     std::vector<int32_t> its;
     const double r2 = glued_residual2(c, 0, &its);
     const double h = fnorm > 0 ? std::sqrt(r2) / fnorm : std::sqrt(r2);

@@ -263,13 +263,26 @@ typedef struct osm_plan_side {
 osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, int* s_end, osm_plan_side* sides,
                     int cap, int* nsides);
 
-/* SpMV implementation of the PCG kernels (all give bitwise-identical iterations):
+/* SpMV implementation of the PCG kernels (all give bitwise-identical iterations for a given row
+ * order, up to the sign of exact zeros):
  * 0 fp64 SELL-256, LDG rows; 1 fp64 SELL-256, warp-specialized cp.async.bulk pipeline;
  * 2 fp64 SELL-256, LDG rows at 32 registers; 3 value-indexed (16-bit dictionary index + 16-bit
- * column offset); 4 = 3 with the dictionary in shared memory (default).  Variants 3/4 fall back
- * to 2 when the matrix does not admit the value-indexed copy.  *active (may be NULL) receives the
- * variant that will actually run.  INVALID_ARG for other values. */
+ * column offset); 4 = 3 with the dictionary in shared memory (default); 5 matrix-free Kuhn
+ * stencil (the K_s values are uniform per parity class and row kind on the
+ * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row
+ * order 4, see osm_set_row_order).  Variants 3/4 fall back to 2 when the matrix does not admit
+ * the value-indexed copy; 5 falls back to 4 without row order 4 or when a slab is too thin for
+ * the tables.  *active (may be NULL) receives the variant that will actually run.  INVALID_ARG
+ * for other values. */
 osm_status osm_set_spmv_variant(osm_ctx* ctx, int variant, int* active);
+
+/* Internal row order of the GPU copy (a permutation private to the library; results are
+ * independent of it up to reduction order).  0 SELL rows by length in sigma windows; 1 by parity
+ * class; 2 class then length; 3 class, length, then lattice (K, I, J) (default); 4 the class-major
+ * lattice layout of the matrix-free variant: every lattice point of the slab box has a row, the
+ * Dirichlet points being inert zero rows (+4..12 % rows).  Must precede osm_assemble (STATE after
+ * it); INVALID_ARG outside 0..4. */
+osm_status osm_set_row_order(osm_ctx* ctx, int order);
 
 /* Number of this library's kernel launches on the context's stream since
  * creation (every kernel of setup, solve and readback). */

@@ -33,7 +33,8 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_get_batch_history", "osm_get_batch_inner_iters", "osm_get_batch_local_solution",
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
-               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector", "osm_solve_batch2"]
+               "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector", "osm_solve_batch2",
+               "osm_set_row_order"]
 
 
 class MeshDesc(C.Structure):
@@ -115,6 +116,7 @@ _sigs = {
     "osm_solve_batch2": (C.c_int, [_P, C.c_int, _pd, C.POINTER(SolveOpts), C.POINTER(BatchReport)]),
     "osm_upload_load_vector": (C.c_int, [_P, _pd, C.c_int64]),
     "osm_set_spmv_variant": (C.c_int, [_P, C.c_int, _pint]),
+    "osm_set_row_order": (C.c_int, [_P, C.c_int]),
     "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
@@ -452,6 +454,10 @@ class Osm:
         _check(_lib.osm_set_spmv_variant(self._h, int(v), C.byref(a)))
         return a.value
 
+    def set_row_order(self, order: int) -> None:
+        """Internal row order of the GPU copy (include/osm.h); 4 enables the matrix-free SpMV (variant 5)."""
+        _check(_lib.osm_set_row_order(self._h, int(order)))
+
     def launch_count(self) -> int:
         n = C.c_int64(0)
         _check(_lib.osm_get_launch_count(self._h, C.byref(n)))
@@ -464,10 +470,15 @@ class Osm:
                     rows=out[5], csr_equiv_bytes=out[6])
 
 
-def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None) -> Osm:
-    """Create, decompose, assemble, set alpha (both sides) and upload the density of a config dict."""
+def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None, row_order=None,
+          spmv=None) -> Osm:
+    """Create, decompose, assemble, set alpha (both sides) and upload the density of a config dict.
+    row_order / spmv optionally select the internal row order and SpMV variant (row_order=4, spmv=5:
+    the matrix-free Kuhn-stencil path)."""
     o = Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], rank, nranks, device,
             nccl_uid)
+    if row_order is not None:
+        o.set_row_order(row_order)
     o.decompose(cfg["nsub"])
     if cfg["nsub"] > 1 and alpha is None and cfg.get("robin") is not None:
         n = cfg["nsub"] - 1
@@ -483,5 +494,7 @@ def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None
             ar = np.broadcast_to(np.asarray(a[1], dtype=np.float64), (n,))
         o.set_robin(al, ar)
     o.assemble()
+    if spmv is not None:
+        o.set_spmv_variant(spmv)
     o.upload_density(drho)
     return o

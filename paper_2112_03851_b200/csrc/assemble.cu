@@ -307,4 +307,71 @@ void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract) {
   ++c.launches;
 }
 
+
+namespace {
+__global__ void k_mf_refresh(int64_t n, const int64_t* __restrict__ src, const double* __restrict__ sval,
+                             double* __restrict__ val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) val[i] = src[i] >= 0 ? sval[src[i]] : 0.0;
+}
+}  // namespace
+
+namespace {
+// Every real row's SELL entries (padding (+0.0, own row) excluded) must equal, in order and
+// bitwise, its table's entries whose target is not a dummy row (islot -2).
+__global__ void k_mf_verify(int64_t nrows, const int32_t* __restrict__ blk_sub, const MfSub* __restrict__ msub,
+                            const int32_t* __restrict__ mf_begin, const int32_t* __restrict__ mf_delta,
+                            const double* __restrict__ mf_val, const int64_t* __restrict__ soff,
+                            const int32_t* __restrict__ swidth, const double* __restrict__ sval,
+                            const int32_t* __restrict__ scol, const int32_t* __restrict__ islot,
+                            int32_t* __restrict__ bad) {
+  const int64_t ri = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ri >= nrows) return;
+  const int64_t blk = ri / kRowsPerBlock;
+  const int lane = (int)(ri % kRowsPerBlock);
+  const MfSub M = msub[blk_sub[blk]];
+  const int t = mf_table_of(M, ri - M.row0);
+  const int w = swidth[blk];
+  const int64_t base = soff[blk] + lane;
+  int e = t >= 0 ? mf_begin[t] : 0;
+  const int e1 = t >= 0 ? mf_begin[t + 1] : 0;
+  for (int k = 0; k < w; ++k) {
+    const double v = sval[base + (int64_t)kRowsPerBlock * k];
+    const int64_t cidx = scol[base + (int64_t)kRowsPerBlock * k];
+    if (cidx == ri && v == 0.0 && !signbit(v)) continue;  // SELL padding (a real diagonal is > 0)
+    while (e < e1 && (mf_val[e] == 0.0 && mf_delta[e] == 0 ? true : islot[ri + mf_delta[e]] == -2) &&
+           !(ri + mf_delta[e] == cidx && mf_val[e] == v))
+      ++e;  // table padding, or an entry into a dummy row (multiplies an exact zero)
+    if (e >= e1 || ri + mf_delta[e] != cidx ||
+        __double_as_longlong(mf_val[e]) != __double_as_longlong(v)) {
+      atomicOr(bad, 1);
+      return;
+    }
+    ++e;
+  }
+  for (; e < e1; ++e)  // leftovers must be padding or point into dummy rows
+    if (!(mf_val[e] == 0.0 && mf_delta[e] == 0) && islot[ri + mf_delta[e]] != -2) {
+      atomicOr(bad, 1);
+      return;
+    }
+}
+}  // namespace
+
+void launch_mf_verify(const Ctx& c, int32_t* d_bad) {
+  if (!c.mf_ok) return;
+  k_mf_verify<<<(unsigned)ceil_div(c.nrows_total, 256), 256, 0, c.stream>>>(
+      c.nrows_total, c.blk_sub, c.d_mf_sub, c.d_mf_begin, c.d_mf_delta, c.d_mf_val, c.sell_soff, c.sell_swidth,
+      c.sell_val, c.sell_col, c.islot, d_bad);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+}
+
+void launch_mf_refresh(const Ctx& c) {
+  if (!c.mf_ok || c.mf_entries == 0) return;
+  k_mf_refresh<<<(unsigned)ceil_div(c.mf_entries, 256), 256, 0, c.stream>>>(c.mf_entries, c.d_mf_src, c.sell_val,
+                                                                           c.d_mf_val);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+}
+
 }  // namespace osm

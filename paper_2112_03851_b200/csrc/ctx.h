@@ -36,6 +36,83 @@ struct StencilDev {
 // row l sits at toff[t] + 256 j + l (column major over the tile), so entries
 // [j0, j1) of the whole tile are one contiguous range (bulk-copy friendly);
 // padding entries have val 0, col = own row.
+// Matrix-free Kuhn-stencil view of one local subdomain (SpMV variant 5, row order 4).
+// Internal layout: the slab's whole lattice box [o c0, o c1] x [0, Ny) x [0, Nz), split into the
+// o^3 parity classes c = rx + o (ry + o rz); class c is the sub-lattice (ii, jj, kk) -> point
+// (o ii + rx, o jj + ry, o kk + rz), stored at internal local index c hIJK + jj + hJ (kk + hK ii)
+// (y fastest, x slowest).  Dirichlet and out-of-box points are inert dummy rows (zero vectors), so
+// a row's neighbour through stencil entry e sits at a constant offset delta_e for every row of
+// its (kind, class): no column indices and no boundary masks.
+struct MfSub {
+  int64_t row0;       // first internal row of the subdomain
+  int32_t hJ, hK;     // sub-lattice extents in y, z
+  int32_t hJK, hIJK;  // hJ hK, hI hJ hK
+  int32_t nIs;        // lattice points of the slab in x (o (c1 - c0) + 1)
+  int32_t Ny, Nz;     // lattice points in y, z
+  int32_t dir_lo;     // 1: the slab's x = first plane is the Dirichlet boundary (first slab)
+  int32_t dir_hi;     // 1: the slab's last plane is the Dirichlet boundary (last slab)
+  int32_t tab0;       // table index of (kind 0, class 0); table t = tab0 + kind nclass + c
+  int32_t o, nclass;
+  double inv_hIJK, inv_hJK, inv_hJ;  // reciprocals for the row decode (exact-corrected division)
+};
+
+// n / d for 0 <= n < 2^31 via a double reciprocal and one correction step (the quotient estimate is
+// within 1 of the truth): ~6 instructions instead of a ~25-instruction integer division.
+__device__ __forceinline__ int mf_div(int n, int d, double inv, int& r) {
+  int q = (int)((double)n * inv);
+  r = n - q * d;
+  if (r < 0) {
+    --q;
+    r += d;
+  } else if (r >= d) {
+    ++q;
+    r -= d;
+  }
+  return q;
+}
+
+// Table of internal local row li of a subdomain (-1: dummy row), see MfSub.
+__device__ __forceinline__ int mf_table_of(const MfSub& M, int64_t li) {
+  if (li >= (int64_t)M.nclass * M.hIJK) return -1;
+  int rem, r2, jj;
+  const int cl = mf_div((int)li, M.hIJK, M.inv_hIJK, rem);
+  const int ii = mf_div(rem, M.hJK, M.inv_hJK, r2);
+  const int kk = mf_div(r2, M.hJ, M.inv_hJ, jj);
+  int rx = 0, ry = 0, rz = 0, o = 1;
+  if (M.o == 2) {
+    rx = cl & 1;
+    ry = (cl >> 1) & 1;
+    rz = cl >> 2;
+    o = 2;
+  }
+  const int I = o * ii + rx, J = o * jj + ry, K = o * kk + rz;
+  if (I >= M.nIs || J < 1 || J > M.Ny - 2 || K < 1 || K > M.Nz - 2 || (M.dir_lo && I == 0) ||
+      (M.dir_hi && I == M.nIs - 1))
+    return -1;
+  const int kind = I == 0 ? 1 : (I == M.nIs - 1 ? 2 : 0);
+  return M.tab0 + kind * M.nclass + cl;
+}
+
+// The matrix-free tables as a kernel parameter (constant bank): table values and offsets are
+// read through the constant cache (uniform broadcast), not the L1/TEX load path, which the x
+// gathers need.  Tables are deduplicated across subdomains; used when they fit.
+constexpr int kMfMaxSub = 16, kMfMaxTab = 128, kMfMaxGroups = 560;
+struct MfConst {
+  int32_t valid;
+  int16_t tabid[kMfMaxSub * 3 * 8];  // (local subdomain, kind, class) -> deduplicated table
+  int32_t gbeg[kMfMaxTab + 1];       // group range [gbeg[t], gbeg[t+1]) of a table
+  int4 delta[kMfMaxGroups];
+  double val[4 * kMfMaxGroups];
+};
+template <int V>
+struct MfArg {
+  int32_t unused;
+};
+template <>
+struct MfArg<5> {
+  MfConst c;
+};
+
 struct SellDev {
   const double* val;
   const int32_t* col;
@@ -45,6 +122,12 @@ struct SellDev {
   const int64_t* poff;     //   4 entries of a row per uint4 (see vi.cu); per-tile word offsets
   const double* dict;      // distinct values
   int ndict;
+  // matrix-free view (variant 5): kinds 0 interior, 1 left interface plane, 2 right interface plane
+  const int32_t* blk_sub;   // block -> local subdomain
+  const MfSub* mf_sub;      // per local subdomain
+  const int32_t* mf_begin;  // table t = entries [mf_begin[t], mf_begin[t+1]), padded to a multiple of 4
+  const int4* mf_delta;     // 4 row offsets per group
+  const double* mf_val;     // values (exact copies of the assembled, Robin-folded SELL entries)
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -193,7 +276,7 @@ struct Ctx {
   int64_t side_nblk = 0;
   SubState* st = nullptr;       // per local subdomain
   int32_t* d_nactive = nullptr;
-  int32_t* d_flags = nullptr;   // [0] precond failure, [1] fold miss
+  int32_t* d_flags = nullptr;   // [0] precond failure, [1] fold miss, [2] vi offset overflow, [3] mf mismatch
   // host staging (pinned)
   int32_t* h_nactive = nullptr;  // 2 slots
   SubState* h_st = nullptr;
@@ -216,11 +299,24 @@ struct Ctx {
   bool force_remote = false;  // debug: every side goes through NCCL (peer = own rank), see osm_create
   int update_variant = 0;  // 0: k_cg_update at 96 regs, 1: capped for 8 blocks/SM
   int sort_key = 3;  // SELL row order inside sigma windows: 0 length desc, 1 parity class, 2 class then length,
-                    // 3 class, length, then (K, I, J) with J fastest (default)
+                    // 3 class, length, then (K, I, J) with J fastest (default); 4: the matrix-free
+                    // class-major lattice layout of MfSub (whole subdomain, dummy rows included)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
   int spmv_variant = 4;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
                          // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary
-                         // in shared memory (default; falls back to 3, then 2, when it does not apply)
+                         // in shared memory (default; falls back to 3, then 2, when it does not apply),
+                         // 5: matrix-free Kuhn stencil (row order 4 only; else as 4)
+
+  // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
+  bool mf_ok = false;
+  MfSub* d_mf_sub = nullptr;
+  int32_t* d_mf_begin = nullptr;
+  int32_t* d_mf_delta = nullptr;  // int4 groups
+  double* d_mf_val = nullptr;
+  int64_t* d_mf_src = nullptr;    // SELL position of each table value (-1: padding)
+  int64_t mf_entries = 0;         // including padding
+  std::vector<int32_t> h_mf_begin, h_mf_delta;
+  MfConst* h_mf_const = nullptr;  // host copy of the kernel-parameter tables (valid = 0: global tables)
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;
@@ -262,6 +358,8 @@ void launch_load(const Ctx& c, const Sub& s, double fourpiG);
 void launch_load_free(const Ctx& c, const Sub& s, const double* d_bfree);
 void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned);
 void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract);
+void launch_mf_refresh(const Ctx& c);  // matrix-free table values <- assembled (folded) SELL values
+void launch_mf_verify(const Ctx& c, int32_t* d_bad);  // every row of every subdomain vs its table
 
 // ---- launchers (schwarz_kernels.cu)
 void launch_warm(Ctx& c, double tol, int warm);

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <string>
 #include <tuple>
@@ -153,6 +154,15 @@ static void free_assembly(Ctx& c) {
   dfree(c.side_cnt);
   dfree(c.st);
   dfree(c.phi);
+  dfree(c.d_mf_sub);
+  dfree(c.d_mf_begin);
+  dfree(c.d_mf_delta);
+  dfree(c.d_mf_val);
+  dfree(c.d_mf_src);
+  c.mf_ok = false;
+  c.mf_entries = 0;
+  delete c.h_mf_const;
+  c.h_mf_const = nullptr;
   c.assembled = false;
   c.density_set = false;
 }
@@ -179,6 +189,146 @@ static SlabGeom slab_geom(const Ctx& c, int s) {
 }
 
 
+// Copy the table values from the (folded) SELL and verify the tables against every row.
+static void mf_refresh(Ctx& c) {
+  launch_mf_refresh(c);
+  OSM_CUDA(cudaMemsetAsync(c.d_flags + 3, 0, sizeof(int32_t), c.stream));
+  launch_mf_verify(c, c.d_flags + 3);
+  int32_t bad = 0;
+  OSM_CUDA(cudaMemcpyAsync(&bad, c.d_flags + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  drop_graph(c);  // captured launches embed the kernel-parameter tables
+  if (bad) {
+    c.mf_ok = false;
+    return;
+  }
+  // deduplicated kernel-parameter copy of the tables
+  if (!c.h_mf_const) c.h_mf_const = new MfConst();
+  MfConst& P = *c.h_mf_const;
+  std::memset(&P, 0, sizeof(MfConst));
+  const int ntab = (int)c.h_mf_begin.size() - 1;
+  const int nloc = c.s_end - c.s_begin, ncls = c.mesh.order * c.mesh.order * c.mesh.order;
+  if (nloc > kMfMaxSub || ncls > 8) return;
+  std::vector<double> val(c.mf_entries);
+  OSM_CUDA(cudaMemcpy(val.data(), c.d_mf_val, sizeof(double) * c.mf_entries, cudaMemcpyDeviceToHost));
+  std::map<std::vector<int64_t>, int> seen;
+  int ng = 0, nt = 0;
+  P.gbeg[0] = 0;
+  for (int t = 0; t < ntab; ++t) {
+    std::vector<int64_t> key;
+    for (int e = c.h_mf_begin[t]; e < c.h_mf_begin[t + 1]; ++e) {
+      int64_t bits;
+      std::memcpy(&bits, &val[e], sizeof(bits));
+      key.push_back(c.h_mf_delta[e]);
+      key.push_back(bits);
+    }
+    auto it = seen.find(key);
+    if (it == seen.end()) {
+      const int g = (c.h_mf_begin[t + 1] - c.h_mf_begin[t]) / 4;
+      if (nt >= kMfMaxTab || ng + g > kMfMaxGroups) return;  // too many: global tables
+      for (int e = c.h_mf_begin[t], k = 4 * ng; e < c.h_mf_begin[t + 1]; ++e, ++k) {
+        (&P.delta[0].x)[k] = c.h_mf_delta[e];
+        P.val[k] = val[e];
+      }
+      ng += g;
+      it = seen.emplace(key, nt).first;
+      P.gbeg[++nt] = ng;
+    }
+    P.tabid[t] = (int16_t)it->second;  // t = (ls * 3 + kind) * ncls + class, as mf_table_of
+  }
+  P.valid = 1;
+}
+
+// Matrix-free Kuhn-stencil tables (SpMV variant 5, row order 4).  For every
+// local subdomain, row kind (0 interior, 1 left interface plane, 2 right interface plane) and
+// parity class, the longest row of that kind and class is the representative: its CSR columns,
+// as lattice offsets, become constant internal offsets (the layout makes them row-independent)
+// and its SELL positions the value sources (k_mf_refresh copies the assembled, Robin-folded
+// values bitwise).  k_mf_verify then checks every row of the subdomain against its table
+// (same entries in the same order, same bits, table entries into dummy rows aside); on any
+// mismatch (e.g. slabs too thin for a complete representative) mf_ok drops to false and
+// variant 5 falls back to the SELL variants.
+static void mf_build(Ctx& c, const std::vector<std::vector<int32_t>>& h_iperm,
+                     const std::vector<std::vector<int32_t>>& h_len, const std::vector<int64_t>& h_soff) {
+  c.mf_ok = false;
+  const int o = c.mesh.order, ncls = o * o * o;
+  const int nloc = c.s_end - c.s_begin;
+  std::vector<MfSub> msub(nloc);
+  std::vector<int32_t> begin(1, 0), delta;
+  std::vector<int64_t> src;
+  for (int ls = 0; ls < nloc; ++ls) {
+    const Sub& S = c.subs[ls];
+    MfSub& M = msub[ls];
+    const int64_t nIs = (int64_t)o * (S.g.c1 - S.g.c0) + 1;
+    const int64_t hI = (nIs + o - 1) / o, hJ = (S.g.Ny + o - 1) / o, hK = (S.g.Nz + o - 1) / o;
+    M.row0 = S.row0;
+    M.hJ = (int32_t)hJ;
+    M.hK = (int32_t)hK;
+    M.hJK = (int32_t)(hJ * hK);
+    M.hIJK = (int32_t)(hI * hJ * hK);
+    M.nIs = (int32_t)nIs;
+    M.Ny = (int32_t)S.g.Ny;
+    M.Nz = (int32_t)S.g.Nz;
+    M.dir_lo = S.g.c0 == 0;
+    M.dir_hi = S.g.c1 == c.mesh.nx;
+    M.tab0 = ls * 3 * ncls;
+    M.o = o;
+    M.nclass = ncls;
+    M.inv_hIJK = 1.0 / (double)M.hIJK;
+    M.inv_hJK = 1.0 / (double)M.hJK;
+    M.inv_hJ = 1.0 / (double)M.hJ;
+    auto internal_of = [&](int64_t Il, int64_t J, int64_t K) {  // slab-local lattice point (>= 0) -> internal
+      const int64_t cl = Il % o + o * (J % o + o * (K % o));
+      return cl * M.hIJK + J / o + hJ * (K / o + hK * (Il / o));
+    };
+    std::vector<int64_t> rep(3 * ncls, -1);
+    const auto& len = h_len[ls];
+    for (int64_t lc = 0; lc < S.n; ++lc) {
+      const int64_t Ig = S.g.I_lo + lc % S.g.nI, t = lc / S.g.nI, J = 1 + t % S.g.nJ, K = 1 + t / S.g.nJ;
+      const int64_t Il = Ig - (int64_t)o * S.g.c0;
+      const int kind = Il == 0 ? 1 : (Il == nIs - 1 ? 2 : 0);
+      const int t2 = kind * ncls + (int)(Il % o + o * (J % o + o * (K % o)));
+      if (rep[t2] < 0 || len[lc] > len[rep[t2]]) rep[t2] = lc;
+    }
+    std::vector<int64_t> rowptr(S.n + 1, 0);
+    for (int64_t i = 0; i < S.n; ++i) rowptr[i + 1] = rowptr[i] + len[i];
+    for (int t2 = 0; t2 < 3 * ncls; ++t2) {
+      if (rep[t2] >= 0) {
+        const int64_t lc = rep[t2], nl = len[lc];
+        std::vector<int32_t> cols(nl);
+        OSM_CUDA(cudaMemcpy(cols.data(), S.col + rowptr[lc], sizeof(int32_t) * nl, cudaMemcpyDeviceToHost));
+        const int64_t I0 = S.g.I_lo + lc % S.g.nI, t0 = lc / S.g.nI, J0 = 1 + t0 % S.g.nJ, K0 = 1 + t0 / S.g.nJ;
+        const int64_t Il0 = I0 - (int64_t)o * S.g.c0;
+        // base point of the same class with coordinates >= 2: offsets of the affine class layout
+        const int64_t bI = 2 * o + Il0 % o, bJ = 2 * o + J0 % o, bK = 2 * o + K0 % o;
+        const int64_t gr = S.row0 + h_iperm[ls][lc], tile = gr / kRowsPerBlock, lane = gr % kRowsPerBlock;
+        for (int64_t j = 0; j < nl; ++j) {
+          const int64_t cc = cols[j];
+          const int64_t I = S.g.I_lo + cc % S.g.nI, t = cc / S.g.nI, J = 1 + t % S.g.nJ, K = 1 + t / S.g.nJ;
+          const int64_t d = internal_of(bI + (I - I0), bJ + (J - J0), bK + (K - K0)) - internal_of(bI, bJ, bK);
+          delta.push_back((int32_t)d);
+          src.push_back(h_soff[tile] + (int64_t)kRowsPerBlock * j + lane);
+        }
+        while (delta.size() % 4) {  // pad the table to whole groups of 4 with (0, +0.0)
+          delta.push_back(0);
+          src.push_back(-1);
+        }
+      }
+      begin.push_back((int32_t)delta.size());
+    }
+  }
+  c.mf_entries = (int64_t)delta.size();
+  c.h_mf_begin = begin;
+  c.h_mf_delta = delta;
+  c.d_mf_sub = dupload(c, msub);
+  c.d_mf_begin = dupload(c, begin);
+  c.d_mf_delta = dupload(c, delta);
+  c.d_mf_src = dupload(c, src);
+  c.d_mf_val = dalloc<double>(std::max<int64_t>(4, c.mf_entries));
+  c.mf_ok = true;
+  mf_refresh(c);
+}
+
 static void assemble(Ctx& c) {
   free_assembly(c);
   const int o = c.mesh.order;
@@ -203,6 +353,7 @@ static void assemble(Ctx& c) {
   c.subs.resize(nloc);
   std::vector<std::vector<int32_t>> h_perm(nloc);
   std::vector<std::vector<int32_t>> h_iperm(nloc);
+  std::vector<std::vector<int32_t>> h_len(nloc);
   std::vector<int64_t> h_soff;
   std::vector<int32_t> h_swidth;
   int64_t row0 = 0, slice0 = 0, sell_off = 0;
@@ -227,7 +378,13 @@ static void assemble(Ctx& c) {
     launch_fill(c, S);
 
     // SELL-32-sigma: within windows of kSigma rows, sort rows by length (descending, stable)
-    S.npad = round_up(S.n, kRowsPerBlock);
+    const bool mf_layout = c.sort_key == 4;
+    const int64_t mf_nIs = (int64_t)o * (S.g.c1 - S.g.c0) + 1;
+    const int64_t mf_hI = (mf_nIs + o - 1) / o, mf_hJ = (S.g.Ny + o - 1) / o, mf_hK = (S.g.Nz + o - 1) / o;
+    const int64_t mf_rows = (int64_t)o * o * o * mf_hI * mf_hJ * mf_hK;
+    S.npad = round_up(mf_layout ? mf_rows : S.n, kRowsPerBlock);
+    if (S.npad >= (int64_t)INT32_MAX) fail(OSM_ERR_INVALID_ARG, "subdomain too large for int32 local indices");
+    h_len[ls] = len;
     S.row0 = row0;
     S.slice0 = slice0;
     S.nslice = S.npad / kWarp;
@@ -249,7 +406,20 @@ static void assemble(Ctx& c) {
       if (sigma + reach > 32767) sigma = 32768;
     }
     sigma = std::max<int64_t>(kRowsPerBlock, sigma);
-    for (int64_t w0 = 0; w0 < S.n; w0 += sigma) {
+    if (mf_layout) {  // class-major lattice layout of MfSub (dummy rows: perm -1)
+      const int64_t hJK = mf_hJ * mf_hK, hIJK = mf_hI * hJK;
+      for (int64_t li = 0; li < mf_rows; ++li) {
+        const int64_t cc = li / hIJK, rem = li % hIJK, ii = rem / hJK, kk = (rem % hJK) / mf_hJ, jj = rem % mf_hJ;
+        const int64_t I = o * ii + cc % o, J = o * jj + (cc / o) % o, K = o * kk + cc / (o * o);
+        const int64_t Ig = (int64_t)o * S.g.c0 + I;
+        if (I >= mf_nIs || Ig < S.g.I_lo || Ig > S.g.I_hi || J < 1 || J > S.g.Ny - 2 || K < 1 || K > S.g.Nz - 2)
+          continue;
+        const int64_t lc = (Ig - S.g.I_lo) + S.g.nI * ((J - 1) + S.g.nJ * (K - 1));
+        perm[li] = (int32_t)lc;
+        iperm[lc] = (int32_t)li;
+      }
+    }
+    for (int64_t w0 = 0; w0 < (mf_layout ? 0 : S.n); w0 += sigma) {
       const int64_t w1 = std::min<int64_t>(S.n, w0 + sigma);
       idx.resize(w1 - w0);
       std::iota(idx.begin(), idx.end(), (int32_t)w0);
@@ -333,7 +503,8 @@ static void assemble(Ctx& c) {
   std::vector<int32_t> islot(c.nrows_total, -1);
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
-    for (int64_t k = S.n; k < S.npad; ++k) islot[S.row0 + k] = -2;
+    for (int64_t k = 0; k < S.npad; ++k)
+      if (h_perm[ls][k] < 0) islot[S.row0 + k] = -2;
   }
   {
     int sb, se;
@@ -399,6 +570,7 @@ static void assemble(Ctx& c) {
     launch_fold_build(c, c.sides[k], c.subs[c.sides[k].sub]);
   }
   vi_build(c);  // value-indexed hot copy (from the unfolded K^N values)
+  if (c.sort_key == 4) mf_build(c, h_iperm, h_len, h_soff);
 
   // --- reductions and device side table
   c.part = dalloc<double>(3 * c.nblk_total);
@@ -478,6 +650,7 @@ static void apply_robin(Ctx& c) {
   double* d_q = dupload(c, qv);
   OSM_CUDA(cudaMemsetAsync(c.d_flags, 0, 4 * sizeof(int32_t), c.stream));
   launch_fold_apply(c, d_a, d_q);
+  if (c.mf_ok) mf_refresh(c);
   OSM_CUDA(cudaMemcpyAsync(c.d_sides, c.h_sides.data(), sizeof(SideDev) * nsides, cudaMemcpyHostToDevice, c.stream));
   int32_t flags[4];
   OSM_CUDA(cudaMemcpyAsync(flags, c.d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c.stream));
@@ -1288,10 +1461,20 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 4) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..4");
+  if (v < 0 || v > 5) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..5");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);
+  return OSM_OK;
+  OSM_API_END
+}
+
+osm_status osm_set_row_order(osm_ctx* h, int order) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (order < 0 || order > 4) fail(OSM_ERR_INVALID_ARG, "row order must be 0..4");
+  if (c.assembled) fail(OSM_ERR_STATE, "osm_set_row_order must precede osm_assemble");
+  c.sort_key = order;
   return OSM_OK;
   OSM_API_END
 }

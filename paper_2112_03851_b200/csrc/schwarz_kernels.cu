@@ -308,14 +308,57 @@ __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk
   return s;
 }
 
+// Variant 5: matrix-free Kuhn stencil (row order 4, see MfSub).  The row's lattice point, kind
+// and parity class follow from its internal index; its table lists (row offset, value) in column
+// order, 4 per group, so the sum is the same FMA chain as the SELL variants (bitwise-identical
+// iterations).  Table loads are warp-uniform (one broadcast per group); the x gathers of a warp
+// are 32 consecutive rows shifted by one offset: coalesced, with no column indices read.
+__device__ __forceinline__ double tile_row_mf(const SellDev& A, int64_t blk, const double* __restrict__ x,
+                                              const MfConst& P) {
+  const int ls = A.blk_sub[blk];
+  const MfSub& M = A.mf_sub[ls];
+  const int64_t ri = blk * kRowsPerBlock + threadIdx.x;
+  double s = 0.0;
+  const int t = mf_table_of(M, ri - M.row0);
+  if (t < 0) return s;  // dummy row (Dirichlet or padding point): like a SELL padding row
+  const double* xr = x + ri;
+  asm("" : "+l"(xr));  // keep the row pointer opaque: each gather is then one wide IMAD off it
+  if (P.valid) {  // tables in the constant bank
+    const int tb = P.tabid[t];
+#pragma unroll 2
+    for (int g = P.gbeg[tb]; g < P.gbeg[tb + 1]; ++g) {
+      const int4 d = P.delta[g];
+      const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
+      s = fma(P.val[4 * g], x0, s);
+      s = fma(P.val[4 * g + 1], x1, s);
+      s = fma(P.val[4 * g + 2], x2, s);
+      s = fma(P.val[4 * g + 3], x3, s);
+    }
+    return s;
+  }
+  const int g0 = A.mf_begin[t] >> 2, g1 = A.mf_begin[t + 1] >> 2;
+  const double2* vv = reinterpret_cast<const double2*>(A.mf_val);
+  for (int g = g0; g < g1; ++g) {
+    const int4 d = A.mf_delta[g];
+    const double2 v01 = vv[2 * g], v23 = vv[2 * g + 1];
+    const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
+    s = fma(v01.x, x0, s);
+    s = fma(v01.y, x1, s);
+    s = fma(v23.x, x2, s);
+    s = fma(v23.y, x3, s);
+  }
+  return s;
+}
+
 // V = 0: LDG rows; V = 2: LDG rows with registers capped at 32 (8 blocks / 64 warps per SM);
 // V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers);
-// V = 4: value-indexed rows, dictionary in shared memory.
+// V = 4: value-indexed rows, dictionary in shared memory; V = 5: matrix-free Kuhn stencil.
 template <int V>
 __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                           unsigned char* smem) {
+                                           unsigned char* smem, const MfArg<V>& mf) {
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
+  if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c);
   if constexpr (V == 4) {
     double* sd = reinterpret_cast<double*>(smem);
     for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];
@@ -333,7 +376,8 @@ template <int V>
 __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restrict__ blk_sub,
                                                       SubState* __restrict__ st, const double* __restrict__ p,
                                                       double* __restrict__ q, double* __restrict__ part,
-                                                      int64_t stride, int32_t* __restrict__ nactive) {
+                                                      int64_t stride, int32_t* __restrict__ nactive,
+                                                      const __grid_constant__ MfArg<V> mf) {
   constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
   __shared__ double sm[NW * 1];
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -343,7 +387,7 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
   if (!st[ls].active) return;
   const bool has_row = threadIdx.x < kRowsPerBlock;
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double y = tile_row<V>(A, blk, p, dsm);
+  const double y = tile_row<V>(A, blk, p, dsm, mf);
   double v[1] = {0.0};
   if (has_row) {
     q[row] = y;
@@ -483,14 +527,14 @@ __global__ void OSM_SPMV_BOUNDS(V) k_warm(SellDev A, const int32_t* __restrict__
                                                    const double* __restrict__ lam_all, const double* __restrict__ dinv,
                                                    double* __restrict__ r, double* __restrict__ p,
                                                    double* __restrict__ part, int64_t stride, double tol,
-                                                   int32_t* __restrict__ nactive) {
+                                                   int32_t* __restrict__ nactive, const __grid_constant__ MfArg<V> mf) {
   constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
   __shared__ double sm[NW * 3];
   extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double ax = tile_row<V>(A, blk, x, dsm);
+  const double ax = tile_row<V>(A, blk, x, dsm, mf);
   double v[3] = {0.0, 0.0, 0.0};
   if (threadIdx.x < kRowsPerBlock) {
     const int sl = islot[row];
@@ -583,14 +627,14 @@ __global__ void OSM_SPMV_BOUNDS(V) k_resid(SellDev A, const int32_t* __restrict_
                                                     SubState* __restrict__ st, const double* __restrict__ ut,
                                                     const double* __restrict__ b, const int32_t* __restrict__ islot,
                                                     double* __restrict__ wif_all, double* __restrict__ part,
-                                                    int64_t stride) {
+                                                    int64_t stride, const __grid_constant__ MfArg<V> mf) {
   constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
   __shared__ double sm[NW * 1];
   extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double ax = tile_row<V>(A, blk, ut, dsm);
+  const double ax = tile_row<V>(A, blk, ut, dsm, mf);
   double v[1] = {0.0};
   if (threadIdx.x < kRowsPerBlock) {
     const double w = b[row] - ax;
@@ -651,14 +695,18 @@ __global__ void __launch_bounds__(kThreads) k_iface_sum(const SideDev* __restric
 }
 
 SellDev sell_of(const Ctx& c) {
-  return SellDev{c.sell_val, c.sell_col, c.sell_soff, c.sell_swidth, c.vi_packed, c.vi_poff, c.vi_dict,
-                 (int)c.vi_ndict};
+  return SellDev{c.sell_val,  c.sell_col,   c.sell_soff,  c.sell_swidth,
+                 c.vi_packed, c.vi_poff,     c.vi_dict,    (int)c.vi_ndict,
+                 c.blk_sub,   c.d_mf_sub,    c.d_mf_begin, reinterpret_cast<const int4*>(c.d_mf_delta),
+                 c.d_mf_val};
 }
 
 }  // namespace
 
 int spmv_variant_of(const Ctx& c) {
+  if (c.spmv_variant == 5 && c.mf_ok) return 5;
   if (c.spmv_variant >= 3 && !c.vi_ok) return 2;
+  if (c.spmv_variant == 5) return c.vi_ndict > kSmemDict ? 3 : 4;
   if (c.spmv_variant == 4 && c.vi_ndict > kSmemDict) return 3;
   return c.spmv_variant;
 }
@@ -678,11 +726,20 @@ void spmv_init_attributes() {
 }
 
 template <int V>
+static MfArg<V> mf_arg(const Ctx& c) {
+  MfArg<V> a{};
+  if constexpr (V == 5) {
+    if (c.h_mf_const) a.c = *c.h_mf_const;
+  }
+  return a;
+}
+
+template <int V>
 static void warm_v(Ctx& c, double tol) {
   const unsigned thr = V == 1 ? kBulkThreads : kThreads;
   k_warm<V><<<(unsigned)c.nblk_total, thr, spmv_smem(c), c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
                                                                       c.lam_all, c.dinv, c.r, c.p, c.part,
-                                                                      c.nblk_total, tol, c.d_nactive);
+                                                                      c.nblk_total, tol, c.d_nactive, mf_arg<V>(c));
 }
 
 void launch_warm(Ctx& c, double tol, int) {
@@ -692,6 +749,7 @@ void launch_warm(Ctx& c, double tol, int) {
     case 1: warm_v<1>(c, tol); break;
     case 2: warm_v<2>(c, tol); break;
     case 3: warm_v<3>(c, tol); break;
+    case 5: warm_v<5>(c, tol); break;
     default: warm_v<4>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
@@ -725,7 +783,7 @@ template <int V>
 static void cg_spmv_v(Ctx& c) {
   launch_pdl(c, k_cg_spmv<V>, (unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
              sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
-             c.part, c.nblk_total, c.d_nactive);
+             c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c));
 }
 
 void launch_cg_spmv(Ctx& c) {
@@ -735,6 +793,7 @@ void launch_cg_spmv(Ctx& c) {
     case 1: cg_spmv_v<1>(c); break;
     case 2: cg_spmv_v<2>(c); break;
     case 3: cg_spmv_v<3>(c); break;
+    case 5: cg_spmv_v<5>(c); break;
     default: cg_spmv_v<4>(c); break;
   }
   ++c.launches;
@@ -790,7 +849,7 @@ void launch_glue(Ctx& c, int zero) {
 template <int V>
 static void resid_v(Ctx& c) {
   k_resid<V><<<(unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, spmv_smem(c), c.stream>>>(
-      sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot, c.wif_all, c.part, c.nblk_total);
+      sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot, c.wif_all, c.part, c.nblk_total, mf_arg<V>(c));
 }
 
 void launch_resid(Ctx& c) {
@@ -800,6 +859,7 @@ void launch_resid(Ctx& c) {
     case 1: resid_v<1>(c); break;
     case 2: resid_v<2>(c); break;
     case 3: resid_v<3>(c); break;
+    case 5: resid_v<5>(c); break;
     default: resid_v<4>(c); break;
   }
   OSM_CHECK_LAUNCH();

@@ -280,7 +280,7 @@ def main():
     step()
     kt2 = osm.kernel_timing()
     tm2 = osm.traffic_model()
-    default_variant = osm.set_spmv_variant(4)
+    default_variant = osm.set_spmv_variant(HOT_VARIANT)
     osm.set_kernel_timing(False)
     peak, peak_src = hbm_peak()
     spmv_launches, spmv_ms = kt["cg_spmv"]
@@ -304,9 +304,16 @@ def main():
                 "kernel_ms": {k: v[1] for k, v in kt.items()}, "kernel_launches": {k: v[0] for k, v in kt.items()},
                 "us_per_launch": 1e3 * spmv_ms / max(1, spmv_launches),
                 "format": "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
-                          "offset) + 16 B per row (p, q); dictionary in shared memory",
+                          "offset) + 16 B per row (p, q); dictionary in the constant bank (kernel parameter)",
                 "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
-                "limiter": "L1/TEX throughput (ncu: l1tex 79% of peak, dram 37%; profiles/r01c_ncu_cg_raw.csv)"}
+                "limiter": "L1/TEX gather path and issue, not HBM (ncu: l1tex 59% of peak, issue 51%, dram 48%; "
+                           "profiles/r01g_ncu_summary.md)"}
+
+    # SURVEY 8(f) NEXT-4, reported separately: the matrix-free Kuhn-stencil SpMV (variant 5, row
+    # order 4) on the same workload, timed the same way (it deviates from the paper's CSR)
+    matrix_free = None
+    if world == 1:
+        matrix_free = run_matrix_free(P, args, cfg, d_drho, stream, peak, torch)
 
     # e2e through the C ABI with host buffers: pinned drho H2D + solve + Phi D2H, every step
     h_drho = torch.from_numpy(drho).pin_memory()
@@ -349,7 +356,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
-            "roofline": roofline, "roofline_fp64_sell": roofline_fp64, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "roofline": roofline, "roofline_fp64_sell": roofline_fp64, "matrix_free": matrix_free,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)
     osm.close()
@@ -358,6 +366,57 @@ def main():
 
 
 _rows = {}
+HOT_VARIANT = 6  # library default SpMV: value-indexed SELL-256, dictionary in the constant bank
+
+
+def run_matrix_free(P, args, cfg, d_drho, stream, peak, torch):
+    """Time the matrix-free SpMV path (variant 5 in row order 4) on the headline workload: K timed
+    steps after W warm-ups (CUDA events on the library stream), then one instrumented solve for the
+    per-launch SpMV time.  Its algorithmic SpMV bytes are only p (read) and q (written): 16 B/row."""
+    S = cfg["nsub"]
+    mf = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"],
+               stream=stream.cuda_stream)
+    mf.set_row_order(4)
+    mf.decompose(S)
+    mf.set_robin2(*synth.robin(cfg))
+    mf.assemble()
+    active = mf.set_spmv_variant(5)
+
+    def step():
+        mf.upload_density_device(d_drho.data_ptr())
+        return mf.solve(tol_outer=1e-8, max_outer=1000)
+
+    for _ in range(args.warmup):
+        st, rep = step()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    work, outer = 0.0, 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st, rep = step()
+        work += local_cg_work(mf, S, 0, 1)
+        outer += rep.outer_iters
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    mf.set_kernel_timing(True)
+    step()
+    kt = mf.kernel_timing()
+    tm = mf.traffic_model()
+    mf.set_kernel_timing(False)
+    mf.close()
+    n, t = kt["cg_spmv"]
+    gbs = tm["spmv_bytes"] / (t / 1e3) / 1e9 if t > 0 else None
+    return {"variant": active, "row_order": 4, "status": int(st), "value": work / (ms / 1e3), "unit": UNIT,
+            "time_to_tol_s": ms / args.steps / 1e3, "outer_iters": outer / args.steps,
+            "spmv_us_per_launch": 1e3 * t / max(1, n),
+            "spmv_share_of_cg_time": t / sum(kt[k][1] for k in ("cg_spmv", "cg_update", "cg_dir")),
+            "roofline": {"bound": "l1/issue", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak if gbs else None,
+                         "note": "algorithmic bytes = 16 B/row (p read, q write): no matrix bytes, so the "
+                                 "kernel is bound by the L1 gather path and instruction issue, not HBM"},
+            "csr_equivalent_gbs": tm["csr_equiv_bytes"] / (t / 1e3) / 1e9 if t > 0 else None,
+            "cg_kernels_us": {k: 1e3 * v[1] / max(1, v[0]) for k, v in kt.items()}}
 
 
 def local_cg_work(osm, S, rank, world):

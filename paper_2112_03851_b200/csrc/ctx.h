@@ -112,6 +112,13 @@ template <>
 struct MfArg<5> {
   MfConst c;
 };
+// Variant 6: the value-indexed dictionary in the constant bank (kernel parameter) instead of
+// shared memory (variant 4).
+constexpr int kCDict = 2048;
+template <>
+struct MfArg<6> {
+  double dict[kCDict];
+};
 
 struct SellDev {
   const double* val;
@@ -302,10 +309,11 @@ struct Ctx {
                     // 3 class, length, then (K, I, J) with J fastest (default); 4: the matrix-free
                     // class-major lattice layout of MfSub (whole subdomain, dummy rows included)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
-  int spmv_variant = 4;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
+  int spmv_variant = 6;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
                          // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary
                          // in shared memory (default; falls back to 3, then 2, when it does not apply),
-                         // 5: matrix-free Kuhn stencil (row order 4 only; else as 4)
+                         // 5: matrix-free Kuhn stencil (row order 4 only; else as 4), 6: 3 with the
+                         // dictionary in the constant bank (default; else 3)
 
   // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
   bool mf_ok = false;
@@ -333,6 +341,7 @@ struct Ctx {
     double kn, m, s;
   };
   std::vector<FoldTuple> vi_fold_tuples;
+  std::vector<double> h_vi_dict;  // host copy of the dictionary (variant 6 kernel parameter)
 
   // instrumentation
   bool timing = false;

@@ -189,6 +189,14 @@ static SlabGeom slab_geom(const Ctx& c, int s) {
 }
 
 
+// Host copy of the value-indexed dictionary (the variant 6 kernel parameter); captured graphs embed it.
+static void vi_sync_host_dict(Ctx& c) {
+  c.h_vi_dict.assign(c.vi_ok ? c.vi_ndict : 0, 0.0);
+  if (c.vi_ok && c.vi_ndict > 0)
+    OSM_CUDA(cudaMemcpy(c.h_vi_dict.data(), c.vi_dict, sizeof(double) * c.vi_ndict, cudaMemcpyDeviceToHost));
+  drop_graph(c);
+}
+
 // Copy the table values from the (folded) SELL and verify the tables against every row.
 static void mf_refresh(Ctx& c) {
   launch_mf_refresh(c);
@@ -570,6 +578,7 @@ static void assemble(Ctx& c) {
     launch_fold_build(c, c.sides[k], c.subs[c.sides[k].sub]);
   }
   vi_build(c);  // value-indexed hot copy (from the unfolded K^N values)
+  vi_sync_host_dict(c);
   if (c.sort_key == 4) mf_build(c, h_iperm, h_len, h_soff);
 
   // --- reductions and device side table
@@ -658,6 +667,7 @@ static void apply_robin(Ctx& c) {
   dfree(d_a);
   dfree(d_q);
   vi_apply_robin(c, a, qv);
+  vi_sync_host_dict(c);
   if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
   c.robin_dirty = false;
 }
@@ -882,14 +892,17 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   // traffic model: algorithmic bytes per CG iteration per subdomain x its iterations
   for (double& t : c.traffic) t = 0;
   const int nloc = c.s_end - c.s_begin;
-  const bool vi = spmv_variant_of(c) >= 3;
+  const int sv = spmv_variant_of(c);
+  const bool vi = sv == 3 || sv == 4 || sv == 6, mf = sv == 5;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
     for (size_t k = S.s; k < c.inner.size(); k += c.nsub) its += std::max(0, c.inner[k]);
-    // SpMV bytes in the format launched: fp64 SELL 12 B/entry (+ CSR-equivalent 4 B/row) or
-    // value-indexed 4 B/entry (index + offset; the dictionary is L1-resident); vectors p, q 16 B/row
-    c.traffic[0] += (double)its * ((vi ? 4.0 * S.nnz : 12.0 * S.nnz + 4.0 * (S.n + 1)) + 16.0 * S.n);
+    // SpMV bytes in the format launched: fp64 SELL 12 B/entry (+ CSR-equivalent 4 B/row),
+    // value-indexed 4 B/entry (index + offset; the dictionary is on chip), or matrix-free 0 B/entry
+    // (tables in the constant bank); vectors p, q 16 B/row
+    const double mat = mf ? 0.0 : (vi ? 4.0 * S.nnz : 12.0 * S.nnz + 4.0 * (S.n + 1));
+    c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
     c.traffic[1] += (double)its * 56.0 * S.n;
     c.traffic[2] += (double)its * 32.0 * S.n;
@@ -1461,7 +1474,7 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 5) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..5");
+  if (v < 0 || v > 6) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..6");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);

@@ -359,6 +359,7 @@ __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const 
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
   if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c);
+  if constexpr (V == 6) return tile_row_vi_smem(A, blk, x, mf.dict);
   if constexpr (V == 4) {
     double* sd = reinterpret_cast<double*>(smem);
     for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];
@@ -705,6 +706,8 @@ SellDev sell_of(const Ctx& c) {
 
 int spmv_variant_of(const Ctx& c) {
   if (c.spmv_variant == 5 && c.mf_ok) return 5;
+  if (c.spmv_variant == 6 && c.vi_ok && c.vi_ndict <= kCDict) return 6;
+  if (c.spmv_variant == 6) return !c.vi_ok ? 2 : 3;
   if (c.spmv_variant >= 3 && !c.vi_ok) return 2;
   if (c.spmv_variant == 5) return c.vi_ndict > kSmemDict ? 3 : 4;
   if (c.spmv_variant == 4 && c.vi_ndict > kSmemDict) return 3;
@@ -731,6 +734,7 @@ static MfArg<V> mf_arg(const Ctx& c) {
   if constexpr (V == 5) {
     if (c.h_mf_const) a.c = *c.h_mf_const;
   }
+  if constexpr (V == 6) std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.dict);
   return a;
 }
 
@@ -750,6 +754,7 @@ void launch_warm(Ctx& c, double tol, int) {
     case 2: warm_v<2>(c, tol); break;
     case 3: warm_v<3>(c, tol); break;
     case 5: warm_v<5>(c, tol); break;
+    case 6: warm_v<6>(c, tol); break;
     default: warm_v<4>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
@@ -794,6 +799,7 @@ void launch_cg_spmv(Ctx& c) {
     case 2: cg_spmv_v<2>(c); break;
     case 3: cg_spmv_v<3>(c); break;
     case 5: cg_spmv_v<5>(c); break;
+    case 6: cg_spmv_v<6>(c); break;
     default: cg_spmv_v<4>(c); break;
   }
   ++c.launches;
@@ -860,6 +866,7 @@ void launch_resid(Ctx& c) {
     case 2: resid_v<2>(c); break;
     case 3: resid_v<3>(c); break;
     case 5: resid_v<5>(c); break;
+    case 6: resid_v<6>(c); break;
     default: resid_v<4>(c); break;
   }
   OSM_CHECK_LAUNCH();

@@ -22,23 +22,29 @@ ap.add_argument("--nsub", type=int, default=8)
 ap.add_argument("--n", type=int, default=192)
 ap.add_argument("--max-outer", type=int, default=40)
 ap.add_argument("--tol", type=float, default=1e-8)
+ap.add_argument("--row-order", type=int, default=None, help="4 with --spmv 5: matrix-free path")
+ap.add_argument("--spmv", type=int, default=None)
 a = ap.parse_args()
 cfg = dict(synth.CONFIGS["C5"])
 cfg.update(nx=a.n, ny=a.n, nz=a.n, nsub=a.nsub)
 t = time.perf_counter()
 drho = synth.density(cfg)
 o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], 2)
+if a.row_order is not None:
+    o.set_row_order(a.row_order)
 o.decompose(cfg["nsub"])
 p1, p2, q1, q2 = [float(v) for v in a.params[0].split(":")]
 o.set_robin2(p1, q1, p2, q2)
 t1 = time.perf_counter()
 o.assemble()
+active = o.set_spmv_variant(a.spmv) if a.spmv is not None else None
 o.upload_density(drho)
 t2 = time.perf_counter()
 import torch  # noqa: E402
 
 free, total = torch.cuda.mem_get_info()
-print(json.dumps(dict(dof=(2 * a.n - 1) ** 3, setup_s=t2 - t1, input_s=t1 - t, device_used_gb=(total - free) / 1e9)),
+print(json.dumps(dict(dof=(2 * a.n - 1) ** 3, setup_s=t2 - t1, input_s=t1 - t, device_used_gb=(total - free) / 1e9,
+                      spmv_active=active, row_order=a.row_order)),
       flush=True)
 for i, prm in enumerate(a.params):
     p1, p2, q1, q2 = [float(v) for v in prm.split(":")]

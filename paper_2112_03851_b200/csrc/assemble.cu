@@ -357,6 +357,24 @@ __global__ void k_mf_verify(int64_t nrows, const int32_t* __restrict__ blk_sub, 
 }
 }  // namespace
 
+namespace {
+__global__ void k_mf_codes(int64_t nrows, const int32_t* __restrict__ blk_sub, const MfSub* __restrict__ msub,
+                           const int16_t* __restrict__ tabid, uint8_t* __restrict__ code) {
+  const int64_t ri = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ri >= nrows) return;
+  const MfSub& M = msub[blk_sub[ri / kRowsPerBlock]];
+  const int t = mf_table_of(M, ri - M.row0);
+  code[ri] = t >= 0 ? (uint8_t)tabid[t] : (uint8_t)0xff;
+}
+}  // namespace
+
+void launch_mf_codes(const Ctx& c, const int16_t* d_tabid) {
+  k_mf_codes<<<(unsigned)ceil_div(c.nrows_total, 256), 256, 0, c.stream>>>(c.nrows_total, c.blk_sub, c.d_mf_sub,
+                                                                          d_tabid, c.d_mf_code);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+}
+
 void launch_mf_verify(const Ctx& c, int32_t* d_bad) {
   if (!c.mf_ok) return;
   k_mf_verify<<<(unsigned)ceil_div(c.nrows_total, 256), 256, 0, c.stream>>>(

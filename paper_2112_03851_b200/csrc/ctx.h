@@ -103,6 +103,7 @@ struct MfConst {
   int32_t gbeg[kMfMaxTab + 1];       // group range [gbeg[t], gbeg[t+1]) of a table
   int4 delta[kMfMaxGroups];
   double val[4 * kMfMaxGroups];
+  double dinv[kMfMaxTab];            // 1 / (Robin-folded) diagonal of a table, as k_sell_build / k_fold_apply
 };
 template <int V>
 struct MfArg {
@@ -325,6 +326,7 @@ struct Ctx {
   int64_t mf_entries = 0;         // including padding
   std::vector<int32_t> h_mf_begin, h_mf_delta;
   MfConst* h_mf_const = nullptr;  // host copy of the kernel-parameter tables (valid = 0: global tables)
+  uint8_t* d_mf_code = nullptr;   // per internal row: deduplicated table id, 0xff dummy (vector kernels)
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;
@@ -369,6 +371,7 @@ void launch_scatter_phi(const Ctx& c, const Sub& s, int only_owned);
 void launch_gather_local(const Ctx& c, const Sub& s, double* out_contract);
 void launch_mf_refresh(const Ctx& c);  // matrix-free table values <- assembled (folded) SELL values
 void launch_mf_verify(const Ctx& c, int32_t* d_bad);  // every row of every subdomain vs its table
+void launch_mf_codes(const Ctx& c, const int16_t* d_tabid);  // per-row table codes (d_mf_code)
 
 // ---- launchers (schwarz_kernels.cu)
 void launch_warm(Ctx& c, double tol, int warm);

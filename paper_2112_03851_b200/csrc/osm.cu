@@ -163,6 +163,7 @@ static void free_assembly(Ctx& c) {
   c.mf_entries = 0;
   delete c.h_mf_const;
   c.h_mf_const = nullptr;
+  dfree(c.d_mf_code);
   c.assembled = false;
   c.density_set = false;
 }
@@ -234,10 +235,13 @@ static void mf_refresh(Ctx& c) {
     if (it == seen.end()) {
       const int g = (c.h_mf_begin[t + 1] - c.h_mf_begin[t]) / 4;
       if (nt >= kMfMaxTab || ng + g > kMfMaxGroups) return;  // too many: global tables
+      double diag = 0.0;
       for (int e = c.h_mf_begin[t], k = 4 * ng; e < c.h_mf_begin[t + 1]; ++e, ++k) {
         (&P.delta[0].x)[k] = c.h_mf_delta[e];
         P.val[k] = val[e];
+        if (c.h_mf_delta[e] == 0 && val[e] != 0.0) diag = val[e];  // (0, +0.0) entries are padding
       }
+      P.dinv[nt] = diag > 0.0 ? 1.0 / diag : 0.0;
       ng += g;
       it = seen.emplace(key, nt).first;
       P.gbeg[++nt] = ng;
@@ -245,6 +249,17 @@ static void mf_refresh(Ctx& c) {
     P.tabid[t] = (int16_t)it->second;  // t = (ls * 3 + kind) * ncls + class, as mf_table_of
   }
   P.valid = 1;
+  // per-row table codes for the vector kernels (D^{-1} from the tables, dummy rows skipped)
+  if (nt <= 255) {
+    if (!c.d_mf_code) c.d_mf_code = dalloc<uint8_t>(c.nrows_total);
+    std::vector<int16_t> tabid(P.tabid, P.tabid + ntab);
+    int16_t* d_tabid = dupload(c, tabid);
+    launch_mf_codes(c, d_tabid);
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+    dfree(d_tabid);
+  } else {
+    dfree(c.d_mf_code);
+  }
 }
 
 // Matrix-free Kuhn-stencil tables (SpMV variant 5, row order 4).  For every

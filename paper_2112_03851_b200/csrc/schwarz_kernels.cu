@@ -418,7 +418,14 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
 // all loads of a thread issued before any use (memory-level parallelism), one reduction
 // and one counter update per 1024 rows.
 constexpr int kVecThreads = kRowsPerBlock / 2;
-template <int MINB>
+// Matrix-free layout (variant 5): D^{-1} of a row pair from the tables via the rows' 1-byte table
+// codes (0xff: dummy row) instead of the 8-byte dinv stream.
+__device__ __forceinline__ double2 mf_dinv2(uint16_t cc, const MfConst& P) {
+  const int c0 = cc & 0xff, c1 = cc >> 8;
+  return make_double2(c0 != 0xff ? P.dinv[c0] : 0.0, c1 != 0xff ? P.dinv[c1] : 0.0);
+}
+
+template <int MINB, int V>
 __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* __restrict__ vblk_sub,
                                                            const int32_t* __restrict__ vblk_tile0,
                                                            const int32_t* __restrict__ vblk_ntile,
@@ -427,7 +434,9 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
                                                            const double* __restrict__ q,
                                                            const double* __restrict__ dinv, double* __restrict__ part,
                                                            int64_t stride, double tol, int maxit,
-                                                           int32_t* __restrict__ nactive) {
+                                                           int32_t* __restrict__ nactive, const uint8_t* __restrict__ mcode,
+                                                           const __grid_constant__ MfArg<V> mf) {
+  constexpr bool MF = V == 5;
   __shared__ double sm[(kVecThreads / 32) * 2];
   pdl_enter();
   const int64_t vb = blockIdx.x;
@@ -437,20 +446,34 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
   const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;  // row-pair index
   const double a = st[ls].alpha;
   double2 pv[kVecTiles], qv[kVecTiles], xv[kVecTiles], rv[kVecTiles], dv[kVecTiles];
+  bool real[kVecTiles];
+  uint16_t cc[kVecTiles];
+#pragma unroll
+  for (int j = 0; j < kVecTiles; ++j) {
+    real[j] = j < nt;
+    if constexpr (MF) {  // codes load alongside the vectors; D^{-1} is looked up after
+      if (j < nt) cc[j] = __ldg(reinterpret_cast<const uint16_t*>(mcode) + p0 + (int64_t)j * kVecThreads);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
-    if (j < nt) {
+    if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
       pv[j] = reinterpret_cast<const double2*>(p)[i2];
       qv[j] = reinterpret_cast<const double2*>(q)[i2];
       xv[j] = reinterpret_cast<const double2*>(x)[i2];
       rv[j] = reinterpret_cast<const double2*>(r)[i2];
-      dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
+      if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
     }
+  if constexpr (MF) {
+#pragma unroll
+    for (int j = 0; j < kVecTiles; ++j)
+      if (real[j]) dv[j] = mf_dinv2(cc[j], mf.c);
+  }
   double v[2] = {0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
-    if (j < nt) {
+    if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
       xv[j].x = fma(a, pv[j].x, xv[j].x);
       xv[j].y = fma(a, pv[j].y, xv[j].y);
@@ -489,11 +512,15 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
 }
 
 // p = D^{-1} r + beta p  (vector blocks as k_cg_update)
+template <int V>
 __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restrict__ vblk_sub,
                                                         const int32_t* __restrict__ vblk_tile0,
                                                         const int32_t* __restrict__ vblk_ntile,
                                                         const SubState* __restrict__ st, const double* __restrict__ r,
-                                                        const double* __restrict__ dinv, double* __restrict__ p) {
+                                                        const double* __restrict__ dinv, double* __restrict__ p,
+                                                        const uint8_t* __restrict__ mcode,
+                                                        const __grid_constant__ MfArg<V> mf) {
+  constexpr bool MF = V == 5;
   pdl_enter();
   const int64_t vb = blockIdx.x;
   const int ls = vblk_sub[vb];
@@ -502,17 +529,31 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restric
   const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;
   const double beta = st[ls].beta;
   double2 rv[kVecTiles], dv[kVecTiles], pv[kVecTiles];
+  bool real[kVecTiles];
+  uint16_t cc[kVecTiles];
+#pragma unroll
+  for (int j = 0; j < kVecTiles; ++j) {
+    real[j] = j < nt;
+    if constexpr (MF) {  // codes load alongside the vectors; D^{-1} is looked up after
+      if (j < nt) cc[j] = __ldg(reinterpret_cast<const uint16_t*>(mcode) + p0 + (int64_t)j * kVecThreads);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
-    if (j < nt) {
+    if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
       rv[j] = reinterpret_cast<const double2*>(r)[i2];
-      dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
+      if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
       pv[j] = reinterpret_cast<const double2*>(p)[i2];
     }
+  if constexpr (MF) {
+#pragma unroll
+    for (int j = 0; j < kVecTiles; ++j)
+      if (real[j]) dv[j] = mf_dinv2(cc[j], mf.c);
+  }
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
-    if (j < nt) {
+    if (real[j]) {
       pv[j].x = fma(beta, pv[j].x, dv[j].x * rv[j].x);
       pv[j].y = fma(beta, pv[j].y, dv[j].y * rv[j].y);
       reinterpret_cast<double2*>(p)[p0 + (int64_t)j * kVecThreads] = pv[j];
@@ -806,25 +847,45 @@ void launch_cg_spmv(Ctx& c) {
   timer_end(c, T_SPMV);
 }
 
+// The vector kernels take D^{-1} from the matrix-free tables (and skip pairs of dummy rows) when
+// variant 5 runs with its tables in the constant bank.
+static bool mf_vectors(const Ctx& c) {
+  return spmv_variant_of(c) == 5 && c.h_mf_const && c.h_mf_const->valid && c.d_mf_code;
+}
+
+template <int MINB, int V>
+static void cg_update_v(Ctx& c, double tol, int maxit) {
+  launch_pdl(c, k_cg_update<MINB, V>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+             (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
+             (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive,
+             (const uint8_t*)c.d_mf_code, mf_arg<V>(c));
+}
+
 void launch_cg_update(Ctx& c, double tol, int maxit) {
   timer_begin(c, T_UPDATE);
-  if (c.update_variant == 1)
-    launch_pdl(c, k_cg_update<8>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
-               (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
-               (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive);
+  if (mf_vectors(c))
+    cg_update_v<1, 5>(c, tol, maxit);
+  else if (c.update_variant == 1)
+    cg_update_v<8, 0>(c, tol, maxit);
   else
-    launch_pdl(c, k_cg_update<1>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
-               (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
-               (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive);
+    cg_update_v<1, 0>(c, tol, maxit);
   ++c.launches;
   timer_end(c, T_UPDATE);
 }
 
+template <int V>
+static void cg_dir_v(Ctx& c) {
+  launch_pdl(c, k_cg_dir<V>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+             (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, (const SubState*)c.st, (const double*)c.r,
+             (const double*)c.dinv, c.p, (const uint8_t*)c.d_mf_code, mf_arg<V>(c));
+}
+
 void launch_cg_dir(Ctx& c) {
   timer_begin(c, T_DIR);
-  launch_pdl(c, k_cg_dir, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
-             (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, (const SubState*)c.st, (const double*)c.r,
-             (const double*)c.dinv, c.p);
+  if (mf_vectors(c))
+    cg_dir_v<5>(c);
+  else
+    cg_dir_v<0>(c);
   ++c.launches;
   timer_end(c, T_DIR);
 }

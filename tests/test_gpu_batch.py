@@ -105,3 +105,40 @@ def test_oo2_batch_matches_oracle():
         for s in range(CFG["nsub"]):
             assert rel_l2(o.batch_local_solution(b, s), orep.u[s]) <= 1e-10
     o.close()
+
+
+def test_stride_64_population_matches_stride_32():
+    """B > 32 runs the stride-64 kernels (lane owns 4 candidates); B <= 32 the stride-32 ones
+    (2 per lane).  The same candidate must give the same history and iterate either way, and both
+    must agree with the single-candidate path."""
+    import paper_2112_03851_b200 as P
+
+    drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=31)
+    o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+    o.decompose(CFG["nsub"])
+    o.set_robin(np.full(2, 20.0), np.full(2, 20.0))
+    o.assemble()
+    o.upload_density(drho)
+    rng = np.random.default_rng(5)
+    pairs = np.exp(rng.uniform(np.log(3.0), np.log(80.0), size=(40, 2)))
+    al = np.repeat(pairs[:, :1], 2, axis=1)
+    ar = np.repeat(pairs[:, 1:], 2, axis=1)
+    rep64 = o.solve_batch(al, ar, tol_outer=1e-8, max_outer=400)
+    assert rep64.B == 40 and rep64.n_converged == 40
+    picks = (0, 17, 39)
+    h64 = {b: o.batch_history(b) for b in picks}
+    u64 = {b: [o.batch_local_solution(b, s) for s in range(CFG["nsub"])] for b in picks}
+    rep32 = o.solve_batch(al[list(picks)], ar[list(picks)], tol_outer=1e-8, max_outer=400)
+    assert rep32.B == 3
+    for i, b in enumerate(picks):
+        h32 = o.batch_history(i)
+        assert len(h32) == len(h64[b])
+        assert np.all(np.abs(h32 - h64[b]) <= 1e-12 * h64[b] + 1e-15)
+        for s in range(CFG["nsub"]):
+            assert rel_l2(o.batch_local_solution(i, s), u64[b][s]) <= 1e-12
+        o.set_robin(al[b], ar[b])
+        st, _ = o.solve(tol_outer=1e-8, max_outer=400)
+        assert st == 0
+        ok, d = history_ok(o.history(), h64[b])
+        assert ok and len(o.history()) == len(h64[b]), d.max()
+    o.close()

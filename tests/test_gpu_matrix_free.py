@@ -109,3 +109,44 @@ def test_matrix_free_c3_full_solve_bitwise():
     assert np.array_equal(hs[0][0], hs[1][0]) and np.array_equal(hs[0][1], hs[1][1])
     assert np.array_equal(hs[0][2], hs[1][2])
     assert hs[0][0][-1] <= 1e-8
+
+
+@pytest.mark.parametrize("case", ["nonuniform_sides", "single_slab", "ragged_p1"])
+def test_matrix_free_more_layouts(case):
+    """Per-interface coefficients (one table set per side), one subdomain (both x ends Dirichlet),
+    and a ragged P1 partition: variant 5 stays bitwise equal to the fp64 SELL in row order 4."""
+    if case == "nonuniform_sides":
+        cfg = dict(nx=15, ny=5, nz=6, lx=1.2, ly=0.6, lz=0.7, order=2, nsub=3)
+        robin = ([10.0, 14.0], [0.05, 0.0], [3.0, 2.0], [0.2, 0.1])
+    elif case == "single_slab":
+        cfg = dict(nx=6, ny=6, nz=5, lx=1.0, ly=1.0, lz=0.8, order=2, nsub=1)
+        robin = ([], [], [], [])
+    else:
+        cfg = dict(nx=17, ny=7, nz=6, lx=1.0, ly=0.5, lz=0.4, order=1, nsub=4)
+        robin = _robin(6.0, 0.0, 9.0, 0.0, 3)
+    drho = synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=37)
+    import paper_2112_03851_b200 as P
+
+    out = []
+    for v in (5, 2):
+        o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+        o.set_row_order(4)
+        o.decompose(cfg["nsub"])
+        if cfg["nsub"] > 1:
+            o.set_robin2(*robin)
+        o.assemble()
+        active = o.set_spmv_variant(v)
+        o.upload_density(drho)
+        st, rep = o.solve(tol_outer=1e-8, max_outer=400)
+        out.append((active, st, o.history(), [o.local_solution(s) for s in range(cfg["nsub"])]))
+        o.close()
+    (a5, st5, h5, u5), (a2, st2, h2, u2) = out
+    assert a5 == 5 and a2 == 2 and st5 == st2 == 0
+    assert np.array_equal(h5, h2)
+    for a, b in zip(u5, u2):
+        assert np.array_equal(a, b)
+    if cfg["nsub"] > 1:
+        q = (robin[1], robin[3]) if case == "nonuniform_sides" else None
+        prob, rep = oracle_run(cfg, drho, robin[0], robin[2], q=q)
+        ok, d = history_ok(h5, rep.h)
+        assert ok and len(h5) == len(rep.h), d.max()

@@ -268,7 +268,9 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * 0 fp64 SELL-256, LDG rows; 1 fp64 SELL-256, warp-specialized cp.async.bulk pipeline;
  * 2 fp64 SELL-256, LDG rows at 32 registers; 3 value-indexed (16-bit dictionary index + 16-bit
  * column offset); 4 = 3 with the dictionary in shared memory; 6 = 3 with the dictionary in the
- * constant bank as a kernel parameter (default, up to 2048 distinct values); 5 matrix-free Kuhn
+ * constant bank as a kernel parameter (default, up to 2048 distinct values); 7 = 6 on wide
+ * entries (12-bit index, 20-bit offset), selected automatically when offsets exceed int16;
+ * 5 matrix-free Kuhn
  * stencil (the K_s values are uniform per parity class and row kind on the
  * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row
  * order 4, see osm_set_row_order).  Variants 3/4/6 fall back to 2 when the matrix does not

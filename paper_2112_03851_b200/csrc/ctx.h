@@ -120,6 +120,10 @@ template <>
 struct MfArg<6> {
   double dict[kCDict];
 };
+template <>
+struct MfArg<7> {  // variant 6 on the wide (20-bit offset) entries
+  double dict[kCDict];
+};
 
 struct SellDev {
   const double* val;
@@ -313,8 +317,9 @@ struct Ctx {
   int spmv_variant = 6;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
                          // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary
                          // in shared memory (default; falls back to 3, then 2, when it does not apply),
-                         // 5: matrix-free Kuhn stencil (row order 4 only; else as 4), 6: 3 with the
-                         // dictionary in the constant bank (default; else 3)
+                         // 5: matrix-free Kuhn stencil (row order 4 only; else as 6), 6: 3 with the
+                         // dictionary in the constant bank (default; else 3), 7: 6 on wide entries
+                         // (chosen automatically when offsets need 20 bits)
 
   // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
   bool mf_ok = false;
@@ -332,7 +337,7 @@ struct Ctx {
   bool vi_ok = false;
   bool vi_per_side = false;  // fold slots per interface side (else per side kind)
   uint16_t* vi_idx = nullptr;
-  int16_t* vi_col = nullptr;
+  bool vi_wide = false;  // entries (12-bit index << 20) | 20-bit offset (else 16 | 16)
   double* vi_dict = nullptr;
   uint32_t* vi_packed = nullptr;
   int64_t* vi_poff = nullptr;

@@ -908,7 +908,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   for (double& t : c.traffic) t = 0;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
-  const bool vi = sv == 3 || sv == 4 || sv == 6, mf = sv == 5;
+  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1489,7 +1489,7 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 6) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..6");
+  if (v < 0 || v > 7) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..7");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);

@@ -286,6 +286,7 @@ __device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, con
 // Variant 4: variant 3 with the dictionary staged in shared memory at block start (dictionary
 // lookups leave the L1 tag path; used when the dictionary fits kSmemDict entries).
 constexpr int kSmemDict = 2048;
+template <bool W = false>  // W: wide entries (12-bit index << 20 | 20-bit signed offset)
 __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk, const double* __restrict__ x,
                                                    const double* sdict) {
   constexpr int T = kRowsPerBlock;
@@ -296,9 +297,26 @@ __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk
   if (ng == 0) return s;
   uint4 e = ld_stream4(gp);
   for (int g = 0; g < ng; ++g) {
-    const double x0 = __ldg(xr + (int16_t)(e.x & 0xffffu)), x1 = __ldg(xr + (int16_t)(e.y & 0xffffu));
-    const double x2 = __ldg(xr + (int16_t)(e.z & 0xffffu)), x3 = __ldg(xr + (int16_t)(e.w & 0xffffu));
-    const double v0 = sdict[e.x >> 16], v1 = sdict[e.y >> 16], v2 = sdict[e.z >> 16], v3 = sdict[e.w >> 16];
+    double x0, x1, x2, x3, v0, v1, v2, v3;
+    if constexpr (W) {
+      x0 = __ldg(xr + ((int32_t)(e.x << 12) >> 12));
+      x1 = __ldg(xr + ((int32_t)(e.y << 12) >> 12));
+      x2 = __ldg(xr + ((int32_t)(e.z << 12) >> 12));
+      x3 = __ldg(xr + ((int32_t)(e.w << 12) >> 12));
+      v0 = sdict[e.x >> 20];
+      v1 = sdict[e.y >> 20];
+      v2 = sdict[e.z >> 20];
+      v3 = sdict[e.w >> 20];
+    } else {
+      x0 = __ldg(xr + (int16_t)(e.x & 0xffffu));
+      x1 = __ldg(xr + (int16_t)(e.y & 0xffffu));
+      x2 = __ldg(xr + (int16_t)(e.z & 0xffffu));
+      x3 = __ldg(xr + (int16_t)(e.w & 0xffffu));
+      v0 = sdict[e.x >> 16];
+      v1 = sdict[e.y >> 16];
+      v2 = sdict[e.z >> 16];
+      v3 = sdict[e.w >> 16];
+    }
     if (g + 1 < ng) e = ld_stream4(gp + 4 * (int64_t)T * (g + 1));
     s = fma(v0, x0, s);
     s = fma(v1, x1, s);
@@ -359,7 +377,8 @@ __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const 
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
   if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c);
-  if constexpr (V == 6) return tile_row_vi_smem(A, blk, x, mf.dict);
+  if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict);
+  if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict);
   if constexpr (V == 4) {
     double* sd = reinterpret_cast<double*>(smem);
     for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];
@@ -746,13 +765,19 @@ SellDev sell_of(const Ctx& c) {
 }  // namespace
 
 int spmv_variant_of(const Ctx& c) {
-  if (c.spmv_variant == 5 && c.mf_ok) return 5;
-  if (c.spmv_variant == 6 && c.vi_ok && c.vi_ndict <= kCDict) return 6;
-  if (c.spmv_variant == 6) return !c.vi_ok ? 2 : 3;
-  if (c.spmv_variant >= 3 && !c.vi_ok) return 2;
-  if (c.spmv_variant == 5) return c.vi_ndict > kSmemDict ? 3 : 4;
-  if (c.spmv_variant == 4 && c.vi_ndict > kSmemDict) return 3;
-  return c.spmv_variant;
+  int v = c.spmv_variant;
+  if (v == 5) {
+    if (c.mf_ok) return 5;
+    v = 6;
+  }
+  if (v < 3) return v;
+  // value-indexed family
+  if (!c.vi_ok) return 2;
+  if (c.vi_wide) return c.vi_ndict <= kCDict ? 7 : 2;  // wide entries: constant-bank kernel only
+  if (v == 7) v = 6;
+  if (v == 6) return c.vi_ndict <= kCDict ? 6 : 3;
+  if (v == 4) return c.vi_ndict <= kSmemDict ? 4 : 3;
+  return 3;
 }
 
 static int spmv_smem(const Ctx& c) {
@@ -775,7 +800,8 @@ static MfArg<V> mf_arg(const Ctx& c) {
   if constexpr (V == 5) {
     if (c.h_mf_const) a.c = *c.h_mf_const;
   }
-  if constexpr (V == 6) std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.dict);
+  if constexpr (V == 6 || V == 7)
+    std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.dict);
   return a;
 }
 
@@ -796,6 +822,7 @@ void launch_warm(Ctx& c, double tol, int) {
     case 3: warm_v<3>(c, tol); break;
     case 5: warm_v<5>(c, tol); break;
     case 6: warm_v<6>(c, tol); break;
+    case 7: warm_v<7>(c, tol); break;
     default: warm_v<4>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
@@ -841,6 +868,7 @@ void launch_cg_spmv(Ctx& c) {
     case 3: cg_spmv_v<3>(c); break;
     case 5: cg_spmv_v<5>(c); break;
     case 6: cg_spmv_v<6>(c); break;
+    case 7: cg_spmv_v<7>(c); break;
     default: cg_spmv_v<4>(c); break;
   }
   ++c.launches;
@@ -928,6 +956,7 @@ void launch_resid(Ctx& c) {
     case 3: resid_v<3>(c); break;
     case 5: resid_v<5>(c); break;
     case 6: resid_v<6>(c); break;
+    case 7: resid_v<7>(c); break;
     default: resid_v<4>(c); break;
   }
   OSM_CHECK_LAUNCH();

@@ -7,8 +7,9 @@
 //
 // Robin folding (K_s = K^N + p M + q S on interface rows) gives each distinct
 // (side, K^N value, m, s) tuple its own dictionary slot; osm_set_robin/2 only rewrites that
-// small dictionary tail.  If the dictionary would exceed 65536 entries or a column offset
-// does not fit int16, the context stays on the fp64 SELL path.
+// small dictionary tail.  Entries are (16-bit index, 16-bit offset); when an offset does not fit
+// int16 the wide form (12-bit index, 20-bit offset; e.g. C5 with S = 8) is used.  If neither fits
+// (more than 65536 / 4096 values, or offsets beyond 2^19) the context stays on the fp64 SELL path.
 #include <thrust/binary_search.h>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
@@ -39,41 +40,44 @@ __global__ void k_vi_index(int64_t n, const double* __restrict__ val, const doub
   vidx[i] = (uint16_t)lo;
 }
 
-// column offsets: col - own internal row (tile t, lane l = row 256 t + l); *overflow = 1 on overflow
-__global__ void k_vi_cols(int64_t ntile, const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
-                          const int32_t* __restrict__ col, int16_t* __restrict__ cidx, int32_t* __restrict__ flags) {
+// Largest |col - own internal row| over the SELL (tile t, lane l = row 256 t + l), into *maxoff.
+__global__ void k_vi_maxoff(int64_t ntile, const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
+                            const int32_t* __restrict__ col, int32_t* __restrict__ maxoff) {
   const int64_t t = blockIdx.x;
   if (t >= ntile) return;
   const int64_t row = t * kRowsPerBlock + threadIdx.x;
   const int w = twidth[t];
   const int64_t base = toff[t] + threadIdx.x;
+  int64_t m = 0;
   for (int k = 0; k < w; ++k) {
     const int64_t d = (int64_t)col[base + (int64_t)kRowsPerBlock * k] - row;
-    if (d < -32768 || d > 32767) {
-      atomicOr(flags, 1);
-      return;
-    }
-    cidx[base + (int64_t)kRowsPerBlock * k] = (int16_t)d;
+    m = max(m, d < 0 ? -d : d);
   }
+  atomicMax(maxoff, (int32_t)min(m, (int64_t)INT32_MAX));
 }
 
 // Packed layout: tile t holds rows 256 t + r; its entries are grouped by 4 (width padded to a
 // multiple of 4 with (zero value, offset 0) entries); group g of row r is the uint4 at
-// poff[t] + 4 (256 g + r) (in 32-bit words), entry = (value index << 16) | (uint16) offset.
+// poff[t] + 4 (256 g + r) (in 32-bit words).  Entry = (value index << 16) | (uint16) offset, or in
+// the wide form (value index << 20) | (offset & 0xfffff) (12-bit index, 20-bit signed offset).
+template <bool W>
 __global__ void k_vi_pack(int64_t ntile, const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
                           const int64_t* __restrict__ poff, const uint16_t* __restrict__ vidx,
-                          const int16_t* __restrict__ cidx, uint32_t zero_idx, uint32_t* __restrict__ packed) {
+                          const int32_t* __restrict__ col, uint32_t zero_idx, uint32_t* __restrict__ packed) {
+  constexpr int IS = W ? 20 : 16;
+  constexpr uint32_t OM = W ? 0xfffffu : 0xffffu;
   const int64_t t = blockIdx.x;
   if (t >= ntile) return;
   const int r = threadIdx.x;
+  const int64_t row = t * kRowsPerBlock + r;
   const int w = twidth[t];
   const int w4 = (w + 3) & ~3;
   const int64_t base = toff[t] + r;
   for (int k = 0; k < w4; ++k) {
-    uint32_t e = zero_idx << 16;
+    uint32_t e = zero_idx << IS;
     if (k < w) {
       const int64_t i = base + (int64_t)kRowsPerBlock * k;
-      e = ((uint32_t)vidx[i] << 16) | (uint32_t)(uint16_t)cidx[i];
+      e = ((uint32_t)vidx[i] << IS) | ((uint32_t)(int32_t)(col[i] - row) & OM);
     }
     packed[poff[t] + 4 * ((int64_t)kRowsPerBlock * (k >> 2) + r) + (k & 3)] = e;
   }
@@ -90,16 +94,15 @@ __global__ void k_vi_fold_slots(int64_t nfold, const int64_t* __restrict__ pos, 
 
 void vi_free(Ctx& c) {
   if (c.vi_idx) cudaFree(c.vi_idx);
-  if (c.vi_col) cudaFree(c.vi_col);
   if (c.vi_dict) cudaFree(c.vi_dict);
   if (c.vi_packed) cudaFree(c.vi_packed);
   if (c.vi_poff) cudaFree(c.vi_poff);
   c.vi_idx = nullptr;
-  c.vi_col = nullptr;
   c.vi_dict = nullptr;
   c.vi_packed = nullptr;
   c.vi_poff = nullptr;
   c.vi_ok = false;
+  c.vi_wide = false;
   c.vi_fold_tuples.clear();
 }
 
@@ -178,20 +181,25 @@ void vi_build(Ctx& c, bool per_side) {
     OSM_CUDA(cudaStreamSynchronize(c.stream));
     cudaFree(d_slot);
   }
-  // 4. int16 column offsets
-  OSM_CUDA(cudaMalloc(&c.vi_col, sizeof(int16_t) * n));
+  // 4. offset width: 16-bit offsets with 16-bit indices, else 20-bit offsets with 12-bit indices
   OSM_CUDA(cudaMemsetAsync(c.d_flags + 2, 0, sizeof(int32_t), c.stream));
-  k_vi_cols<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(c.nblk_total, c.sell_soff, c.sell_swidth,
-                                                                   c.sell_col, c.vi_col, c.d_flags + 2);
+  k_vi_maxoff<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(c.nblk_total, c.sell_soff, c.sell_swidth,
+                                                                     c.sell_col, c.d_flags + 2);
   OSM_CHECK_LAUNCH();
   ++c.launches;
   int32_t flags[4];
   OSM_CUDA(cudaMemcpyAsync(flags, c.d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c.stream));
   OSM_CUDA(cudaStreamSynchronize(c.stream));
+  OSM_CUDA(cudaMemsetAsync(c.d_flags + 2, 0, sizeof(int32_t), c.stream));
   cudaFree(tmp);
-  if (flags[2]) {  // a column offset does not fit int16
-    vi_free(c);
-    return;
+  const int32_t maxoff = flags[2];
+  bool wide = false;
+  if (maxoff > 32767) {
+    if (maxoff > 524287 || ndict > 4096) {  // neither form fits: stay on the fp64 SELL path
+      vi_free(c);
+      return;
+    }
+    wide = true;
   }
   // 5. packed copy (4 entries of a row per 16-byte load); the 2-byte arrays are freed
   std::vector<int32_t> tw(c.nblk_total);
@@ -209,18 +217,20 @@ void vi_build(Ctx& c, bool per_side) {
   OSM_CUDA(cudaMalloc(&c.vi_poff, sizeof(int64_t) * c.nblk_total));
   OSM_CUDA(cudaMemcpy(c.vi_poff, poff.data(), sizeof(int64_t) * c.nblk_total, cudaMemcpyHostToDevice));
   OSM_CUDA(cudaMalloc(&c.vi_packed, sizeof(uint32_t) * std::max<int64_t>(1, words)));
-  k_vi_pack<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(c.nblk_total, c.sell_soff, c.sell_swidth,
-                                                                   c.vi_poff, c.vi_idx, c.vi_col, zero_idx,
-                                                                   c.vi_packed);
+  if (wide)
+    k_vi_pack<true><<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(
+        c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_poff, c.vi_idx, c.sell_col, zero_idx, c.vi_packed);
+  else
+    k_vi_pack<false><<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(
+        c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_poff, c.vi_idx, c.sell_col, zero_idx, c.vi_packed);
   OSM_CHECK_LAUNCH();
   ++c.launches;
   OSM_CUDA(cudaStreamSynchronize(c.stream));
   cudaFree(c.vi_idx);
-  cudaFree(c.vi_col);
   c.vi_idx = nullptr;
-  c.vi_col = nullptr;
   c.vi_words = words;
   c.vi_per_side = per_side;
+  c.vi_wide = wide;
   c.vi_ok = true;
 }
 

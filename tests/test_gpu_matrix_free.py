@@ -71,9 +71,9 @@ def test_matrix_free_p1_and_row_order_4_default_variant():
     robin = _robin(a, 0.0, a, 0.0, cfg["nsub"] - 1)
     mf = _solve(cfg, drho, robin, 5)
     assert mf["active"] == 5 and mf["st"] == 0
-    dflt = _solve(cfg, drho, robin, 4)  # row order 4: 16-bit offsets do not fit -> fp64 SELL
-    assert dflt["active"] in (2, 4)
-    assert np.array_equal(mf["h"], dflt["h"]) if dflt["active"] == 2 else True
+    dflt = _solve(cfg, drho, robin, 6)  # row order 4: offsets need 20 bits -> wide value-indexed (7)
+    assert dflt["active"] in (6, 7)
+    assert np.array_equal(mf["h"], dflt["h"])
     prob, rep = oracle_run(cfg, drho, robin[0], robin[2])
     ok, d = history_ok(mf["h"], rep.h)
     assert ok and len(mf["h"]) == len(rep.h), d.max()
@@ -86,7 +86,7 @@ def test_thin_slabs_fall_back_or_verify():
     drho = synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=29)
     robin = _robin(8.0, 0.0, 8.0, 0.0, cfg["nsub"] - 1)
     mf = _solve(cfg, drho, robin, 5)
-    assert mf["active"] in (2, 3, 4, 5) and mf["st"] == 0
+    assert mf["active"] in (2, 3, 4, 5, 6, 7) and mf["st"] == 0
     prob, rep = oracle_run(cfg, drho, robin[0], robin[2])
     ok, d = history_ok(mf["h"], rep.h)
     assert ok and len(mf["h"]) == len(rep.h), d.max()
@@ -150,3 +150,18 @@ def test_matrix_free_more_layouts(case):
         prob, rep = oracle_run(cfg, drho, robin[0], robin[2], q=q)
         ok, d = history_ok(h5, rep.h)
         assert ok and len(h5) == len(rep.h), d.max()
+
+
+def test_wide_value_indexed_entries_in_row_order_4():
+    """Row order 4 puts neighbours up to ~7 hIJK rows apart: the value-indexed copy switches to wide
+    entries (12-bit index, 20-bit offset; variant 7), bitwise equal to the fp64 SELL and to variant 5."""
+    cfg = dict(nx=12, ny=40, nz=40, lx=1.0, ly=1.0, lz=1.0, order=2, nsub=3)  # class stride 8405 rows
+    S = cfg["nsub"]
+    drho = synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=41)
+    robin = _robin(30.0, 0.005, 20.0, 0.002, S - 1)
+    w = _solve(cfg, drho, robin, 6)
+    ref = _solve(cfg, drho, robin, 2)
+    assert w["active"] == 7 and w["st"] == 0
+    assert np.array_equal(w["h"], ref["h"]) and np.array_equal(w["h2"], ref["h2"])
+    for a, b in zip(w["u"], ref["u"]):
+        assert np.array_equal(a, b)

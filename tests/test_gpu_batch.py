@@ -142,3 +142,31 @@ def test_stride_64_population_matches_stride_32():
         ok, d = history_ok(o.history(), h64[b])
         assert ok and len(o.history()) == len(h64[b]), d.max()
     o.close()
+
+
+def test_batch_is_independent_of_the_single_path_row_order():
+    """The batched solver keeps its own contract-order layout: a context assembled in row order 4
+    (matrix-free layout, dummy rows) gives bitwise the same iterates; h(n) differs only through
+    ||f||, which the single path reduces in its own row order (last-bit differences)."""
+    import paper_2112_03851_b200 as P
+
+    drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=43)
+    out = []
+    for order in (3, 4):
+        o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+        o.set_row_order(order)
+        o.decompose(CFG["nsub"])
+        o.set_robin(np.full(2, 20.0), np.full(2, 20.0))
+        o.assemble()
+        o.upload_density(drho)
+        al = np.array([[a, a] for a, _ in CANDS])
+        ar = np.array([[b, b] for _, b in CANDS])
+        rep = o.solve_batch(al, ar, tol_outer=1e-8, max_outer=400)
+        assert rep.n_converged == len(CANDS)
+        out.append([(o.batch_history(b), [o.batch_local_solution(b, s) for s in range(CFG["nsub"])])
+                    for b in range(len(CANDS))])
+        o.close()
+    for (h3, u3), (h4, u4) in zip(*out):
+        assert len(h3) == len(h4) and np.all(np.abs(h3 - h4) <= 1e-14 * h3)
+        for a, b in zip(u3, u4):
+            assert np.array_equal(a, b)

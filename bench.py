@@ -306,6 +306,7 @@ def main():
                 "format": "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
                           "offset) + 16 B per row (p, q); dictionary in the constant bank (kernel parameter)",
                 "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
+                "exchange": exchange_block(kt, tm, world),
                 "limiter": "L1/TEX gather path and issue, not HBM (ncu: l1tex 59% of peak, issue 51%, dram 48%; "
                            "profiles/r01g_ncu_summary.md)"}
 
@@ -363,6 +364,19 @@ def main():
     osm.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def exchange_block(kt, tm, world):
+    """NCCL trace exchange of the instrumented solve: bytes this rank sent, time of the
+    exchange calls on the stream, and the resulting rate (latency-bound at these message sizes)."""
+    if world == 1:
+        return None
+    n, ms = kt.get("exchange", (0, 0.0))
+    b = tm.get("exchange_bytes", 0.0)
+    return {"calls": n, "ms": ms, "bytes_sent": b, "us_per_call": 1e3 * ms / max(1, n),
+            "gbs": b / (ms / 1e3) / 1e9 if ms > 0 else None,
+            "note": "per outer iteration: [g|u] to each neighbour and the interface-row residual; NVLink "
+                    "fraction = gbs / 900 GB/s per direction"}
 
 
 _rows = {}

@@ -243,7 +243,9 @@ osm_status osm_get_kernel_timing(osm_ctx* ctx, osm_kernel_time* out, int cap, in
  * the last solve: out[0] = SpMV kernel bytes (in the format of the
  * SpMV variant that ran), out[1] = update kernel bytes, out[2] = direction kernel bytes,
  * out[3] = SELL padding entries, out[4] = structural nnz (local), out[5] = local rows,
- * out[6] = SpMV bytes of the CSR-equivalent fp64 format (12 nnz + 4 (n+1) + 16 n). n <= 8. */
+ * out[6] = SpMV bytes of the CSR-equivalent fp64 format (12 nnz + 4 (n+1) + 16 n), out[7] = bytes
+ * this rank sent through NCCL in the interface exchanges of the last solve. n <= 8.  With timing
+ * on, osm_get_kernel_timing also reports "exchange": the NCCL exchange calls on the stream. */
 osm_status osm_get_traffic_model(osm_ctx* ctx, double* out, int n);
 
 /* Host-only distribution plan (no GPU needed): subdomains [s_begin, s_end) of `rank`, and

@@ -467,7 +467,7 @@ class Osm:
         out = np.zeros(8)
         _check(_lib.osm_get_traffic_model(self._h, _ptr(out, C.c_double), 8))
         return dict(spmv_bytes=out[0], update_bytes=out[1], dir_bytes=out[2], pad_entries=out[3], nnz=out[4],
-                    rows=out[5], csr_equiv_bytes=out[6])
+                    rows=out[5], csr_equiv_bytes=out[6], exchange_bytes=out[7])
 
 
 def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None, row_order=None,

@@ -361,6 +361,7 @@ struct Ctx {
 
   // traffic model of the last solve
   double traffic[8] = {0};
+  double exch_bytes = 0;  // NCCL exchange bytes sent in the current solve
   mutable int64_t launches = 0;  // kernel launches issued by this context
 };
 
@@ -409,6 +410,6 @@ int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls ba
 // timing helpers (osm.cu)
 void timer_begin(Ctx& c, int id);
 void timer_end(Ctx& c, int id);
-enum TimerId { T_SPMV = 0, T_UPDATE, T_DIR, T_WARM, T_RESID, T_OUTER_MISC, T_COUNT };
+enum TimerId { T_SPMV = 0, T_UPDATE, T_DIR, T_WARM, T_RESID, T_OUTER_MISC /* NCCL exchange */, T_COUNT };
 
 }  // namespace osm

@@ -690,11 +690,20 @@ static void apply_robin(Ctx& c) {
 // ------------------------------------------------------------------ exchange
 // part 1: [g | u] both directions for every remote side; part 2: the right slab's
 // interface-row residual w to the owner (left slab).
+static void exchange_calls(Ctx& c, int part);
 static void exchange(Ctx& c, int part) {
   if (!c.comm) return;
   bool any = false;
   for (const Side& sd : c.sides) any = any || sd.remote;
   if (!any) return;
+  timer_begin(c, T_OUTER_MISC);  // NCCL trace exchange, timed on the library stream
+  exchange_calls(c, part);
+  timer_end(c, T_OUTER_MISC);
+  for (const Side& sd : c.sides)  // bytes this rank sends (traffic[7])
+    if (sd.remote && (part == 1 || sd.which == 1)) c.exch_bytes += (part == 1 ? 16.0 : 8.0) * c.nG;
+}
+
+static void exchange_calls(Ctx& c, int part) {
   const int64_t nG = c.nG;
   if (c.force_remote) {
     // every side talks to its own rank: NCCL matches the j-th send with the j-th receive, so each
@@ -841,6 +850,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     OSM_CUDA(cudaMemsetAsync(c.unbr_all, 0, sizeof(double) * nGs, c.stream));
   }
   c.hist.clear();
+  c.exch_bytes = 0;
   c.inner.clear();
   int status = OSM_NOT_CONVERGED;
   int grow = 0;
@@ -906,6 +916,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   timers_collect(c);
   // traffic model: algorithmic bytes per CG iteration per subdomain x its iterations
   for (double& t : c.traffic) t = 0;
+  c.traffic[7] = c.exch_bytes;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
   const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5;
@@ -1024,7 +1035,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_SORT")) c.sort_key = std::atoi(e);
     spmv_init_attributes();
     c.timers.resize(T_COUNT);
-    const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "outer_misc"};
+    const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "exchange"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
     if (const char* e = std::getenv("OSM_FORCE_REMOTE")) c.force_remote = std::atoi(e) != 0 && c.nranks == 1;
     if (c.nranks > 1) {

@@ -281,7 +281,9 @@ struct Ctx {
   SideDev* d_sides = nullptr;
   std::vector<SideDev> h_sides;
   // reductions
-  double* part = nullptr;  // 3 * nblk_total block partials
+  double* part = nullptr;  // 3 * nblk_total block partials (SpMV / warm / residual kernels)
+  double* part_upd = nullptr;  // 2 * nvblk_total vector-block partials (update kernel; separate so that
+                               // two subdomain groups' SpMV and update can run concurrently)
   double* side_part = nullptr;  // per side block partials
   double* side_sum = nullptr;   // per side result
   uint32_t* side_cnt = nullptr;
@@ -302,6 +304,18 @@ struct Ctx {
   std::vector<double> hist;
   std::vector<int32_t> inner;  // [outer][nsub]
   double fnorm2 = 0;
+
+  // Two-stream PCG: the local subdomains split into two groups whose chunk graphs run on their own
+  // streams, so one group's kernels fill the other's wave tails (iterations are unchanged: every
+  // subdomain's arithmetic is the same).  grp_cur selects the group a launcher works on (-1: all).
+  static constexpr int kMaxGroups = 8;
+  int ngroups = 1;
+  int grp_cur = -1;
+  cudaStream_t gstream[kMaxGroups] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
+  cudaGraphExec_t cg_graph_g[kMaxGroups] = {};
+  int64_t g_blk0[kMaxGroups] = {}, g_nblk[kMaxGroups] = {}, g_vb0[kMaxGroups] = {}, g_nvb[kMaxGroups] = {};
+  int want_groups = 4;  // OSM_GROUPS = 1, 2, 4 or 8 (capped by the local subdomain count)
 
   // CUDA graph of one chunk of PCG iterations (spmv, update, dir) x kCgChunk, with PDL edges
   cudaGraphExec_t cg_graph = nullptr;

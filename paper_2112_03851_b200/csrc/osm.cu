@@ -92,6 +92,10 @@ static void timers_collect(Ctx& c) {
 static void drop_graph(Ctx& c) {
   if (c.cg_graph) cudaGraphExecDestroy(c.cg_graph);
   c.cg_graph = nullptr;
+  for (auto& g : c.cg_graph_g) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
 }
 
 static void free_assembly(Ctx& c) {
@@ -149,6 +153,7 @@ static void free_assembly(Ctx& c) {
   dfree(c.wif_all);
   dfree(c.d_sides);
   dfree(c.part);
+  dfree(c.part_upd);
   dfree(c.side_part);
   dfree(c.side_sum);
   dfree(c.side_cnt);
@@ -598,6 +603,7 @@ static void assemble(Ctx& c) {
 
   // --- reductions and device side table
   c.part = dalloc<double>(3 * c.nblk_total);
+  c.part_upd = dalloc<double>(2 * std::max<int64_t>(1, c.nvblk_total));
   c.side_nblk = std::max<int64_t>(1, ceil_div(nG, 256));
   c.side_part = dalloc<double>(std::max(1, nsides) * c.side_nblk);
   c.side_sum = dalloc<double>(std::max(1, nsides));
@@ -616,6 +622,16 @@ static void assemble(Ctx& c) {
     hst[ls].nvblk = (int32_t)ceil_div(c.subs[ls].nblk, kVecTiles);
   }
   OSM_CUDA(cudaMemcpyAsync(c.st, hst.data(), sizeof(SubState) * nloc, cudaMemcpyHostToDevice, c.stream));
+  // two subdomain groups for the two-stream PCG (halves of the local subdomains, in block order)
+  c.ngroups = 1;
+  while (c.ngroups * 2 <= std::min(c.want_groups, nloc)) c.ngroups *= 2;
+  for (int g = 0; g < c.ngroups; ++g) {  // group g = local subdomains [g nloc / G, (g + 1) nloc / G)
+    const int s0 = g * nloc / c.ngroups, s1 = (g + 1) * nloc / c.ngroups;
+    c.g_blk0[g] = c.subs[s0].blk0;
+    c.g_nblk[g] = (s1 < nloc ? c.subs[s1].blk0 : c.nblk_total) - c.subs[s0].blk0;
+    c.g_vb0[g] = hst[s0].vblk0;
+    c.g_nvb[g] = (s1 < nloc ? hst[s1].vblk0 : c.nvblk_total) - hst[s0].vblk0;
+  }
   if (c.h_st) cudaFreeHost(c.h_st);
   OSM_CUDA(cudaMallocHost((void**)&c.h_st, sizeof(SubState) * std::max(1, nloc)));
   if (c.h_side_sum) cudaFreeHost(c.h_side_sum);
@@ -790,7 +806,47 @@ static constexpr int kCgChunk = 8;  // PCG iterations per enqueued chunk
 
 // One chunk of kCgChunk batched PCG iterations: replayed from a CUDA graph (kernels
 // chained by programmatic dependent launch) unless per-launch timing is on.
+// One chunk of kCgChunk PCG iterations of group g on its stream, from a captured graph.
+static void enqueue_group_chunk(Ctx& c, int g, double tol, int maxit) {
+  if (!c.cg_graph_g[g] || c.graph_tol != tol || c.graph_maxit != maxit) {
+    if (c.cg_graph_g[g]) cudaGraphExecDestroy(c.cg_graph_g[g]);
+    c.cg_graph_g[g] = nullptr;
+    const int64_t l0 = c.launches;
+    cudaGraph_t gr = nullptr;
+    c.grp_cur = g;
+    OSM_CUDA(cudaStreamBeginCapture(c.gstream[g], cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int it = 0; it < kCgChunk; ++it) {
+        launch_cg_spmv(c);
+        launch_cg_update(c, tol, maxit);
+        launch_cg_dir(c);
+      }
+    } catch (...) {
+      c.grp_cur = -1;
+      cudaStreamEndCapture(c.gstream[g], &gr);
+      if (gr) cudaGraphDestroy(gr);
+      throw;
+    }
+    c.grp_cur = -1;
+    OSM_CUDA(cudaStreamEndCapture(c.gstream[g], &gr));
+    const cudaError_t e = cudaGraphInstantiate(&c.cg_graph_g[g], gr, 0);
+    cudaGraphDestroy(gr);
+    c.launches = l0;
+    if (e != cudaSuccess) fail(OSM_ERR_CUDA, "graph instantiation failed");
+  }
+  OSM_CUDA(cudaGraphLaunch(c.cg_graph_g[g], c.gstream[g]));
+  c.launches += 3 * kCgChunk;
+}
+
+static bool group_streams(const Ctx& c) { return c.ngroups > 1 && !c.timing && c.use_graph; }
+
 static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
+  if (group_streams(c)) {
+    for (int g = 0; g < c.ngroups; ++g) enqueue_group_chunk(c, g, tol, maxit);
+    c.graph_tol = tol;
+    c.graph_maxit = maxit;
+    return;
+  }
   if (c.timing || !c.use_graph) {
     for (int it = 0; it < kCgChunk; ++it) {
       launch_cg_spmv(c);
@@ -866,18 +922,32 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     OSM_CUDA(cudaStreamSynchronize(c.stream));
     if (c.h_nactive[0] > 0) {
       NvtxRange nv_pcg("batched_pcg");
-      // batched masked PCG: enqueue chunks; poll the active count one chunk behind
-      for (int ch = 0;; ++ch) {
+      // batched masked PCG: enqueue chunks; poll the active count one chunk behind.  With subdomain
+      // groups, the group streams fork from the library stream; group 0's stream joins the others
+      // after every chunk (the active count covers all) and the library stream joins at the end.
+      const bool grp = group_streams(c);
+      cudaStream_t ps = c.stream;
+      if (grp) {
+        OSM_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        for (int g = 0; g < c.ngroups; ++g) OSM_CUDA(cudaStreamWaitEvent(c.gstream[g], c.ev_fork, 0));
+        ps = c.gstream[0];
+      }
+      int ch = 0;
+      for (;; ++ch) {
         enqueue_cg_chunk(c, o.tol_inner, o.max_inner);
-        OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[ch & 1], c.d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                 c.stream));
-        OSM_CUDA(cudaEventRecord(c.ev_chunk[ch & 1], c.stream));
+        for (int g = 1; grp && g < c.ngroups; ++g) {
+          OSM_CUDA(cudaEventRecord(c.ev_join[g], c.gstream[g]));
+          OSM_CUDA(cudaStreamWaitEvent(ps, c.ev_join[g], 0));
+        }
+        OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[ch & 1], c.d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, ps));
+        OSM_CUDA(cudaEventRecord(c.ev_chunk[ch & 1], ps));
         if (ch > 0) {
           OSM_CUDA(cudaEventSynchronize(c.ev_chunk[(ch - 1) & 1]));
           if (c.h_nactive[(ch - 1) & 1] == 0) break;
         }
         if ((int64_t)ch * kCgChunk > (int64_t)o.max_inner + 2 * kCgChunk) break;  // safety net
       }
+      if (grp) OSM_CUDA(cudaStreamWaitEvent(c.stream, c.ev_chunk[ch & 1], 0));
     }
     {
       NvtxRange nv_x("trace_exchange");
@@ -1028,6 +1098,10 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     c.d_nactive = dalloc<int32_t>(1);
     OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[0], cudaEventDisableTiming));
     OSM_CUDA(cudaEventCreateWithFlags(&c.ev_chunk[1], cudaEventDisableTiming));
+    OSM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    for (auto& e : c.ev_join) OSM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& gs : c.gstream) OSM_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+    if (const char* e = std::getenv("OSM_GROUPS")) c.want_groups = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
     if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);
@@ -1073,6 +1147,11 @@ void osm_destroy(osm_ctx* h) {
   if (c.h_side_sum) cudaFreeHost(c.h_side_sum);
   for (auto& e : c.ev_chunk)
     if (e) cudaEventDestroy(e);
+  if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  for (auto& e : c.ev_join)
+    if (e) cudaEventDestroy(e);
+  for (auto& gs : c.gstream)
+    if (gs) cudaStreamDestroy(gs);
   for (auto& t : c.timers)
     for (auto& e : t.ev) cudaEventDestroy(e);
   if (c.comm) ncclCommDestroy(c.comm);

@@ -397,12 +397,12 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
                                                       SubState* __restrict__ st, const double* __restrict__ p,
                                                       double* __restrict__ q, double* __restrict__ part,
                                                       int64_t stride, int32_t* __restrict__ nactive,
-                                                      const __grid_constant__ MfArg<V> mf) {
+                                                      const __grid_constant__ MfArg<V> mf, int64_t blk_base) {
   constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
   __shared__ double sm[NW * 1];
   extern __shared__ __align__(128) unsigned char dsm[];
   pdl_enter();
-  const int64_t blk = blockIdx.x;
+  const int64_t blk = blockIdx.x + blk_base;
   const int ls = blk_sub[blk];
   if (!st[ls].active) return;
   const bool has_row = threadIdx.x < kRowsPerBlock;
@@ -454,11 +454,11 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
                                                            const double* __restrict__ dinv, double* __restrict__ part,
                                                            int64_t stride, double tol, int maxit,
                                                            int32_t* __restrict__ nactive, const uint8_t* __restrict__ mcode,
-                                                           const __grid_constant__ MfArg<V> mf) {
+                                                           const __grid_constant__ MfArg<V> mf, int64_t vb_base) {
   constexpr bool MF = V == 5;
   __shared__ double sm[(kVecThreads / 32) * 2];
   pdl_enter();
-  const int64_t vb = blockIdx.x;
+  const int64_t vb = blockIdx.x + vb_base;
   const int ls = vblk_sub[vb];
   if (!st[ls].active) return;
   const int nt = vblk_ntile[vb];
@@ -538,10 +538,10 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restric
                                                         const SubState* __restrict__ st, const double* __restrict__ r,
                                                         const double* __restrict__ dinv, double* __restrict__ p,
                                                         const uint8_t* __restrict__ mcode,
-                                                        const __grid_constant__ MfArg<V> mf) {
+                                                        const __grid_constant__ MfArg<V> mf, int64_t vb_base) {
   constexpr bool MF = V == 5;
   pdl_enter();
-  const int64_t vb = blockIdx.x;
+  const int64_t vb = blockIdx.x + vb_base;
   const int ls = vblk_sub[vb];
   if (!st[ls].active) return;
   const int nt = vblk_ntile[vb];
@@ -836,6 +836,13 @@ void launch_zero_if(Ctx& c) {
   ++c.launches;
 }
 
+// Stream and block ranges of the group being launched (Ctx::grp_cur; -1: every local subdomain).
+static cudaStream_t launch_stream(const Ctx& c) { return c.grp_cur >= 0 ? c.gstream[c.grp_cur] : c.stream; }
+static int64_t grp_blk0(const Ctx& c) { return c.grp_cur >= 0 ? c.g_blk0[c.grp_cur] : 0; }
+static int64_t grp_nblk(const Ctx& c) { return c.grp_cur >= 0 ? c.g_nblk[c.grp_cur] : c.nblk_total; }
+static int64_t grp_vb0(const Ctx& c) { return c.grp_cur >= 0 ? c.g_vb0[c.grp_cur] : 0; }
+static int64_t grp_nvb(const Ctx& c) { return c.grp_cur >= 0 ? c.g_nvb[c.grp_cur] : c.nvblk_total; }
+
 template <typename... KArgs, typename... Args>
 static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
                        Args... args) {
@@ -843,7 +850,7 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = c.stream;
+  cfg.stream = launch_stream(c);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -854,9 +861,9 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
 
 template <int V>
 static void cg_spmv_v(Ctx& c) {
-  launch_pdl(c, k_cg_spmv<V>, (unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
+  launch_pdl(c, k_cg_spmv<V>, (unsigned)grp_nblk(c), V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
              sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
-             c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c));
+             c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c), grp_blk0(c));
 }
 
 void launch_cg_spmv(Ctx& c) {
@@ -883,10 +890,10 @@ static bool mf_vectors(const Ctx& c) {
 
 template <int MINB, int V>
 static void cg_update_v(Ctx& c, double tol, int maxit) {
-  launch_pdl(c, k_cg_update<MINB, V>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+  launch_pdl(c, k_cg_update<MINB, V>, (unsigned)grp_nvb(c), kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
              (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
-             (const double*)c.q, (const double*)c.dinv, c.part, c.nvblk_total, tol, maxit, c.d_nactive,
-             (const uint8_t*)c.d_mf_code, mf_arg<V>(c));
+             (const double*)c.q, (const double*)c.dinv, c.part_upd, c.nvblk_total, tol, maxit, c.d_nactive,
+             (const uint8_t*)c.d_mf_code, mf_arg<V>(c), grp_vb0(c));
 }
 
 void launch_cg_update(Ctx& c, double tol, int maxit) {
@@ -903,9 +910,9 @@ void launch_cg_update(Ctx& c, double tol, int maxit) {
 
 template <int V>
 static void cg_dir_v(Ctx& c) {
-  launch_pdl(c, k_cg_dir<V>, (unsigned)c.nvblk_total, kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
+  launch_pdl(c, k_cg_dir<V>, (unsigned)grp_nvb(c), kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
              (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, (const SubState*)c.st, (const double*)c.r,
-             (const double*)c.dinv, c.p, (const uint8_t*)c.d_mf_code, mf_arg<V>(c));
+             (const double*)c.dinv, c.p, (const uint8_t*)c.d_mf_code, mf_arg<V>(c), grp_vb0(c));
 }
 
 void launch_cg_dir(Ctx& c) {

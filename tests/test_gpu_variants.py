@@ -78,3 +78,30 @@ def test_value_indexed_nonuniform_interface_coefficients():
         hs.append(o.history())
         o.close()
     assert np.array_equal(hs[0], hs[1])
+
+
+@pytest.mark.parametrize("groups", ["1", "2", "8"])
+def test_subdomain_group_streams_bitwise(groups):
+    """The PCG chunks of subdomain groups run on separate streams (default 4 groups); every group
+    count gives bitwise the same iterations as one stream."""
+    import paper_2112_03851_b200 as P
+
+    cfg = dict(synth.CONFIGS["C3"])
+    drho = synth.density(cfg)
+    out = []
+    for g in ("4", groups):
+        old = os.environ.get("OSM_GROUPS")
+        os.environ["OSM_GROUPS"] = g
+        try:
+            o = P.setup(cfg, drho)
+        finally:
+            if old is None:
+                del os.environ["OSM_GROUPS"]
+            else:
+                os.environ["OSM_GROUPS"] = old
+        st, rep = o.solve(tol_outer=1e-8, max_outer=100)
+        assert st == 0
+        out.append((o.history(), o.inner_iters(), o.solution()))
+        o.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)

@@ -310,6 +310,15 @@ def main():
                 "limiter": "L1/TEX gather path and issue, not HBM (ncu: l1tex 59% of peak, issue 51%, dram 48%; "
                            "profiles/r01g_ncu_summary.md)"}
 
+    # Whole PCG hot loop against the HBM roofline: algorithmic bytes of the three CG kernels (SpMV in
+    # its own format + update + direction) of one solve, over the timed step (everything included).
+    cg_bytes = (traffic["spmv_bytes"] + traffic["update_bytes"] + traffic["dir_bytes"]) / max(1, args.timing_steps)
+    cg_gbs = cg_bytes / (ms_step / 1e3) / 1e9
+    cg_roofline = {"bound": "hbm", "achieved": cg_gbs, "peak": peak, "unit": "GB/s", "frac": cg_gbs / peak,
+                   "bytes_per_step": cg_bytes,
+                   "note": "algorithmic bytes of k_cg_spmv + k_cg_update + k_cg_dir per solve / ms_per_step "
+                           "(the step also holds the outer-iteration kernels and host polling)"}
+
     # SURVEY 8(f) NEXT-4, reported separately: the matrix-free Kuhn-stencil SpMV (variant 5, row
     # order 4) on the same workload, timed the same way (it deviates from the paper's CSR)
     matrix_free = None
@@ -357,7 +366,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
-            "roofline": roofline, "roofline_fp64_sell": roofline_fp64, "matrix_free": matrix_free,
+            "roofline": roofline, "roofline_cg_step": cg_roofline, "roofline_fp64_sell": roofline_fp64,
+            "matrix_free": matrix_free,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)

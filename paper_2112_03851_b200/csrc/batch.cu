@@ -84,7 +84,10 @@ struct BatchBuf {
   uint32_t* cnt = nullptr;
   int32_t* nact = nullptr;      // per local subdomain: active candidates (CG)
   int32_t* d_nactive = nullptr; // total active (s, b)
-  double* part = nullptr;       // [nblk][3][KB]
+  double* part = nullptr;       // [nblk][3][KB] (SpMM kernels)
+  double* part_v = nullptr;     // [nblk][2][KB] (vector kernel; separate so subdomain groups overlap)
+  std::vector<int64_t> sblk0_h; // first block of each local subdomain
+  int64_t nblk_h = 0;
   double* side_sum = nullptr;   // [nsides][KB]
   std::vector<int64_t> rc0;     // contract row offset of each local subdomain
   // results
@@ -160,11 +163,12 @@ __global__ void __launch_bounds__(kBT, 3) kb_spmm(BatchDev D, BState* __restrict
                                                const int32_t* __restrict__ sub_nblk, const double* __restrict__ X,
                                                double* __restrict__ Y, double* __restrict__ R, double* __restrict__ P,
                                                const double* __restrict__ lam, double* __restrict__ wif,
-                                               double* __restrict__ part, double tol, int32_t* __restrict__ nactive) {
+                                               double* __restrict__ part, double tol, int32_t* __restrict__ nactive,
+                                               int64_t blk_base = 0) {
   constexpr int NP = MODE == MODE_WARM ? 3 : 1;
   __shared__ double wsum[kBT / 32][NP][KB];
   __shared__ double sm[NP * KB];
-  const int64_t blk = blockIdx.x;
+  const int64_t blk = blockIdx.x + blk_base;
   const int ls = D.blk_sub[blk];
   if (MODE == MODE_CG && nact[ls] == 0) return;
   // One warp per row, split in two half-warps h = lane / 16: half h takes the row's nonzeros
@@ -389,10 +393,10 @@ __global__ void __launch_bounds__(kBT) kb_vec(BatchDev D, BState* __restrict__ s
                                               const int32_t* __restrict__ sub_nblk, double* __restrict__ x,
                                               double* __restrict__ r, double* __restrict__ p,
                                               const double* __restrict__ q, double* __restrict__ part, double tol,
-                                              int maxit, int32_t* __restrict__ nactive) {
+                                              int maxit, int32_t* __restrict__ nactive, int64_t blk_base) {
   __shared__ double red[kBT / KB][2][KB];
   __shared__ double sm[2 * KB];
-  const int64_t blk = blockIdx.x;
+  const int64_t blk = blockIdx.x + blk_base;
   const int ls = D.blk_sub[blk];
   if (nact[ls] == 0) return;
   const int b = threadIdx.x % KB, rg = threadIdx.x / KB;
@@ -580,7 +584,7 @@ void batch_free(Ctx& c) {
   void* ptrs[] = {B->rowptr, B->col, B->val, B->dkn, B->b, B->islot, B->blk_sub, B->blk_nrow, B->blk_row0, B->mapg, B->mcolg,
                   B->mdiag, B->sdiag, B->q_own, B->q_sum, B->alpha_own, B->alpha_sum, B->side_which, B->side_partner, B->cand_active, B->x, B->r,
                   B->p, B->q, B->ut, B->lam, B->unbr, B->wif, B->out, B->st, B->cnt, B->nact, B->d_nactive,
-                  B->part, B->side_sum};
+                  B->part, B->part_v, B->side_sum};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete B;
@@ -712,6 +716,9 @@ static void batch_setup(Ctx& c) {
   B->nact = balloc<int32_t>(nloc);
   B->d_nactive = balloc<int32_t>(1);
   B->part = balloc<double>(B->nblk * 3 * kBmax);
+  B->part_v = balloc<double>(B->nblk * 2 * kBmax);
+  B->sblk0_h = sblk0;
+  B->nblk_h = B->nblk;
   B->side_sum = balloc<double>(std::max(1, nsides) * kBmax);
   for (double* v : {B->x, B->r, B->p, B->q, B->ut}) OSM_CUDA(cudaMemsetAsync(v, 0, sizeof(double) * nv, c.stream));
   OSM_CUDA(cudaMemsetAsync(B->cnt, 0, sizeof(uint32_t) * nloc, c.stream));
@@ -843,27 +850,47 @@ static osm_status solve_batch_kb(Ctx& c, int nB, const double* pq, const osm_sol
     OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[0], B->d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
     OSM_CUDA(cudaStreamSynchronize(c.stream));
     if (c.h_nactive[0] > 0) {
-      for (int ch = 0;; ++ch) {
-        for (int it = 0; it < kChunk; ++it) {
-          kb_spmm<MODE_CG, KB><<<nblk, kBT, 0, c.stream>>>(D, B->st, B->cnt, B->nact, c.batch_sub_blk0, c.batch_sub_nblk,
-                                                       B->p, B->q, nullptr, nullptr, nullptr, nullptr, B->part,
-                                                       o.tol_inner, B->d_nactive);
-          kb_vec<0, KB><<<nblk, kBT, 0, c.stream>>>(D, B->st, B->cnt, B->nact, c.batch_sub_blk0, c.batch_sub_nblk, B->x,
-                                                B->r, B->p, B->q, B->part, o.tol_inner, o.max_inner, B->d_nactive);
-          kb_vec<1, KB><<<nblk, kBT, 0, c.stream>>>(D, B->st, B->cnt, B->nact, c.batch_sub_blk0, c.batch_sub_nblk, B->x,
-                                                B->r, B->p, B->q, B->part, o.tol_inner, o.max_inner, B->d_nactive);
+      // subdomain groups on the library's group streams (as osm_solve): one group's kernels fill the
+      // others' wave tails; the first group's stream joins the rest after every chunk
+      const int G = std::min(std::min(c.want_groups, nloc), Ctx::kMaxGroups);
+      cudaStream_t ps = c.stream;
+      if (G > 1) {
+        OSM_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        for (int g = 0; g < G; ++g) OSM_CUDA(cudaStreamWaitEvent(c.gstream[g], c.ev_fork, 0));
+        ps = c.gstream[0];
+      }
+      int ch = 0;
+      for (;; ++ch) {
+        for (int g = 0; g < G; ++g) {
+          const int s0 = g * nloc / G, s1 = (g + 1) * nloc / G;
+          const int64_t b0 = B->sblk0_h[s0], b1 = s1 < nloc ? B->sblk0_h[s1] : B->nblk_h;
+          const unsigned gb = (unsigned)(b1 - b0);
+          cudaStream_t gs = G > 1 ? c.gstream[g] : c.stream;
+          for (int it = 0; it < kChunk; ++it) {
+            kb_spmm<MODE_CG, KB><<<gb, kBT, 0, gs>>>(D, B->st, B->cnt, B->nact, c.batch_sub_blk0, c.batch_sub_nblk,
+                                                     B->p, B->q, nullptr, nullptr, nullptr, nullptr, B->part,
+                                                     o.tol_inner, B->d_nactive, b0);
+            kb_vec<0, KB><<<gb, kBT, 0, gs>>>(D, B->st, B->cnt, B->nact, c.batch_sub_blk0, c.batch_sub_nblk, B->x,
+                                              B->r, B->p, B->q, B->part_v, o.tol_inner, o.max_inner, B->d_nactive, b0);
+            kb_vec<1, KB><<<gb, kBT, 0, gs>>>(D, B->st, B->cnt, B->nact, c.batch_sub_blk0, c.batch_sub_nblk, B->x,
+                                              B->r, B->p, B->q, B->part_v, o.tol_inner, o.max_inner, B->d_nactive, b0);
+          }
+          if (G > 1 && g > 0) {
+            OSM_CUDA(cudaEventRecord(c.ev_join[g], gs));
+            OSM_CUDA(cudaStreamWaitEvent(ps, c.ev_join[g], 0));
+          }
         }
         OSM_CHECK_LAUNCH();
-        c.launches += 3 * kChunk;
-        OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[ch & 1], B->d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                 c.stream));
-        OSM_CUDA(cudaEventRecord(c.ev_chunk[ch & 1], c.stream));
+        c.launches += 3 * kChunk * G;
+        OSM_CUDA(cudaMemcpyAsync(&c.h_nactive[ch & 1], B->d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, ps));
+        OSM_CUDA(cudaEventRecord(c.ev_chunk[ch & 1], ps));
         if (ch > 0) {
           OSM_CUDA(cudaEventSynchronize(c.ev_chunk[(ch - 1) & 1]));
           if (c.h_nactive[(ch - 1) & 1] == 0) break;
         }
         if ((int64_t)ch * kChunk > (int64_t)o.max_inner + 2 * kChunk) break;
       }
+      if (G > 1) OSM_CUDA(cudaStreamWaitEvent(c.stream, c.ev_chunk[ch & 1], 0));
     }
     if (nsides) {
       kb_trace<KB><<<gI, 256, 0, c.stream>>>(D, B->x, B->lam, B->out);

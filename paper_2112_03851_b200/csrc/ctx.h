@@ -315,6 +315,8 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
   cudaGraphExec_t cg_graph_g[kMaxGroups] = {};
   int64_t g_blk0[kMaxGroups] = {}, g_nblk[kMaxGroups] = {}, g_vb0[kMaxGroups] = {}, g_nvb[kMaxGroups] = {};
+  int vec_tiles = kVecTiles;  // tiles per vector block (update/dir kernels), chosen at assembly
+  int vt_override = 0;         // OSM_VT
   int want_groups = 4;  // OSM_GROUPS = 1, 2, 4 or 8 (capped by the local subdomain count)
 
   // CUDA graph of one chunk of PCG iterations (spmv, update, dir) x kCgChunk, with PDL edges

@@ -510,14 +510,17 @@ static void assemble(Ctx& c) {
   for (int ls = 0; ls < nloc; ++ls)
     for (int64_t k = 0; k < c.subs[ls].nblk; ++k) blk_sub[c.subs[ls].blk0 + k] = ls;
   c.blk_sub = dupload(c, blk_sub);
+  // tiles per vector block: 4 (8 rows per thread) measured best even for one C3 slab per GPU
+  // (tools/slab_probe.py: 23.9 / 24.5 / 26.5 us per PCG iteration with 4 / 2 / 1); OSM_VT overrides
+  c.vec_tiles = c.vt_override > 0 ? std::min(kVecTiles, c.vt_override) : kVecTiles;
   {
     std::vector<int32_t> vs, vt, vn;
     for (int ls = 0; ls < nloc; ++ls) {
       Sub& S = c.subs[ls];
-      for (int64_t t = 0; t < S.nblk; t += kVecTiles) {
+      for (int64_t t = 0; t < S.nblk; t += c.vec_tiles) {
         vs.push_back(ls);
         vt.push_back((int32_t)(S.blk0 + t));
-        vn.push_back((int32_t)std::min<int64_t>(kVecTiles, S.nblk - t));
+        vn.push_back((int32_t)std::min<int64_t>(c.vec_tiles, S.nblk - t));
       }
     }
     c.nvblk_total = (int64_t)vs.size();
@@ -617,9 +620,9 @@ static void assemble(Ctx& c) {
     hst[ls].blk0 = c.subs[ls].blk0;
     hst[ls].nblk = (int32_t)c.subs[ls].nblk;
     int64_t v0 = 0;
-    for (int j = 0; j < ls; ++j) v0 += ceil_div(c.subs[j].nblk, kVecTiles);
+    for (int j = 0; j < ls; ++j) v0 += ceil_div(c.subs[j].nblk, c.vec_tiles);
     hst[ls].vblk0 = v0;
-    hst[ls].nvblk = (int32_t)ceil_div(c.subs[ls].nblk, kVecTiles);
+    hst[ls].nvblk = (int32_t)ceil_div(c.subs[ls].nblk, c.vec_tiles);
   }
   OSM_CUDA(cudaMemcpyAsync(c.st, hst.data(), sizeof(SubState) * nloc, cudaMemcpyHostToDevice, c.stream));
   // two subdomain groups for the two-stream PCG (halves of the local subdomains, in block order)
@@ -1102,6 +1105,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     for (auto& e : c.ev_join) OSM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& gs : c.gstream) OSM_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
     if (const char* e = std::getenv("OSM_GROUPS")) c.want_groups = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("OSM_VT")) c.vt_override = std::atoi(e);
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
     if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);

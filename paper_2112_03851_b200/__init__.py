@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libosm.so")
+LIB_PATH = os.environ.get("OSM_LIB") or os.path.join(_HERE, "libosm.so")  # OSM_LIB: experiment builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libosm.so not built ({LIB_PATH}); run `python paper_2112_03851_b200/build.py`")

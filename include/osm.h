@@ -272,6 +272,7 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * column offset); 4 = 3 with the dictionary in shared memory; 6 = 3 with the dictionary in the
  * constant bank as a kernel parameter (default, up to 2048 distinct values); 7 = 6 on wide
  * entries (12-bit index, 20-bit offset), selected automatically when offsets exceed int16;
+ * 8 = 5 with each tile's x window staged in shared memory by bulk copies (experimental, slower);
  * 5 matrix-free Kuhn
  * stencil (the K_s values are uniform per parity class and row kind on the
  * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row

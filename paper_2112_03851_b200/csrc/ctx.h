@@ -117,6 +117,10 @@ struct MfArg<5> {
 // shared memory (variant 4).
 constexpr int kCDict = 2048;
 template <>
+struct MfArg<8> {  // variant 5 with the x window staged in shared memory: delta[] holds window offsets
+  MfConst c;
+};
+template <>
 struct MfArg<6> {
   double dict[kCDict];
 };
@@ -140,6 +144,11 @@ struct SellDev {
   const int32_t* mf_begin;  // table t = entries [mf_begin[t], mf_begin[t+1]), padded to a multiple of 4
   const int4* mf_delta;     // 4 row offsets per group
   const double* mf_val;     // values (exact copies of the assembled, Robin-folded SELL entries)
+  // variant 8: per deduplicated table tb, the merged x window [mf_win_begin[tb], mf_win_begin[tb+1]) as
+  // (first row offset a, rows len, shared-memory row base) triples
+  const int32_t* mf_win_begin;
+  const int3* mf_win;
+  int64_t nrows;            // rows of the concatenated vectors (bulk-copy bounds)
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -335,7 +344,8 @@ struct Ctx {
                          // in shared memory (default; falls back to 3, then 2, when it does not apply),
                          // 5: matrix-free Kuhn stencil (row order 4 only; else as 6), 6: 3 with the
                          // dictionary in the constant bank (default; else 3), 7: 6 on wide entries
-                         // (chosen automatically when offsets need 20 bits)
+                         // (chosen automatically when offsets need 20 bits), 8: 5 with the x window staged
+                         // in shared memory by bulk copies
 
   // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
   bool mf_ok = false;
@@ -347,6 +357,10 @@ struct Ctx {
   int64_t mf_entries = 0;         // including padding
   std::vector<int32_t> h_mf_begin, h_mf_delta;
   MfConst* h_mf_const = nullptr;  // host copy of the kernel-parameter tables (valid = 0: global tables)
+  MfConst* h_mf_win_const = nullptr;  // variant 8: the same tables with window offsets in delta[]
+  int32_t* d_mf_win_begin = nullptr;
+  int3* d_mf_win = nullptr;
+  int mf_win_rows = 0;            // largest window (rows) = shared memory of variant 8 / 8 B
   uint8_t* d_mf_code = nullptr;   // per internal row: deduplicated table id, 0xff dummy (vector kernels)
 
   // value-indexed SELL (vi.cu)

@@ -168,6 +168,11 @@ static void free_assembly(Ctx& c) {
   c.mf_entries = 0;
   delete c.h_mf_const;
   c.h_mf_const = nullptr;
+  delete c.h_mf_win_const;
+  c.h_mf_win_const = nullptr;
+  dfree(c.d_mf_win_begin);
+  dfree(c.d_mf_win);
+  c.mf_win_rows = 0;
   dfree(c.d_mf_code);
   c.assembled = false;
   c.density_set = false;
@@ -201,6 +206,50 @@ static void vi_sync_host_dict(Ctx& c) {
   if (c.vi_ok && c.vi_ndict > 0)
     OSM_CUDA(cudaMemcpy(c.h_vi_dict.data(), c.vi_dict, sizeof(double) * c.vi_ndict, cudaMemcpyDeviceToHost));
   drop_graph(c);
+}
+
+// Variant 8 windows: for every deduplicated table, the union over its entries e of the row ranges
+// [delta_e, delta_e + 256) of a 256-row tile, merged into intervals (16-byte aligned), laid out back
+// to back in shared memory; the table's delta_e are replaced by the shared-memory row of delta_e.
+static void mf_windows(Ctx& c, int ntab) {
+  dfree(c.d_mf_win_begin);
+  dfree(c.d_mf_win);
+  c.mf_win_rows = 0;
+  const MfConst& P = *c.h_mf_const;
+  if (!c.h_mf_win_const) c.h_mf_win_const = new MfConst();
+  MfConst& W = *c.h_mf_win_const;
+  W = P;
+  std::vector<int32_t> wbeg(1, 0);
+  std::vector<int3> win;
+  for (int tb = 0; tb < ntab; ++tb) {
+    const int e0 = 4 * P.gbeg[tb], e1 = 4 * P.gbeg[tb + 1];
+    std::vector<int> ds;
+    for (int e = e0; e < e1; ++e) ds.push_back((&P.delta[0].x)[e]);
+    std::sort(ds.begin(), ds.end());
+    std::vector<std::pair<int, int>> iv;  // merged [a, b)
+    for (int d : ds) {
+      const int a = d & ~1, b = (d + kRowsPerBlock + 1) & ~1;  // even bounds: 16-byte copies
+      if (!iv.empty() && a <= iv.back().second) iv.back().second = std::max(iv.back().second, b);
+      else iv.push_back({a, b});
+    }
+    int base = 0;
+    for (auto& ab : iv) {
+      win.push_back(make_int3(ab.first, ab.second - ab.first, base));
+      base += ab.second - ab.first;
+    }
+    c.mf_win_rows = std::max(c.mf_win_rows, base);
+    for (int e = e0; e < e1; ++e) {
+      const int d = (&P.delta[0].x)[e];
+      for (size_t i = 0; i < iv.size(); ++i)
+        if (d >= iv[i].first && d + kRowsPerBlock <= iv[i].second) {
+          (&W.delta[0].x)[e] = win[win.size() - iv.size() + i].z + (d - iv[i].first);
+          break;
+        }
+    }
+    wbeg.push_back((int32_t)win.size());
+  }
+  c.d_mf_win_begin = dupload(c, wbeg);
+  c.d_mf_win = dupload(c, win);
 }
 
 // Copy the table values from the (folded) SELL and verify the tables against every row.
@@ -254,6 +303,7 @@ static void mf_refresh(Ctx& c) {
     P.tabid[t] = (int16_t)it->second;  // t = (ls * 3 + kind) * ncls + class, as mf_table_of
   }
   P.valid = 1;
+  mf_windows(c, nt);
   // per-row table codes for the vector kernels (D^{-1} from the tables, dummy rows skipped)
   if (nt <= 255) {
     if (!c.d_mf_code) c.d_mf_code = dalloc<uint8_t>(c.nrows_total);
@@ -992,7 +1042,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   c.traffic[7] = c.exch_bytes;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
-  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5;
+  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5 || sv == 8;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1583,7 +1633,7 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 7) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..7");
+  if (v < 0 || v > 8) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..8");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);

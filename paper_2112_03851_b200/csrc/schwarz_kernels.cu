@@ -368,6 +368,82 @@ __device__ __forceinline__ double tile_row_mf(const SellDev& A, int64_t blk, con
   return s;
 }
 
+// Variant 8: variant 5 with the tile's x window staged in shared memory.  When all real rows of
+// the tile share one table (all but the tiles straddling a class or plane boundary), one thread
+// issues the bulk copies (cp.async.bulk, one per merged window interval, completing on an
+// mbarrier) and every gather becomes a shared-memory read at the entry's window offset; the FMA
+// chain is the same, so the iterations are still bitwise identical.  Straddling tiles use the
+// global-table gathers of variant 5.  Every thread of the block must call this (block barriers).
+__device__ __forceinline__ double tile_row_mf_win(const SellDev& A, int64_t blk, const double* __restrict__ x,
+                                                  const MfConst& P, unsigned char* smem) {
+  __shared__ uint64_t bar;
+  __shared__ int tlo, thi;
+  const int ls = A.blk_sub[blk];
+  const MfSub& M = A.mf_sub[ls];
+  const int64_t r0 = blk * kRowsPerBlock;
+  const int64_t ri = r0 + threadIdx.x;
+  const int t = mf_table_of(M, ri - M.row0);
+  if (threadIdx.x == 0) {
+    tlo = 0x7fffffff;
+    thi = -1;
+  }
+  __syncthreads();
+  if (t >= 0) {
+    atomicMin(&tlo, t);
+    atomicMax(&thi, t);
+  }
+  __syncthreads();
+  double s = 0.0;
+  if (thi < 0) return s;  // dummy rows only
+  if (tlo != thi) {       // straddling tile
+    if (t < 0) return s;
+    const double* xr = x + ri;
+    const double2* vv = reinterpret_cast<const double2*>(A.mf_val);
+    for (int g = A.mf_begin[t] >> 2; g < (A.mf_begin[t + 1] >> 2); ++g) {
+      const int4 d = A.mf_delta[g];
+      const double2 v01 = vv[2 * g], v23 = vv[2 * g + 1];
+      const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
+      s = fma(v01.x, x0, s);
+      s = fma(v01.y, x1, s);
+      s = fma(v23.x, x2, s);
+      s = fma(v23.y, x3, s);
+    }
+    return s;
+  }
+  const int tb = P.tabid[tlo];
+  double* xs = reinterpret_cast<double*>(smem);
+  if (threadIdx.x == 0) {
+    mbar_init_n(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int w0 = A.mf_win_begin[tb], w1 = A.mf_win_begin[tb + 1];
+    uint32_t bytes = 0;
+    for (int i = w0; i < w1; ++i) {
+      const int3 w = A.mf_win[i];
+      const int64_t lo = max(r0 + w.x, (int64_t)0), hi = min(r0 + w.x + w.y, A.nrows);
+      if (hi > lo) bytes += (uint32_t)(hi - lo) * 8u;
+    }
+    mbar_expect(&bar, bytes);
+    for (int i = w0; i < w1; ++i) {
+      const int3 w = A.mf_win[i];
+      const int64_t lo = max(r0 + w.x, (int64_t)0), hi = min(r0 + w.x + w.y, A.nrows);
+      if (hi > lo) bulk_g2s(xs + w.z + (lo - (r0 + w.x)), x + lo, (uint32_t)(hi - lo) * 8u, &bar);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (t < 0) return s;
+  const double* xt = xs + threadIdx.x;
+  for (int g = P.gbeg[tb]; g < P.gbeg[tb + 1]; ++g) {
+    const int4 d = P.delta[g];  // window offsets
+    const double x0 = xt[d.x], x1 = xt[d.y], x2 = xt[d.z], x3 = xt[d.w];
+    s = fma(P.val[4 * g], x0, s);
+    s = fma(P.val[4 * g + 1], x1, s);
+    s = fma(P.val[4 * g + 2], x2, s);
+    s = fma(P.val[4 * g + 3], x3, s);
+  }
+  return s;
+}
+
 // V = 0: LDG rows; V = 2: LDG rows with registers capped at 32 (8 blocks / 64 warps per SM);
 // V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers);
 // V = 4: value-indexed rows, dictionary in shared memory; V = 5: matrix-free Kuhn stencil.
@@ -377,6 +453,7 @@ __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const 
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
   if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c);
+  if constexpr (V == 8) return tile_row_mf_win(A, blk, x, mf.c, smem);
   if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict);
   if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict);
   if constexpr (V == 4) {
@@ -759,13 +836,21 @@ SellDev sell_of(const Ctx& c) {
   return SellDev{c.sell_val,  c.sell_col,   c.sell_soff,  c.sell_swidth,
                  c.vi_packed, c.vi_poff,     c.vi_dict,    (int)c.vi_ndict,
                  c.blk_sub,   c.d_mf_sub,    c.d_mf_begin, reinterpret_cast<const int4*>(c.d_mf_delta),
-                 c.d_mf_val};
+                 c.d_mf_val,  c.d_mf_win_begin, c.d_mf_win, c.nrows_total};
 }
 
 }  // namespace
 
+constexpr int kMfWinSmemMax = 200 * 1024;  // variant 8 window (bytes); larger windows fall back to 5
+
 int spmv_variant_of(const Ctx& c) {
   int v = c.spmv_variant;
+  if (v == 8) {
+    if (c.mf_ok && c.h_mf_win_const && c.h_mf_win_const->valid && c.d_mf_win &&
+        c.mf_win_rows * 8 <= kMfWinSmemMax)
+      return 8;
+    v = 5;
+  }
   if (v == 5) {
     if (c.mf_ok) return 5;
     v = 6;
@@ -782,7 +867,14 @@ int spmv_variant_of(const Ctx& c) {
 
 static int spmv_smem(const Ctx& c) {
   const int v = spmv_variant_of(c);
+  if (v == 8) return 8 * c.mf_win_rows;
   return v == 1 ? kBulkSmem : (v == 4 ? (int)(sizeof(double) * c.vi_ndict) : 0);
+}
+
+// dynamic shared memory above the 48 KB default needs the per-kernel opt-in
+template <typename K>
+static void smem_optin(K kern, int bytes) {
+  if (bytes > 48 * 1024) OSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 void spmv_init_attributes() {
@@ -800,6 +892,9 @@ static MfArg<V> mf_arg(const Ctx& c) {
   if constexpr (V == 5) {
     if (c.h_mf_const) a.c = *c.h_mf_const;
   }
+  if constexpr (V == 8) {
+    if (c.h_mf_win_const) a.c = *c.h_mf_win_const;
+  }
   if constexpr (V == 6 || V == 7)
     std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.dict);
   return a;
@@ -808,6 +903,7 @@ static MfArg<V> mf_arg(const Ctx& c) {
 template <int V>
 static void warm_v(Ctx& c, double tol) {
   const unsigned thr = V == 1 ? kBulkThreads : kThreads;
+  if constexpr (V == 8) smem_optin(k_warm<8>, spmv_smem(c));
   k_warm<V><<<(unsigned)c.nblk_total, thr, spmv_smem(c), c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
                                                                       c.lam_all, c.dinv, c.r, c.p, c.part,
                                                                       c.nblk_total, tol, c.d_nactive, mf_arg<V>(c));
@@ -823,6 +919,7 @@ void launch_warm(Ctx& c, double tol, int) {
     case 5: warm_v<5>(c, tol); break;
     case 6: warm_v<6>(c, tol); break;
     case 7: warm_v<7>(c, tol); break;
+    case 8: warm_v<8>(c, tol); break;
     default: warm_v<4>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
@@ -861,6 +958,7 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
 
 template <int V>
 static void cg_spmv_v(Ctx& c) {
+  if constexpr (V == 8) smem_optin(k_cg_spmv<8>, spmv_smem(c));
   launch_pdl(c, k_cg_spmv<V>, (unsigned)grp_nblk(c), V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
              sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
              c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c), grp_blk0(c));
@@ -876,6 +974,7 @@ void launch_cg_spmv(Ctx& c) {
     case 5: cg_spmv_v<5>(c); break;
     case 6: cg_spmv_v<6>(c); break;
     case 7: cg_spmv_v<7>(c); break;
+    case 8: cg_spmv_v<8>(c); break;
     default: cg_spmv_v<4>(c); break;
   }
   ++c.launches;
@@ -885,7 +984,8 @@ void launch_cg_spmv(Ctx& c) {
 // The vector kernels take D^{-1} from the matrix-free tables (and skip pairs of dummy rows) when
 // variant 5 runs with its tables in the constant bank.
 static bool mf_vectors(const Ctx& c) {
-  return spmv_variant_of(c) == 5 && c.h_mf_const && c.h_mf_const->valid && c.d_mf_code;
+  const int v = spmv_variant_of(c);
+  return (v == 5 || v == 8) && c.h_mf_const && c.h_mf_const->valid && c.d_mf_code;
 }
 
 template <int MINB, int V>
@@ -950,6 +1050,7 @@ void launch_glue(Ctx& c, int zero) {
 
 template <int V>
 static void resid_v(Ctx& c) {
+  if constexpr (V == 8) smem_optin(k_resid<8>, spmv_smem(c));
   k_resid<V><<<(unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, spmv_smem(c), c.stream>>>(
       sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot, c.wif_all, c.part, c.nblk_total, mf_arg<V>(c));
 }
@@ -964,6 +1065,7 @@ void launch_resid(Ctx& c) {
     case 5: resid_v<5>(c); break;
     case 6: resid_v<6>(c); break;
     case 7: resid_v<7>(c); break;
+    case 8: resid_v<8>(c); break;
     default: resid_v<4>(c); break;
   }
   OSM_CHECK_LAUNCH();

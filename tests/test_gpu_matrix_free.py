@@ -50,7 +50,9 @@ def test_matrix_free_bitwise_equals_sell_and_meets_oracle(q):
     robin = _robin(10.0, q[0], 3.0, q[1], S - 1)
     mf = _solve(CFG, drho, robin, 5)
     ref = _solve(CFG, drho, robin, 2)
-    assert mf["active"] == 5 and ref["active"] == 2
+    win = _solve(CFG, drho, robin, 8)  # x window staged in shared memory by bulk copies
+    assert mf["active"] == 5 and ref["active"] == 2 and win["active"] == 8
+    assert np.array_equal(win["h"], ref["h"]) and np.array_equal(win["h2"], ref["h2"])
     assert mf["st"] == ref["st"] == 0 and mf["st2"] == 0
     assert np.array_equal(mf["h"], ref["h"])
     assert np.array_equal(mf["inner"], ref["inner"])

@@ -325,6 +325,12 @@ def main():
     if world == 1:
         matrix_free = run_matrix_free(P, args, cfg, d_drho, stream, peak, torch)
 
+    # C4 (BASELINE configs[3]), reported alongside: one batched-alpha evaluation of a CMA-ES population
+    # (lambda = 25) on the C2 problem, 30 outer iterations per candidate (the cost window)
+    batched = None
+    if world == 1:
+        batched = run_batched_alpha(P, stream, torch)
+
     # e2e through the C ABI with host buffers: pinned drho H2D + solve + Phi D2H, every step
     h_drho = torch.from_numpy(drho).pin_memory()
     phi = torch.empty(int(np.prod(osm.lattice)), dtype=torch.float64).pin_memory() if rank == 0 else None
@@ -367,7 +373,7 @@ def main():
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
             "roofline": roofline, "roofline_cg_step": cg_roofline, "roofline_fp64_sell": roofline_fp64,
-            "matrix_free": matrix_free,
+            "matrix_free": matrix_free, "batched_alpha": batched,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)
@@ -391,6 +397,33 @@ def exchange_block(kt, tm, world):
 
 _rows = {}
 HOT_VARIANT = 6  # library default SpMV: value-indexed SELL-256, dictionary in the constant bank
+
+
+def run_batched_alpha(P, stream, torch, B=25, N=30, reps=2):
+    """C4 workload: B candidate Robin parameters alpha_b = alpha0 exp(0.5 z_b) on C2 (synth), one batched
+    solve of N outer iterations each, device-timed (CUDA events on the library stream)."""
+    cfg = dict(synth.CONFIGS["C2"])
+    o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], stream=stream.cuda_stream)
+    o.decompose(cfg["nsub"])
+    o.set_robin(np.full(cfg["nsub"] - 1, cfg["alpha"]), np.full(cfg["nsub"] - 1, cfg["alpha"]))
+    o.assemble()
+    o.upload_density(synth.density(cfg))
+    al = np.repeat(synth.alpha_candidates(cfg["alpha"], B=B)[:, None], cfg["nsub"] - 1, axis=1)
+    o.solve_batch(al, al, tol_outer=1e-300, max_outer=2)  # warm-up (buffers, first launches)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(reps):
+        rep = o.solve_batch(al, al, tol_outer=1e-300, max_outer=N)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    s = ev0.elapsed_time(ev1) / 1e3 / reps
+    rows = sum(o.local_solution_size(k) for k in range(cfg["nsub"]))
+    o.close()
+    return {"workload": f"C4: {B} candidates x {N} outer iterations on C2 (P2 32^3, 2 subdomains)",
+            "seconds": s, "candidate_outer_iters_per_s": B * N / s,
+            "dof_cg_iter_per_s": rows / cfg["nsub"] * rep.inner_total / s,  # equal slabs: mean n_s x inner
+            "inner_total": rep.inner_total}
 
 
 def run_matrix_free(P, args, cfg, d_drho, stream, peak, torch):

@@ -306,6 +306,9 @@ def main():
                 "format": "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
                           "offset) + 16 B per row (p, q); dictionary in the constant bank (kernel parameter)",
                 "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
+                "frac_vs_spec_8000": achieved / SPEC_HBM_GBS if achieved else None,
+                "dram_gbs_from_ncu_traffic": (tr / (1e-3 * spmv_ms / max(1, spmv_launches)) / 1e9
+                                              if tr and spmv_ms > 0 else None),
                 "exchange": exchange_block(kt, tm, world),
                 "limiter": "L1/TEX gather path and issue, not HBM (ncu: l1tex 59% of peak, issue 51%, dram 48%; "
                            "profiles/r01g_ncu_summary.md)"}
@@ -315,6 +318,7 @@ def main():
     cg_bytes = (traffic["spmv_bytes"] + traffic["update_bytes"] + traffic["dir_bytes"]) / max(1, args.timing_steps)
     cg_gbs = cg_bytes / (ms_step / 1e3) / 1e9
     cg_roofline = {"bound": "hbm", "achieved": cg_gbs, "peak": peak, "unit": "GB/s", "frac": cg_gbs / peak,
+                   "frac_vs_spec_8000": cg_gbs / SPEC_HBM_GBS,
                    "bytes_per_step": cg_bytes,
                    "note": "algorithmic bytes of k_cg_spmv + k_cg_update + k_cg_dir per solve / ms_per_step "
                            "(the step also holds the outer-iteration kernels and host polling)"}
@@ -396,7 +400,8 @@ def exchange_block(kt, tm, world):
 
 
 _rows = {}
-HOT_VARIANT = 6  # library default SpMV: value-indexed SELL-256, dictionary in the constant bank
+HOT_VARIANT = 6
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e specification (SURVEY 8(d) reports against both)  # library default SpMV: value-indexed SELL-256, dictionary in the constant bank
 
 
 def run_batched_alpha(P, stream, torch, B=25, N=30, reps=2):

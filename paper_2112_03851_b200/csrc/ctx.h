@@ -326,6 +326,7 @@ struct Ctx {
   int64_t g_blk0[kMaxGroups] = {}, g_nblk[kMaxGroups] = {}, g_vb0[kMaxGroups] = {}, g_nvb[kMaxGroups] = {};
   int vec_tiles = kVecTiles;  // tiles per vector block (update/dir kernels), chosen at assembly
   int vt_override = 0;         // OSM_VT
+  bool groups_forced = false;  // OSM_GROUPS given: no size-based reduction
   int want_groups = 8;  // OSM_GROUPS = 1, 2, 4 or 8 (capped by the local subdomain count)
 
   // CUDA graph of one chunk of PCG iterations (spmv, update, dir) x kCgChunk, with PDL edges

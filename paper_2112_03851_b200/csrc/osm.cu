@@ -678,6 +678,12 @@ static void assemble(Ctx& c) {
   // two subdomain groups for the two-stream PCG (halves of the local subdomains, in block order)
   c.ngroups = 1;
   while (c.ngroups * 2 <= std::min(c.want_groups, nloc)) c.ngroups *= 2;
+  {  // groups only pay while a group's SpMV is a few waves (C3: ~1 wave); at C5 they thrash L2
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    const int64_t wave = 8LL * sms;  // SpMV blocks resident per wave
+    while (c.ngroups > 1 && c.nblk_total / c.ngroups > 8 * wave && !c.groups_forced) c.ngroups /= 2;
+  }
   for (int g = 0; g < c.ngroups; ++g) {  // group g = local subdomains [g nloc / G, (g + 1) nloc / G)
     const int s0 = g * nloc / c.ngroups, s1 = (g + 1) * nloc / c.ngroups;
     c.g_blk0[g] = c.subs[s0].blk0;
@@ -1154,7 +1160,10 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     OSM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     for (auto& e : c.ev_join) OSM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& gs : c.gstream) OSM_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
-    if (const char* e = std::getenv("OSM_GROUPS")) c.want_groups = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("OSM_GROUPS")) {
+      c.want_groups = std::max(1, std::atoi(e));
+      c.groups_forced = true;
+    }
     if (const char* e = std::getenv("OSM_VT")) c.vt_override = std::atoi(e);
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;

@@ -136,6 +136,7 @@ struct SellDev {
   const int32_t* twidth;
   const uint32_t* packed;  // value-indexed copy (variant 3): (dict index << 16) | (uint16)(col - row),
   const int64_t* poff;     //   4 entries of a row per uint4 (see vi.cu); per-tile word offsets
+  const int32_t* vtw;      //   per-tile packed widths (exact zeros dropped)
   const double* dict;      // distinct values
   int ndict;
   // matrix-free view (variant 5): kinds 0 interior, 1 left interface plane, 2 right interface plane
@@ -372,6 +373,8 @@ struct Ctx {
   double* vi_dict = nullptr;
   uint32_t* vi_packed = nullptr;
   int64_t* vi_poff = nullptr;
+  int32_t* vi_tw = nullptr;          // per tile: packed width (kept entries of the longest row)
+  std::vector<int64_t> vi_kept;      // per local subdomain: kept (nonzero-value) entries
   int64_t vi_words = 0;
   int64_t vi_ndict = 0, vi_nbase = 0;
   struct FoldTuple {

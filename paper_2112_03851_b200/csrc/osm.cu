@@ -287,13 +287,21 @@ static void mf_refresh(Ctx& c) {
     }
     auto it = seen.find(key);
     if (it == seen.end()) {
-      const int g = (c.h_mf_begin[t + 1] - c.h_mf_begin[t]) / 4;
-      if (nt >= kMfMaxTab || ng + g > kMfMaxGroups) return;  // too many: global tables
+      // the constant-bank copy keeps only the nonzero values (the Kuhn stencil's exact zeros add +-0
+      // to the row sums), in column order, padded to whole groups of 4 with (0, +0.0)
+      std::vector<int> keep;
       double diag = 0.0;
-      for (int e = c.h_mf_begin[t], k = 4 * ng; e < c.h_mf_begin[t + 1]; ++e, ++k) {
-        (&P.delta[0].x)[k] = c.h_mf_delta[e];
-        P.val[k] = val[e];
-        if (c.h_mf_delta[e] == 0 && val[e] != 0.0) diag = val[e];  // (0, +0.0) entries are padding
+      for (int e = c.h_mf_begin[t]; e < c.h_mf_begin[t + 1]; ++e) {
+        if (val[e] == 0.0) continue;
+        keep.push_back(e);
+        if (c.h_mf_delta[e] == 0) diag = val[e];
+      }
+      const int g = ((int)keep.size() + 3) / 4;
+      if (nt >= kMfMaxTab || ng + g > kMfMaxGroups) return;  // too many: global tables
+      for (int k = 0; k < 4 * g; ++k) {
+        const bool real = k < (int)keep.size();
+        (&P.delta[0].x)[4 * ng + k] = real ? c.h_mf_delta[keep[k]] : 0;
+        P.val[4 * ng + k] = real ? val[keep[k]] : 0.0;
       }
       P.dinv[nt] = diag > 0.0 ? 1.0 / diag : 0.0;
       ng += g;
@@ -1056,7 +1064,8 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     // SpMV bytes in the format launched: fp64 SELL 12 B/entry (+ CSR-equivalent 4 B/row),
     // value-indexed 4 B/entry (index + offset; the dictionary is on chip), or matrix-free 0 B/entry
     // (tables in the constant bank); vectors p, q 16 B/row
-    const double mat = mf ? 0.0 : (vi ? 4.0 * S.nnz : 12.0 * S.nnz + 4.0 * (S.n + 1));
+    const double kept = ls < (int)c.vi_kept.size() ? (double)c.vi_kept[ls] : (double)S.nnz;
+    const double mat = mf ? 0.0 : (vi ? 4.0 * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
     c.traffic[1] += (double)its * 56.0 * S.n;

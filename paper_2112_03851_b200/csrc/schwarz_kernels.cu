@@ -263,7 +263,7 @@ __device__ __forceinline__ uint4 ld_stream4(const uint32_t* p) {
 }
 __device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, const double* __restrict__ x) {
   constexpr int T = kRowsPerBlock;
-  const int ng = (A.twidth[blk] + 3) >> 2;
+  const int ng = (A.vtw[blk] + 3) >> 2;
   const uint32_t* gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
   const double* xr = x + blk * T + threadIdx.x;
   double s = 0.0;
@@ -290,7 +290,7 @@ template <bool W = false>  // W: wide entries (12-bit index << 20 | 20-bit signe
 __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk, const double* __restrict__ x,
                                                    const double* sdict) {
   constexpr int T = kRowsPerBlock;
-  const int ng = (A.twidth[blk] + 3) >> 2;
+  const int ng = (A.vtw[blk] + 3) >> 2;
   const uint32_t* gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
   const double* xr = x + blk * T + threadIdx.x;
   double s = 0.0;
@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(kThreads) k_iface_sum(const SideDev* __restric
 
 SellDev sell_of(const Ctx& c) {
   return SellDev{c.sell_val,  c.sell_col,   c.sell_soff,  c.sell_swidth,
-                 c.vi_packed, c.vi_poff,     c.vi_dict,    (int)c.vi_ndict,
+                 c.vi_packed, c.vi_poff,     c.vi_tw,      c.vi_dict,    (int)c.vi_ndict,
                  c.blk_sub,   c.d_mf_sub,    c.d_mf_begin, reinterpret_cast<const int4*>(c.d_mf_delta),
                  c.d_mf_val,  c.d_mf_win_begin, c.d_mf_win, c.nrows_total};
 }

@@ -62,8 +62,9 @@ __global__ void k_vi_maxoff(int64_t ntile, const int64_t* __restrict__ toff, con
 // the wide form (value index << 20) | (offset & 0xfffff) (12-bit index, 20-bit signed offset).
 template <bool W>
 __global__ void k_vi_pack(int64_t ntile, const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
-                          const int64_t* __restrict__ poff, const uint16_t* __restrict__ vidx,
-                          const int32_t* __restrict__ col, uint32_t zero_idx, uint32_t* __restrict__ packed) {
+                          const int32_t* __restrict__ vtw, const int64_t* __restrict__ poff,
+                          const uint16_t* __restrict__ vidx, const int32_t* __restrict__ col, uint32_t zero_idx,
+                          uint32_t* __restrict__ packed) {
   constexpr int IS = W ? 20 : 16;
   constexpr uint32_t OM = W ? 0xfffffu : 0xffffu;
   const int64_t t = blockIdx.x;
@@ -71,16 +72,36 @@ __global__ void k_vi_pack(int64_t ntile, const int64_t* __restrict__ toff, const
   const int r = threadIdx.x;
   const int64_t row = t * kRowsPerBlock + r;
   const int w = twidth[t];
-  const int w4 = (w + 3) & ~3;
+  const int w4 = (vtw[t] + 3) & ~3;
   const int64_t base = toff[t] + r;
-  for (int k = 0; k < w4; ++k) {
-    uint32_t e = zero_idx << IS;
-    if (k < w) {
-      const int64_t i = base + (int64_t)kRowsPerBlock * k;
-      e = ((uint32_t)vidx[i] << IS) | ((uint32_t)(int32_t)(col[i] - row) & OM);
-    }
-    packed[poff[t] + 4 * ((int64_t)kRowsPerBlock * (k >> 2) + r) + (k & 3)] = e;
+  int kk = 0;  // kept entries so far (the row's exact zeros and SELL padding are dropped, order kept)
+  for (int k = 0; k < w; ++k) {
+    const int64_t i = base + (int64_t)kRowsPerBlock * k;
+    if (vidx[i] == zero_idx) continue;
+    const uint32_t e = ((uint32_t)vidx[i] << IS) | ((uint32_t)(int32_t)(col[i] - row) & OM);
+    packed[poff[t] + 4 * ((int64_t)kRowsPerBlock * (kk >> 2) + r) + (kk & 3)] = e;
+    ++kk;
   }
+  for (; kk < w4; ++kk) packed[poff[t] + 4 * ((int64_t)kRowsPerBlock * (kk >> 2) + r) + (kk & 3)] = zero_idx << IS;
+}
+
+// Kept (nonzero-value) entries per row: per-tile maximum (the packed width) and per-subdomain totals.
+__global__ void k_vi_kept(int64_t ntile, const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
+                          const uint16_t* __restrict__ vidx, uint32_t zero_idx, const int32_t* __restrict__ blk_sub,
+                          int32_t* __restrict__ vtw, unsigned long long* __restrict__ kept_sub) {
+  __shared__ int wmax;
+  const int64_t t = blockIdx.x;
+  if (t >= ntile) return;
+  if (threadIdx.x == 0) wmax = 0;
+  __syncthreads();
+  const int w = twidth[t];
+  const int64_t base = toff[t] + threadIdx.x;
+  int kk = 0;
+  for (int k = 0; k < w; ++k) kk += vidx[base + (int64_t)kRowsPerBlock * k] != zero_idx;
+  atomicMax(&wmax, kk);
+  atomicAdd(&kept_sub[blk_sub[t]], (unsigned long long)kk);
+  __syncthreads();
+  if (threadIdx.x == 0) vtw[t] = wmax;
 }
 
 __global__ void k_vi_fold_slots(int64_t nfold, const int64_t* __restrict__ pos, const int32_t* __restrict__ slot,
@@ -97,6 +118,9 @@ void vi_free(Ctx& c) {
   if (c.vi_dict) cudaFree(c.vi_dict);
   if (c.vi_packed) cudaFree(c.vi_packed);
   if (c.vi_poff) cudaFree(c.vi_poff);
+  if (c.vi_tw) cudaFree(c.vi_tw);
+  c.vi_tw = nullptr;
+  c.vi_kept.clear();
   c.vi_idx = nullptr;
   c.vi_dict = nullptr;
   c.vi_packed = nullptr;
@@ -201,28 +225,46 @@ void vi_build(Ctx& c, bool per_side) {
     }
     wide = true;
   }
-  // 5. packed copy (4 entries of a row per 16-byte load); the 2-byte arrays are freed
+  // index of 0.0 in the sorted dictionary
+  std::vector<double> hd(nd);
+  OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * nd, cudaMemcpyDeviceToHost));
+  const uint32_t zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
+  // 5. packed copy (4 entries of a row per 16-byte load).  Entries whose value is exactly 0.0 -- the
+  // Kuhn stencil's structural zeros (~19 % of P2 entries) and the SELL padding -- are
+  // dropped: they add exact zeros (+-0) to the row sums, so the iterations stay the same.  Fold
+  // positions keep their own dictionary slots and are never dropped.
+  const int nloc = c.s_end - c.s_begin;
+  unsigned long long* d_kept = nullptr;
+  OSM_CUDA(cudaMalloc(&d_kept, sizeof(unsigned long long) * std::max(1, nloc)));
+  OSM_CUDA(cudaMemsetAsync(d_kept, 0, sizeof(unsigned long long) * std::max(1, nloc), c.stream));
+  OSM_CUDA(cudaMalloc(&c.vi_tw, sizeof(int32_t) * c.nblk_total));
+  k_vi_kept<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_idx,
+                                                                   zero_idx, c.blk_sub, c.vi_tw, d_kept);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
   std::vector<int32_t> tw(c.nblk_total);
-  OSM_CUDA(cudaMemcpy(tw.data(), c.sell_swidth, sizeof(int32_t) * c.nblk_total, cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> kept(std::max(1, nloc));
+  OSM_CUDA(cudaMemcpyAsync(tw.data(), c.vi_tw, sizeof(int32_t) * c.nblk_total, cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaMemcpyAsync(kept.data(), d_kept, sizeof(unsigned long long) * kept.size(), cudaMemcpyDeviceToHost,
+                           c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  cudaFree(d_kept);
+  c.vi_kept.assign(kept.begin(), kept.begin() + nloc);
   std::vector<int64_t> poff(c.nblk_total);
   int64_t words = 0;
   for (int64_t t = 0; t < c.nblk_total; ++t) {
     poff[t] = words;
     words += (int64_t)((tw[t] + 3) & ~3) * kRowsPerBlock;
   }
-  // index of 0.0 in the sorted dictionary
-  std::vector<double> hd(nd);
-  OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * nd, cudaMemcpyDeviceToHost));
-  const uint32_t zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
   OSM_CUDA(cudaMalloc(&c.vi_poff, sizeof(int64_t) * c.nblk_total));
   OSM_CUDA(cudaMemcpy(c.vi_poff, poff.data(), sizeof(int64_t) * c.nblk_total, cudaMemcpyHostToDevice));
   OSM_CUDA(cudaMalloc(&c.vi_packed, sizeof(uint32_t) * std::max<int64_t>(1, words)));
   if (wide)
     k_vi_pack<true><<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(
-        c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_poff, c.vi_idx, c.sell_col, zero_idx, c.vi_packed);
+        c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_tw, c.vi_poff, c.vi_idx, c.sell_col, zero_idx, c.vi_packed);
   else
     k_vi_pack<false><<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(
-        c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_poff, c.vi_idx, c.sell_col, zero_idx, c.vi_packed);
+        c.nblk_total, c.sell_soff, c.sell_swidth, c.vi_tw, c.vi_poff, c.vi_idx, c.sell_col, zero_idx, c.vi_packed);
   OSM_CHECK_LAUNCH();
   ++c.launches;
   OSM_CUDA(cudaStreamSynchronize(c.stream));

@@ -169,6 +169,7 @@ struct SubState {
   int32_t status;  // 0 running, 1 converged, 2 max_inner, 3 breakdown
   int32_t zero_rhs;
   uint32_t cnt;    // last-block counter
+  int32_t xpend;   // the PCG stopped in this iteration's update: the direction kernel still owes x += alpha p
 };
 
 // Device view of one interface side (grid.y of the interface kernels).

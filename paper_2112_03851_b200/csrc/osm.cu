@@ -1068,8 +1068,8 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     const double mat = mf ? 0.0 : (vi ? 4.0 * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
-    c.traffic[1] += (double)its * 56.0 * S.n;
-    c.traffic[2] += (double)its * 32.0 * S.n;
+    c.traffic[1] += (double)its * 32.0 * S.n;  // update: read r, q, D^-1; write r
+    c.traffic[2] += (double)its * 48.0 * S.n;  // direction: read r, D^-1, p, x; write p, x
     c.traffic[3] += (double)(S.sell_entries - S.nnz);
     c.traffic[4] += (double)S.nnz;
     c.traffic[5] += (double)S.n;

@@ -481,7 +481,10 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
   pdl_enter();
   const int64_t blk = blockIdx.x + blk_base;
   const int ls = blk_sub[blk];
-  if (!st[ls].active) return;
+  if (!st[ls].active) {  // the previous direction kernel has paid the stopped subdomain's x update
+    if (threadIdx.x == 0 && blk == st[ls].blk0) st[ls].xpend = 0;
+    return;
+  }
   const bool has_row = threadIdx.x < kRowsPerBlock;
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
   const double y = tile_row<V>(A, blk, p, dsm, mf);
@@ -509,7 +512,8 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
   }
 }
 
-// x += alpha p ; r -= alpha q ; z = D^{-1} r ; r.z, r.r ; stop test ||r|| <= tol ||rhs||; beta.
+// r -= alpha q ; z = D^{-1} r ; r.z, r.r ; stop test ||r|| <= tol ||rhs||; beta.  (x += alpha p moves to
+// the direction kernel, which reads p anyway: 8 bytes per row per iteration less.)
 // Vector blocks: up to kVecTiles tiles (1024 rows) of one subdomain, 128 threads x 8 rows,
 // all loads of a thread issued before any use (memory-level parallelism), one reduction
 // and one counter update per 1024 rows.
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
   const int nt = vblk_ntile[vb];
   const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;  // row-pair index
   const double a = st[ls].alpha;
-  double2 pv[kVecTiles], qv[kVecTiles], xv[kVecTiles], rv[kVecTiles], dv[kVecTiles];
+  double2 qv[kVecTiles], rv[kVecTiles], dv[kVecTiles];
   bool real[kVecTiles];
   uint16_t cc[kVecTiles];
 #pragma unroll
@@ -555,9 +559,7 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
-      pv[j] = reinterpret_cast<const double2*>(p)[i2];
       qv[j] = reinterpret_cast<const double2*>(q)[i2];
-      xv[j] = reinterpret_cast<const double2*>(x)[i2];
       rv[j] = reinterpret_cast<const double2*>(r)[i2];
       if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
     }
@@ -571,11 +573,8 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
-      xv[j].x = fma(a, pv[j].x, xv[j].x);
-      xv[j].y = fma(a, pv[j].y, xv[j].y);
       rv[j].x = fma(-a, qv[j].x, rv[j].x);
       rv[j].y = fma(-a, qv[j].y, rv[j].y);
-      reinterpret_cast<double2*>(x)[i2] = xv[j];
       reinterpret_cast<double2*>(r)[i2] = rv[j];
       const double z0 = dv[j].x * rv[j].x, z1 = dv[j].y * rv[j].y;
       v[0] += rv[j].x * z0 + rv[j].y * z1;
@@ -594,10 +593,12 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
       if (sqrt(rr) <= tol * sqrt(S.bb)) {
         S.status = 1;
         S.active = 0;
+        S.xpend = 1;
         atomicSub(nactive, 1);
       } else if (S.iters >= maxit) {
         S.status = 2;
         S.active = 0;
+        S.xpend = 1;
         atomicSub(nactive, 1);
       } else {
         S.beta = rz / S.rho;
@@ -607,52 +608,65 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
   }
 }
 
-// p = D^{-1} r + beta p  (vector blocks as k_cg_update)
+// x += alpha p ; p = D^{-1} r + beta p  (vector blocks as k_cg_update).  A subdomain whose PCG stopped in
+// this iteration's update (xpend) only gets its x update.
 template <int V>
 __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restrict__ vblk_sub,
                                                         const int32_t* __restrict__ vblk_tile0,
                                                         const int32_t* __restrict__ vblk_ntile,
                                                         const SubState* __restrict__ st, const double* __restrict__ r,
                                                         const double* __restrict__ dinv, double* __restrict__ p,
-                                                        const uint8_t* __restrict__ mcode,
+                                                        double* __restrict__ x, const uint8_t* __restrict__ mcode,
                                                         const __grid_constant__ MfArg<V> mf, int64_t vb_base) {
   constexpr bool MF = V == 5;
   pdl_enter();
   const int64_t vb = blockIdx.x + vb_base;
   const int ls = vblk_sub[vb];
-  if (!st[ls].active) return;
+  const bool act = st[ls].active;
+  if (!act && !st[ls].xpend) return;  // stopped in this iteration's update: only x += alpha p is owed
   const int nt = vblk_ntile[vb];
   const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;
-  const double beta = st[ls].beta;
-  double2 rv[kVecTiles], dv[kVecTiles], pv[kVecTiles];
+  const double beta = st[ls].beta, a = st[ls].alpha;
+  double2 rv[kVecTiles], dv[kVecTiles], pv[kVecTiles], xv[kVecTiles];
   bool real[kVecTiles];
   uint16_t cc[kVecTiles];
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j) {
     real[j] = j < nt;
     if constexpr (MF) {  // codes load alongside the vectors; D^{-1} is looked up after
-      if (j < nt) cc[j] = __ldg(reinterpret_cast<const uint16_t*>(mcode) + p0 + (int64_t)j * kVecThreads);
+      if (act && j < nt) cc[j] = __ldg(reinterpret_cast<const uint16_t*>(mcode) + p0 + (int64_t)j * kVecThreads);
     }
   }
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
-      rv[j] = reinterpret_cast<const double2*>(r)[i2];
-      if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
       pv[j] = reinterpret_cast<const double2*>(p)[i2];
+      xv[j] = reinterpret_cast<const double2*>(x)[i2];
+      if (act) {
+        rv[j] = reinterpret_cast<const double2*>(r)[i2];
+        if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
+      }
     }
   if constexpr (MF) {
+    if (act) {
 #pragma unroll
-    for (int j = 0; j < kVecTiles; ++j)
-      if (real[j]) dv[j] = mf_dinv2(cc[j], mf.c);
+      for (int j = 0; j < kVecTiles; ++j)
+        if (real[j]) dv[j] = mf_dinv2(cc[j], mf.c);
+    }
   }
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
-      pv[j].x = fma(beta, pv[j].x, dv[j].x * rv[j].x);
-      pv[j].y = fma(beta, pv[j].y, dv[j].y * rv[j].y);
-      reinterpret_cast<double2*>(p)[p0 + (int64_t)j * kVecThreads] = pv[j];
+      const int64_t i2 = p0 + (int64_t)j * kVecThreads;
+      xv[j].x = fma(a, pv[j].x, xv[j].x);  // x_{k+1} = x_k + alpha_k p_k (p_k: before the update below)
+      xv[j].y = fma(a, pv[j].y, xv[j].y);
+      reinterpret_cast<double2*>(x)[i2] = xv[j];
+      if (act) {
+        pv[j].x = fma(beta, pv[j].x, dv[j].x * rv[j].x);
+        pv[j].y = fma(beta, pv[j].y, dv[j].y * rv[j].y);
+        reinterpret_cast<double2*>(p)[i2] = pv[j];
+      }
     }
 }
 
@@ -696,6 +710,7 @@ __global__ void OSM_SPMV_BOUNDS(V) k_warm(SellDev A, const int32_t* __restrict__
       S.rr = t[1];
       S.bb = t[2];
       S.iters = 0;
+      S.xpend = 0;
       S.zero_rhs = (t[2] == 0.0);
       if (t[2] == 0.0 || sqrt(t[1]) <= tol * sqrt(t[2])) {
         S.status = 1;
@@ -1012,7 +1027,7 @@ template <int V>
 static void cg_dir_v(Ctx& c) {
   launch_pdl(c, k_cg_dir<V>, (unsigned)grp_nvb(c), kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
              (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, (const SubState*)c.st, (const double*)c.r,
-             (const double*)c.dinv, c.p, (const uint8_t*)c.d_mf_code, mf_arg<V>(c), grp_vb0(c));
+             (const double*)c.dinv, c.p, c.x, (const uint8_t*)c.d_mf_code, mf_arg<V>(c), grp_vb0(c));
 }
 
 void launch_cg_dir(Ctx& c) {

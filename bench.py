@@ -185,6 +185,8 @@ def main():
 
             dist.init_process_group("gloo")
         run_reference(args, cfg, drho, rank)
+        if world > 1:
+            dist.destroy_process_group()
         return
 
     import torch

@@ -273,13 +273,16 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * constant bank as a kernel parameter (default, up to 2048 distinct values); 7 = 6 on wide
  * entries (12-bit index, 20-bit offset), selected automatically when offsets exceed int16;
  * 8 = 5 with each tile's x window staged in shared memory by bulk copies (experimental, slower);
+ * 9 value-indexed rows with implicit column offsets (row order 4: each row stores one 16-bit
+ * dictionary index per slot of its stencil's offset list, the offset lists and the dictionary are
+ * kernel parameters; experimental, slower than 6 and 5; falls back to 6);
  * 5 matrix-free Kuhn
  * stencil (the K_s values are uniform per parity class and row kind on the
  * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row
  * order 4, see osm_set_row_order).  Variants 3/4/6 fall back to 2 when the matrix does not
  * admit the value-indexed copy (6 to 3 beyond 2048 values); 5 falls back to 4 without row order 4
  * or when a slab is too thin for the tables.  *active (may be NULL) receives the variant that will actually run.  INVALID_ARG
- * for other values. */
+ * outside 0..9. */
 osm_status osm_set_spmv_variant(osm_ctx* ctx, int variant, int* active);
 
 /* Internal row order of the GPU copy (a permutation private to the library; results are

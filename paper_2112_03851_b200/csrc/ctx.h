@@ -128,6 +128,20 @@ template <>
 struct MfArg<7> {  // variant 6 on the wide (20-bit offset) entries
   double dict[kCDict];
 };
+// Variant 9: value-indexed rows with implicit column offsets (row order 4).  Every row of a
+// (subdomain, kind, class) has its nonzeros at the same internal row offsets, so a row stores only
+// its 16-bit dictionary indices, one per slot of its stencil's offset list (4 slots per 8-byte
+// group); the offset lists and the dictionary are kernel parameters.
+struct MfDia {
+  int32_t valid;
+  int32_t gbeg[kMfMaxTab + 1];  // slot groups of offset list tb: [gbeg[tb], gbeg[tb+1])
+  int4 delta[kMfMaxGroups];     // 4 internal row offsets per group
+  double dict[kCDict];
+};
+template <>
+struct MfArg<9> {
+  MfDia c;
+};
 
 struct SellDev {
   const double* val;
@@ -150,6 +164,9 @@ struct SellDev {
   const int32_t* mf_win_begin;
   const int3* mf_win;
   int64_t nrows;            // rows of the concatenated vectors (bulk-copy bounds)
+  const uint8_t* mf_code;   // per row: deduplicated table id of the constant-bank tables, 0xff dummy row
+  const uint2* dia_idx;     // variant 9: per tile, group g of row r at dia_off[tile] + 256 g + r (4 x u16)
+  const int64_t* dia_off;
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -364,6 +381,12 @@ struct Ctx {
   int32_t* d_mf_win_begin = nullptr;
   int3* d_mf_win = nullptr;
   int mf_win_rows = 0;            // largest window (rows) = shared memory of variant 8 / 8 B
+  MfDia* h_dia = nullptr;         // variant 9 kernel parameter (offset lists + dictionary)
+  uint2* d_dia_idx = nullptr;     // variant 9 per-row dictionary indices
+  int64_t* d_dia_off = nullptr;
+  int64_t dia_groups = 0;         // stored 8-byte groups (4 slots each)
+  bool dia_ok = false;
+  std::vector<double> dia_sub_bytes;  // variant 9 bytes read per SpMV per local subdomain (traffic model)
   uint8_t* d_mf_code = nullptr;   // per internal row: deduplicated table id, 0xff dummy (vector kernels)
 
   // value-indexed SELL (vi.cu)
@@ -439,6 +462,7 @@ void spmv_init_attributes();
 void gravity_z(Ctx& c, double z0, double* d_out);  // gravity.cu (uses c.phi)
 void vi_build(Ctx& c, bool per_side = false);
 void vi_free(Ctx& c);
+void launch_dia_pack(Ctx& c, const int32_t* d_gbeg, const int32_t* d_delta, const uint8_t* d_real, int32_t* d_bad);
 void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side);
 int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)
 

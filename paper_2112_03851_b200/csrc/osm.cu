@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -89,6 +90,8 @@ static void timers_collect(Ctx& c) {
 }
 
 // ------------------------------------------------------------------ teardown
+static void dia_free(Ctx& c);
+
 static void drop_graph(Ctx& c) {
   if (c.cg_graph) cudaGraphExecDestroy(c.cg_graph);
   c.cg_graph = nullptr;
@@ -174,6 +177,7 @@ static void free_assembly(Ctx& c) {
   dfree(c.d_mf_win);
   c.mf_win_rows = 0;
   dfree(c.d_mf_code);
+  dia_free(c);
   c.assembled = false;
   c.density_set = false;
 }
@@ -323,6 +327,96 @@ static void mf_refresh(Ctx& c) {
   } else {
     dfree(c.d_mf_code);
   }
+}
+
+static void dia_free(Ctx& c) {
+  dfree(c.d_dia_idx);
+  dfree(c.d_dia_off);
+  delete c.h_dia;
+  c.h_dia = nullptr;
+  c.dia_groups = 0;
+  c.dia_ok = false;
+  c.dia_sub_bytes.clear();
+}
+
+// Value-indexed rows with implicit column offsets (SpMV variant 9, row order 4).  The offset list of
+// a row is the nonzero part of its (subdomain, kind, class) stencil table (MfConst.delta, padding
+// slots aside); the row stores one 16-bit dictionary index per slot, taken from its own assembled,
+// Robin-folded SELL entries by k_dia_pack.  Rebuilt whenever the tables or the dictionary slots
+// change (assembly, osm_set_robin).
+static void dia_build(Ctx& c) {
+  dia_free(c);
+  const bool dbg = std::getenv("OSM_DEBUG") != nullptr;
+  if (!c.mf_ok || !c.h_mf_const || !c.h_mf_const->valid || !c.d_mf_code || !c.vi_ok || !c.vi_idx ||
+      c.vi_ndict > kCDict) {
+    if (dbg)
+      std::fprintf(stderr, "dia: prerequisites mf_ok %d const %d code %d vi_ok %d vi_idx %d ndict %lld\n", (int)c.mf_ok,
+                   c.h_mf_const && c.h_mf_const->valid, c.d_mf_code != nullptr, (int)c.vi_ok, c.vi_idx != nullptr,
+                   (long long)c.vi_ndict);
+    return;
+  }
+  const MfConst& P = *c.h_mf_const;
+  int ntab = 0;  // deduplicated tables (some may be empty)
+  for (size_t t = 0; t + 1 < c.h_mf_begin.size(); ++t) ntab = std::max(ntab, P.tabid[t] + 1);
+  std::vector<uint8_t> code(c.nrows_total);
+  OSM_CUDA(cudaMemcpy(code.data(), c.d_mf_code, c.nrows_total, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> doff(c.nblk_total);
+  const int nloc = c.s_end - c.s_begin;
+  c.dia_sub_bytes.assign(nloc, 0.0);
+  int64_t groups = 0;
+  std::vector<int> tsub(c.nblk_total, 0);
+  for (int ls = 0; ls < nloc; ++ls)
+    for (int64_t k = 0; k < c.subs[ls].nblk; ++k) tsub[c.subs[ls].blk0 + k] = ls;
+  for (int64_t t = 0; t < c.nblk_total; ++t) {
+    int w = 0;
+    for (int l = 0; l < kRowsPerBlock; ++l) {
+      const int tb = code[t * kRowsPerBlock + l];
+      if (tb == 0xff) continue;
+      if (tb >= ntab) {
+        if (dbg) std::fprintf(stderr, "dia: code %d >= ntab %d\n", tb, ntab);
+        return;
+      }
+      const int g = P.gbeg[tb + 1] - P.gbeg[tb];
+      w = std::max(w, g);
+      c.dia_sub_bytes[tsub[t]] += 8.0 * g;  // the row's index groups
+    }
+    c.dia_sub_bytes[tsub[t]] += kRowsPerBlock;  // 1-byte codes
+    doff[t] = groups;
+    groups += (int64_t)w * kRowsPerBlock;
+  }
+  const int nslot = 4 * P.gbeg[ntab];
+  std::vector<int32_t> gbeg(P.gbeg, P.gbeg + ntab + 1), delta(std::max(1, nslot));
+  std::vector<uint8_t> real(std::max(1, nslot));
+  for (int k = 0; k < nslot; ++k) {
+    delta[k] = (&P.delta[0].x)[k];
+    real[k] = P.val[k] != 0.0;  // the tables hold only nonzero values; +0.0 marks padding
+  }
+  c.d_dia_off = dupload(c, doff);
+  c.d_dia_idx = dalloc<uint2>(std::max<int64_t>(1, groups));
+  int32_t* d_gbeg = dupload(c, gbeg);
+  int32_t* d_delta = dupload(c, delta);
+  uint8_t* d_real = dupload(c, real);
+  OSM_CUDA(cudaMemsetAsync(c.d_flags + 3, 0, sizeof(int32_t), c.stream));
+  launch_dia_pack(c, d_gbeg, d_delta, d_real, c.d_flags + 3);
+  int32_t bad = 0;
+  OSM_CUDA(cudaMemcpyAsync(&bad, c.d_flags + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  dfree(d_gbeg);
+  dfree(d_delta);
+  dfree(d_real);
+  drop_graph(c);
+  if (bad) {
+    if (dbg) std::fprintf(stderr, "dia: %d rows do not match their offset lists\n", bad);
+    dia_free(c);
+    return;
+  }
+  c.h_dia = new MfDia();
+  std::memset(c.h_dia, 0, sizeof(MfDia));
+  c.h_dia->valid = 1;
+  std::copy(gbeg.begin(), gbeg.end(), c.h_dia->gbeg);
+  std::copy(P.delta, P.delta + P.gbeg[ntab], c.h_dia->delta);
+  c.dia_groups = groups;
+  c.dia_ok = true;
 }
 
 // Matrix-free Kuhn-stencil tables (SpMV variant 5, row order 4).  For every
@@ -660,7 +754,10 @@ static void assemble(Ctx& c) {
   }
   vi_build(c);  // value-indexed hot copy (from the unfolded K^N values)
   vi_sync_host_dict(c);
-  if (c.sort_key == 4) mf_build(c, h_iperm, h_len, h_soff);
+  if (c.sort_key == 4) {
+    mf_build(c, h_iperm, h_len, h_soff);
+    dia_build(c);
+  }
 
   // --- reductions and device side table
   c.part = dalloc<double>(3 * c.nblk_total);
@@ -766,6 +863,7 @@ static void apply_robin(Ctx& c) {
   dfree(d_q);
   vi_apply_robin(c, a, qv);
   vi_sync_host_dict(c);
+  if (c.sort_key == 4) dia_build(c);
   if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
   c.robin_dirty = false;
 }
@@ -1056,7 +1154,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   c.traffic[7] = c.exch_bytes;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
-  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5 || sv == 8;
+  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5 || sv == 8, dia = sv == 9;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1065,7 +1163,9 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     // value-indexed 4 B/entry (index + offset; the dictionary is on chip), or matrix-free 0 B/entry
     // (tables in the constant bank); vectors p, q 16 B/row
     const double kept = ls < (int)c.vi_kept.size() ? (double)c.vi_kept[ls] : (double)S.nnz;
-    const double mat = mf ? 0.0 : (vi ? 4.0 * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
+    // (variant 5 reads a 1-byte table code per row; variant 9 its 8-byte index groups and the code)
+    const double mat = mf ? (c.d_mf_code ? (double)S.npad : 0.0)
+                          : dia ? c.dia_sub_bytes[ls] : (vi ? 4.0 * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
     c.traffic[1] += (double)its * 32.0 * S.n;  // update: read r, q, D^-1; write r
@@ -1651,7 +1751,7 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 8) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..8");
+  if (v < 0 || v > 9) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..9");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);

@@ -333,10 +333,28 @@ __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk
 // are 32 consecutive rows shifted by one offset: coalesced, with no column indices read.
 __device__ __forceinline__ double tile_row_mf(const SellDev& A, int64_t blk, const double* __restrict__ x,
                                               const MfConst& P) {
-  const int ls = A.blk_sub[blk];
-  const MfSub& M = A.mf_sub[ls];
   const int64_t ri = blk * kRowsPerBlock + threadIdx.x;
   double s = 0.0;
+#ifndef OSM_MF_NOCODE
+  if (P.valid && A.mf_code) {  // the row's 1-byte table code instead of its lattice arithmetic
+    const int tb = __ldg(A.mf_code + ri);
+    if (tb == 0xff) return s;  // dummy row (Dirichlet or padding point): like a SELL padding row
+    const double* xr = x + ri;
+    asm("" : "+l"(xr));
+#pragma unroll 2
+    for (int g = P.gbeg[tb]; g < P.gbeg[tb + 1]; ++g) {
+      const int4 d = P.delta[g];
+      const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
+      s = fma(P.val[4 * g], x0, s);
+      s = fma(P.val[4 * g + 1], x1, s);
+      s = fma(P.val[4 * g + 2], x2, s);
+      s = fma(P.val[4 * g + 3], x3, s);
+    }
+    return s;
+  }
+#endif
+  const int ls = A.blk_sub[blk];
+  const MfSub& M = A.mf_sub[ls];
   const int t = mf_table_of(M, ri - M.row0);
   if (t < 0) return s;  // dummy row (Dirichlet or padding point): like a SELL padding row
   const double* xr = x + ri;
@@ -364,6 +382,42 @@ __device__ __forceinline__ double tile_row_mf(const SellDev& A, int64_t blk, con
     s = fma(v01.y, x1, s);
     s = fma(v23.x, x2, s);
     s = fma(v23.y, x3, s);
+  }
+  return s;
+}
+
+__device__ __forceinline__ uint2 ld_stream2(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// Variant 9: value-indexed rows with implicit column offsets (row order 4, see MfDia).  The row's
+// 1-byte code selects its offset list (constant bank); the row's own 16-bit dictionary indices
+// stream in 8-byte groups of 4, coalesced across the warp, and no longer gate the x gathers (their
+// addresses come from the offset list).  Same FMA chain as the SELL variants.
+__device__ __forceinline__ double tile_row_dia(const SellDev& A, int64_t blk, const double* __restrict__ x,
+                                               const MfDia& P) {
+  const int64_t ri = blk * kRowsPerBlock + threadIdx.x;
+  double s = 0.0;
+  const int tb = __ldg(A.mf_code + ri);
+  if (tb == 0xff) return s;  // dummy row
+  const double* xr = x + ri;
+  asm("" : "+l"(xr));
+  const uint2* ip = A.dia_idx + A.dia_off[blk] + threadIdx.x;
+  const int g0 = P.gbeg[tb], ng = P.gbeg[tb + 1] - g0;
+  if (ng == 0) return s;
+  uint2 e = ld_stream2(ip);
+  for (int j = 0; j < ng; ++j) {
+    const int4 d = P.delta[g0 + j];
+    const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
+    const double v0 = P.dict[e.x & 0xffffu], v1 = P.dict[e.x >> 16], v2 = P.dict[e.y & 0xffffu],
+                 v3 = P.dict[e.y >> 16];
+    if (j + 1 < ng) e = ld_stream2(ip + (int64_t)kRowsPerBlock * (j + 1));
+    s = fma(v0, x0, s);
+    s = fma(v1, x1, s);
+    s = fma(v2, x2, s);
+    s = fma(v3, x3, s);
   }
   return s;
 }
@@ -454,6 +508,7 @@ __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const 
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
   if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c);
   if constexpr (V == 8) return tile_row_mf_win(A, blk, x, mf.c, smem);
+  if constexpr (V == 9) return tile_row_dia(A, blk, x, mf.c);
   if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict);
   if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict);
   if constexpr (V == 4) {
@@ -851,7 +906,9 @@ SellDev sell_of(const Ctx& c) {
   return SellDev{c.sell_val,  c.sell_col,   c.sell_soff,  c.sell_swidth,
                  c.vi_packed, c.vi_poff,     c.vi_tw,      c.vi_dict,    (int)c.vi_ndict,
                  c.blk_sub,   c.d_mf_sub,    c.d_mf_begin, reinterpret_cast<const int4*>(c.d_mf_delta),
-                 c.d_mf_val,  c.d_mf_win_begin, c.d_mf_win, c.nrows_total};
+                 c.d_mf_val,  c.d_mf_win_begin, c.d_mf_win, c.nrows_total,
+                 c.h_mf_const && c.h_mf_const->valid ? c.d_mf_code : nullptr,
+                 c.d_dia_idx, c.d_dia_off};
 }
 
 }  // namespace
@@ -860,6 +917,10 @@ constexpr int kMfWinSmemMax = 200 * 1024;  // variant 8 window (bytes); larger w
 
 int spmv_variant_of(const Ctx& c) {
   int v = c.spmv_variant;
+  if (v == 9) {
+    if (c.dia_ok && c.h_dia && c.vi_ndict <= kCDict) return 9;
+    v = 6;
+  }
   if (v == 8) {
     if (c.mf_ok && c.h_mf_win_const && c.h_mf_win_const->valid && c.d_mf_win &&
         c.mf_win_rows * 8 <= kMfWinSmemMax)
@@ -912,6 +973,10 @@ static MfArg<V> mf_arg(const Ctx& c) {
   }
   if constexpr (V == 6 || V == 7)
     std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.dict);
+  if constexpr (V == 9) {
+    if (c.h_dia) a.c = *c.h_dia;
+    std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.c.dict);
+  }
   return a;
 }
 
@@ -935,6 +1000,7 @@ void launch_warm(Ctx& c, double tol, int) {
     case 6: warm_v<6>(c, tol); break;
     case 7: warm_v<7>(c, tol); break;
     case 8: warm_v<8>(c, tol); break;
+    case 9: warm_v<9>(c, tol); break;
     default: warm_v<4>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
@@ -990,6 +1056,7 @@ void launch_cg_spmv(Ctx& c) {
     case 6: cg_spmv_v<6>(c); break;
     case 7: cg_spmv_v<7>(c); break;
     case 8: cg_spmv_v<8>(c); break;
+    case 9: cg_spmv_v<9>(c); break;
     default: cg_spmv_v<4>(c); break;
   }
   ++c.launches;
@@ -1081,6 +1148,7 @@ void launch_resid(Ctx& c) {
     case 6: resid_v<6>(c); break;
     case 7: resid_v<7>(c); break;
     case 8: resid_v<8>(c); break;
+    case 9: resid_v<9>(c); break;
     default: resid_v<4>(c); break;
   }
   OSM_CHECK_LAUNCH();

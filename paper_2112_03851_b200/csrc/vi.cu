@@ -111,7 +111,55 @@ __global__ void k_vi_fold_slots(int64_t nfold, const int64_t* __restrict__ pos, 
   vidx[pos[e]] = (uint16_t)slot[e];
 }
 
+// Variant 9 copy: one thread per row of tile t.  The row's nonzero SELL entries (current, Robin-folded
+// values; exact zeros and padding skipped) are matched in order against the slots of its offset list
+// (code[row] = list id; real[] marks the non-padding slots); each matched slot takes the entry's
+// dictionary index, the others the index of 0.0.  An entry with no slot left sets *bad.
+__global__ void k_dia_pack(const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
+                           const int32_t* __restrict__ col, const double* __restrict__ sval,
+                           const uint16_t* __restrict__ vidx, uint32_t zero_idx, const uint8_t* __restrict__ code,
+                           const int32_t* __restrict__ gbeg, const int32_t* __restrict__ delta,
+                           const uint8_t* __restrict__ real, const int64_t* __restrict__ doff,
+                           uint16_t* __restrict__ out, int32_t* __restrict__ bad) {
+  const int64_t t = blockIdx.x;
+  const int r = threadIdx.x;
+  const int64_t row = t * kRowsPerBlock + r;
+  const int tb = code[row];
+  if (tb == 0xff) return;
+  const int s0 = 4 * gbeg[tb], ns = 4 * (gbeg[tb + 1] - gbeg[tb]);
+  auto at = [&](int j) -> uint16_t& { return out[4 * (doff[t] + (int64_t)kRowsPerBlock * (j >> 2) + r) + (j & 3)]; };
+  for (int j = 0; j < ns; ++j) at(j) = (uint16_t)zero_idx;
+  const int w = twidth[t];
+  const int64_t base = toff[t] + r;
+  int j = 0;
+  for (int k = 0; k < w; ++k) {
+    const int64_t i = base + (int64_t)kRowsPerBlock * k;
+    if (sval[i] == 0.0) continue;
+    const int32_t d = col[i] - (int32_t)row;
+    while (j < ns && !(real[s0 + j] && delta[s0 + j] == d)) ++j;
+    if (j == ns) {
+      atomicAdd(bad, 1);
+      return;
+    }
+    at(j++) = vidx[i];
+  }
+}
+
 }  // namespace
+
+void launch_dia_pack(Ctx& c, const int32_t* d_gbeg, const int32_t* d_delta, const uint8_t* d_real, int32_t* d_bad) {
+  uint32_t zero_idx = 0;
+  {
+    std::vector<double> hd(c.vi_nbase);
+    OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * c.vi_nbase, cudaMemcpyDeviceToHost));
+    zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
+  }
+  k_dia_pack<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(
+      c.sell_soff, c.sell_swidth, c.sell_col, c.sell_val, c.vi_idx, zero_idx, c.d_mf_code, d_gbeg, d_delta, d_real,
+      c.d_dia_off, reinterpret_cast<uint16_t*>(c.d_dia_idx), d_bad);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+}
 
 void vi_free(Ctx& c) {
   if (c.vi_idx) cudaFree(c.vi_idx);
@@ -268,8 +316,10 @@ void vi_build(Ctx& c, bool per_side) {
   OSM_CHECK_LAUNCH();
   ++c.launches;
   OSM_CUDA(cudaStreamSynchronize(c.stream));
-  cudaFree(c.vi_idx);
-  c.vi_idx = nullptr;
+  if (c.sort_key != 4) {  // row order 4 keeps the indices for the implicit-offset copy (variant 9)
+    cudaFree(c.vi_idx);
+    c.vi_idx = nullptr;
+  }
   c.vi_words = words;
   c.vi_per_side = per_side;
   c.vi_wide = wide;

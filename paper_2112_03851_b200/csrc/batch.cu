@@ -115,11 +115,11 @@ __device__ __forceinline__ bool bpublish(double* part, int64_t blk, int NP, cons
                                          int nblk_sub) {
   __shared__ bool last;
   for (int i = threadIdx.x; i < NP * KB; i += blockDim.x) part[blk * NP * KB + i] = sm[i];
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(cnt, 1u);
+  if (threadIdx.x == 0) {  // release is cumulative: it orders the block's stores seen through the barrier
+    const uint32_t prev = atom_add_release_gpu(cnt, 1u);
     last = prev == (uint32_t)(nblk_sub - 1);
+    if (last) __threadfence();
   }
   __syncthreads();
   return last;

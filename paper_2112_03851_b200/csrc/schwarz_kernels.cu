@@ -69,9 +69,9 @@ __device__ __forceinline__ bool publish(const double (&v)[N], double* part, int6
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < N; ++i) part[i * stride + blk] = v[i];
-    __threadfence();
-    const uint32_t prev = atomicAdd(cnt, 1u);
+    const uint32_t prev = atom_add_release_gpu(cnt, 1u);
     last = (prev == (uint32_t)(nblk - 1));
+    if (last) __threadfence();  // acquire side: only the last block pays a full fence
   }
   __syncthreads();
   return last;

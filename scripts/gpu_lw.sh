@@ -1,0 +1,7 @@
+OSM_LIB=expt/c/libosm.so timeout 900 python -m pytest tests/test_gpu_variants.py tests/test_gpu_parity.py tests/test_gpu_matrix_free.py -m gpu -x -q 2>&1 | tail -2
+for L in "" expt/c/libosm.so; do
+  OSM_LIB=$L OSM_GROUPS=1 timeout 300 python tools/cg_bench.py --solves 2 --timing | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$L', {k:round(v['us_per_launch'],2) for k,v in d['kernels'].items() if k in ('cg_spmv','cg_update','cg_dir')}, d['h'])"
+  OSM_LIB=$L timeout 300 python tools/cg_bench.py --solves 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$L', [round(x,4) for x in d['seconds']], d['h'])"
+  OSM_LIB=$L OSM_SORT=4 OSM_SPMV=5 OSM_GROUPS=1 timeout 300 python tools/cg_bench.py --solves 2 --timing | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$L MF', {k:round(v['us_per_launch'],2) for k,v in d['kernels'].items() if k in ('cg_spmv',)})"
+  OSM_LIB=$L OSM_SORT=4 OSM_SPMV=5 timeout 300 python tools/cg_bench.py --solves 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$L MF', [round(x,4) for x in d['seconds']])"
+done

@@ -346,6 +346,12 @@ struct Ctx {
   int vec_tiles = kVecTiles;  // tiles per vector block (update/dir kernels), chosen at assembly
   int vt_override = 0;         // OSM_VT
   bool groups_forced = false;  // OSM_GROUPS given: no size-based reduction
+  // SM-affine persistent SpMV (experimental, OSM_PERSIST=1): tiles in region-major, class-minor order,
+  // one contiguous range per SM and group; per-(group, SM) tile counters + one exit counter per group
+  bool persist = false;
+  int nsm = 148;
+  int32_t* d_tseq = nullptr;
+  uint32_t* d_sm_ctr = nullptr;
   int want_groups = 8;  // OSM_GROUPS = 1, 2, 4 or 8 (capped by the local subdomain count)
 
   // CUDA graph of one chunk of PCG iterations (spmv, update, dir) x kCgChunk, with PDL edges

@@ -103,6 +103,8 @@ static void drop_graph(Ctx& c) {
 
 static void free_assembly(Ctx& c) {
   drop_graph(c);
+  dfree(c.d_tseq);
+  dfree(c.d_sm_ctr);
   batch_free(c);
   vi_free(c);
   for (auto& s : c.subs) {
@@ -796,6 +798,49 @@ static void assemble(Ctx& c) {
     c.g_vb0[g] = hst[s0].vblk0;
     c.g_nvb[g] = (s1 < nloc ? hst[s1].vblk0 : c.nvblk_total) - hst[s0].vblk0;
   }
+  if (c.persist) {  // tile order of the SM-affine SpMV: per group, by (region of the first row, class)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    c.nsm = sms;
+    std::vector<int32_t> seq(c.nblk_total);
+    std::vector<std::tuple<int64_t, int64_t, int64_t, int64_t, int32_t>> key;  // (sub, region a, b, d; tile)
+    for (int g = 0; g < c.ngroups; ++g) {
+      key.clear();
+      for (int64_t t = c.g_blk0[g]; t < c.g_blk0[g] + c.g_nblk[g]; ++t) {
+        int ls = 0;
+        while (ls + 1 < nloc && c.subs[ls + 1].blk0 <= t) ++ls;
+        const Sub& S = c.subs[ls];
+        const auto& perm = h_perm[ls];
+        int64_t a = INT64_MAX, b = 0, d = 0;  // the first real row's position on the class sub-lattice
+        for (int l = 0; l < kRowsPerBlock; ++l) {
+          const int32_t lc = perm[(t - S.blk0) * kRowsPerBlock + l];
+          if (lc < 0) continue;
+          const int64_t I = S.g.I_lo + lc % S.g.nI, t2 = lc / S.g.nI, J = 1 + t2 % S.g.nJ, K = 1 + t2 / S.g.nJ;
+          if (c.sort_key == 4) {
+            a = I / o, b = K / o, d = J / o;
+          } else {
+            a = K / o, b = I / o, d = J / o;
+          }
+          break;
+        }
+        key.emplace_back(ls, a, b, d, (int32_t)t);  // stable sort: equal regions keep the class order
+      }
+      std::vector<size_t> ix(key.size());
+      std::iota(ix.begin(), ix.end(), 0);
+      std::stable_sort(ix.begin(), ix.end(), [&](size_t i, size_t j) {
+        const auto& A = key[i];
+        const auto& B = key[j];
+        return std::make_tuple(std::get<0>(A), std::get<1>(A), std::get<2>(A), std::get<3>(A)) <
+               std::make_tuple(std::get<0>(B), std::get<1>(B), std::get<2>(B), std::get<3>(B));
+      });
+      for (size_t k = 0; k < ix.size(); ++k) seq[c.g_blk0[g] + (int64_t)k] = std::get<4>(key[ix[k]]);
+    }
+    dfree(c.d_tseq);
+    dfree(c.d_sm_ctr);
+    c.d_tseq = dupload(c, seq);
+    c.d_sm_ctr = dalloc<uint32_t>((int64_t)Ctx::kMaxGroups * (c.nsm + 1));
+    OSM_CUDA(cudaMemsetAsync(c.d_sm_ctr, 0, sizeof(uint32_t) * Ctx::kMaxGroups * (c.nsm + 1), c.stream));
+  }
   if (c.h_st) cudaFreeHost(c.h_st);
   OSM_CUDA(cudaMallocHost((void**)&c.h_st, sizeof(SubState) * std::max(1, nloc)));
   if (c.h_side_sum) cudaFreeHost(c.h_side_sum);
@@ -1273,6 +1318,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
       c.want_groups = std::max(1, std::atoi(e));
       c.groups_forced = true;
     }
+    if (const char* e = std::getenv("OSM_PERSIST")) c.persist = std::atoi(e) != 0;
     if (const char* e = std::getenv("OSM_VT")) c.vt_override = std::atoi(e);
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;

@@ -523,18 +523,13 @@ __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const 
 
 // ---------------------------------------------------------------- PCG kernels
 
-// q = K_s p ; p.q -> alpha = rho / (p.q)
-template <int V>
-__global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restrict__ blk_sub,
-                                                      SubState* __restrict__ st, const double* __restrict__ p,
-                                                      double* __restrict__ q, double* __restrict__ part,
-                                                      int64_t stride, int32_t* __restrict__ nactive,
-                                                      const __grid_constant__ MfArg<V> mf, int64_t blk_base) {
-  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
-  __shared__ double sm[NW * 1];
-  extern __shared__ __align__(128) unsigned char dsm[];
-  pdl_enter();
-  const int64_t blk = blockIdx.x + blk_base;
+// q = K_s p ; p.q -> alpha = rho / (p.q), for tile blk (one block)
+template <int V, int NW>
+__device__ __forceinline__ void spmv_tile(const SellDev& A, int64_t blk, const int32_t* __restrict__ blk_sub,
+                                          SubState* __restrict__ st, const double* __restrict__ p,
+                                          double* __restrict__ q, double* __restrict__ part, int64_t stride,
+                                          int32_t* __restrict__ nactive, const MfArg<V>& mf, double* sm,
+                                          unsigned char* dsm) {
   const int ls = blk_sub[blk];
   if (!st[ls].active) {  // the previous direction kernel has paid the stopped subdomain's x update
     if (threadIdx.x == 0 && blk == st[ls].blk0) st[ls].xpend = 0;
@@ -563,6 +558,81 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
       } else {
         S.alpha = S.rho / pq;
       }
+    }
+  }
+}
+
+template <int V>
+__global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restrict__ blk_sub,
+                                                      SubState* __restrict__ st, const double* __restrict__ p,
+                                                      double* __restrict__ q, double* __restrict__ part,
+                                                      int64_t stride, int32_t* __restrict__ nactive,
+                                                      const __grid_constant__ MfArg<V> mf, int64_t blk_base) {
+  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  __shared__ double sm[NW * 1];
+  extern __shared__ __align__(128) unsigned char dsm[];
+  pdl_enter();
+  spmv_tile<V, NW>(A, blockIdx.x + blk_base, blk_sub, st, p, q, part, stride, nactive, mf, sm, dsm);
+}
+
+// SM-affine persistent SpMV (experimental, OSM_PERSIST=1).  The group's tiles, in region-major /
+// class-minor order (seq), are cut into one contiguous range per SM; a block takes tiles from the range
+// of the SM it runs on, so the blocks resident on one SM work on the same few regions in all classes
+// and share their x lines in L1.  Exhausted ranges are skipped; other SMs' ranges are stolen at the
+// end.  Each tile is computed exactly as k_cg_spmv computes it (same partials, bitwise).
+__device__ __forceinline__ unsigned smid_reg() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+template <int V>
+__global__ void __launch_bounds__(kThreads, 8) k_cg_spmv_sm(SellDev A, const int32_t* __restrict__ blk_sub,
+                                                           SubState* __restrict__ st, const double* __restrict__ p,
+                                                           double* __restrict__ q, double* __restrict__ part,
+                                                           int64_t stride, int32_t* __restrict__ nactive,
+                                                           const __grid_constant__ MfArg<V> mf,
+                                                           const int32_t* __restrict__ seq, int nseq, int nsm,
+                                                           uint32_t* __restrict__ ctr) {
+  constexpr int NW = kSlicesPerBlock;
+  __shared__ double sm[NW];
+  __shared__ int pos_sh, found_sh;
+  pdl_enter();
+  const int me = (int)(smid_reg() % (unsigned)nsm);
+  int s = me;
+  for (;;) {
+    const int b = (int)((int64_t)s * nseq / nsm), e = (int)((int64_t)(s + 1) * nseq / nsm);
+    if (threadIdx.x == 0) pos_sh = b + (int)atomicAdd(&ctr[s], 1u);
+    __syncthreads();
+    int pos = pos_sh;
+    while (pos < e) {
+      // the next tile's counter bump is in flight while this tile runs (thread 0 waits on it at the end)
+      unsigned nxt = 0;
+      if (threadIdx.x == 0) nxt = atomicAdd(&ctr[s], 1u);
+      spmv_tile<V, NW>(A, seq[pos], blk_sub, st, p, q, part, stride, nactive, mf, sm, nullptr);
+      __syncthreads();  // every thread has read pos_sh
+      if (threadIdx.x == 0) pos_sh = b + (int)nxt;
+      __syncthreads();
+      pos = pos_sh;
+    }
+    // steal: the nearest SM range (in SM order after this one) with tiles left
+    if (threadIdx.x == 0) found_sh = nsm;
+    __syncthreads();
+    for (int k = threadIdx.x + 1; k < nsm; k += blockDim.x) {
+      const int s2 = (me + k) % nsm;
+      const int b2 = (int)((int64_t)s2 * nseq / nsm), e2 = (int)((int64_t)(s2 + 1) * nseq / nsm);
+      if (b2 + (int)__ldcg(&ctr[s2]) < e2) atomicMin(&found_sh, k);
+    }
+    __syncthreads();
+    const int f = found_sh;
+    __syncthreads();
+    if (f >= nsm) break;
+    s = (me + f) % nsm;
+  }
+  if (threadIdx.x == 0) {  // the last block out resets the counters for the next launch
+    __threadfence();
+    if (atomicAdd(&ctr[nsm], 1u) == gridDim.x - 1) {
+      for (int k = 0; k <= nsm; ++k) ctr[k] = 0;
+      __threadfence();
     }
   }
 }
@@ -1039,6 +1109,17 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
 
 template <int V>
 static void cg_spmv_v(Ctx& c) {
+  if constexpr (V == 5 || V == 6) {
+    if (c.persist && c.d_tseq) {
+      const int g = c.grp_cur >= 0 ? c.grp_cur : 0;
+      const int nt = (int)grp_nblk(c);
+      const unsigned grid = (unsigned)std::min<int64_t>(nt, 8LL * c.nsm);
+      launch_pdl(c, k_cg_spmv_sm<V>, grid, kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub, c.st,
+                 (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c),
+                 (const int32_t*)(c.d_tseq + grp_blk0(c)), nt, c.nsm, c.d_sm_ctr + (int64_t)g * (c.nsm + 1));
+      return;
+    }
+  }
   if constexpr (V == 8) smem_optin(k_cg_spmv<8>, spmv_smem(c));
   launch_pdl(c, k_cg_spmv<V>, (unsigned)grp_nblk(c), V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
              sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,

@@ -1,0 +1,8 @@
+OSM_PERSIST=1 timeout 900 python -m pytest tests/test_gpu_variants.py tests/test_gpu_matrix_free.py -m gpu -x -q 2>&1 | tail -2
+for E in "OSM_PERSIST=0" "OSM_PERSIST=1"; do
+  env $E OSM_GROUPS=1 timeout 300 python tools/cg_bench.py --solves 2 --timing | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$E', {k:round(v['us_per_launch'],2) for k,v in d['kernels'].items() if k in ('cg_spmv',)}, d['h'])"
+  env $E OSM_GROUPS=1 timeout 300 python tools/cg_bench.py --solves 2 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$E g1', [round(x,4) for x in d['seconds']])"
+  env $E timeout 300 python tools/cg_bench.py --solves 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$E', [round(x,4) for x in d['seconds']])"
+  env $E OSM_SORT=4 OSM_SPMV=5 OSM_GROUPS=1 timeout 300 python tools/cg_bench.py --solves 2 --timing | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$E MF', {k:round(v['us_per_launch'],2) for k,v in d['kernels'].items() if k in ('cg_spmv',)})"
+  env $E OSM_SORT=4 OSM_SPMV=5 timeout 300 python tools/cg_bench.py --solves 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$E MF', [round(x,4) for x in d['seconds']])"
+done

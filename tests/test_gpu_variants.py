@@ -105,3 +105,30 @@ def test_subdomain_group_streams_bitwise(groups):
         o.close()
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+def test_sm_affine_persistent_spmv_bitwise(monkeypatch):
+    """OSM_PERSIST=1 (experimental SM-affine persistent SpMV, variants 5 and 6): every tile is computed as
+    in k_cg_spmv, only the tile-to-block schedule changes, so the iterations are bitwise identical."""
+    import paper_2112_03851_b200 as P
+
+    cfg = dict(nx=12, ny=6, nz=5, lx=1.0, ly=0.7, lz=0.5, order=2, nsub=3)
+    drho = synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=53)
+    out = {}
+    for persist in ("0", "1"):
+        monkeypatch.setenv("OSM_PERSIST", persist)
+        for order, v in ((3, 6), (4, 5)):
+            o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+            o.set_row_order(order)
+            o.decompose(cfg["nsub"])
+            o.set_robin([10.0] * 2, [3.0] * 2)
+            o.assemble()
+            assert o.set_spmv_variant(v) == v
+            o.upload_density(drho)
+            st, _ = o.solve(tol_outer=1e-8, max_outer=300)
+            assert st == 0
+            out[(persist, v)] = (o.history(), o.inner_iters(), o.solution())
+            o.close()
+    for v in (6, 5):
+        a, b = out[("0", v)], out[("1", v)]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])

@@ -312,8 +312,9 @@ def main():
                 "dram_gbs_from_ncu_traffic": (tr / (1e-3 * spmv_ms / max(1, spmv_launches)) / 1e9
                                               if tr and spmv_ms > 0 else None),
                 "exchange": exchange_block(kt, tm, world),
-                "limiter": "L1/TEX gather path and issue, not HBM (ncu: l1tex 59% of peak, issue 51%, dram 48%; "
-                           "profiles/r01g_ncu_summary.md)"}
+                "limiter": "latency of the dependent load chains (packed entry -> x gather -> FMA), not HBM, L2 or "
+                           "the L1 pipes (ncu: l1tex 59% of peak, issue 51%, dram 48%, xbar->L1 25%; "
+                           "profiles/r01m_ncu_summary.md; DESIGN.md 'SM-affine persistent SpMV')"}
 
     # Whole PCG hot loop against the HBM roofline: algorithmic bytes of the three CG kernels (SpMV in
     # its own format + update + direction) of one solve, over the timed step (everything included).
@@ -436,7 +437,8 @@ def run_batched_alpha(P, stream, torch, B=25, N=30, reps=2):
 def run_matrix_free(P, args, cfg, d_drho, stream, peak, torch):
     """Time the matrix-free SpMV path (variant 5 in row order 4) on the headline workload: K timed
     steps after W warm-ups (CUDA events on the library stream), then one instrumented solve for the
-    per-launch SpMV time.  Its algorithmic SpMV bytes are only p (read) and q (written): 16 B/row."""
+    per-launch SpMV time.  Its algorithmic SpMV bytes are p (read), q (written) and the 1-byte row
+    table code: 17 B/row."""
     S = cfg["nsub"]
     mf = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"],
                stream=stream.cuda_stream)
@@ -475,10 +477,10 @@ def run_matrix_free(P, args, cfg, d_drho, stream, peak, torch):
             "time_to_tol_s": ms / args.steps / 1e3, "outer_iters": outer / args.steps,
             "spmv_us_per_launch": 1e3 * t / max(1, n),
             "spmv_share_of_cg_time": t / sum(kt[k][1] for k in ("cg_spmv", "cg_update", "cg_dir")),
-            "roofline": {"bound": "l1/issue", "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "latency", "achieved": gbs, "peak": peak, "unit": "GB/s",
                          "frac": gbs / peak if gbs else None,
-                         "note": "algorithmic bytes = 16 B/row (p read, q write): no matrix bytes, so the "
-                                 "kernel is bound by the L1 gather path and instruction issue, not HBM"},
+                         "note": "algorithmic bytes = 17 B/row (p read, q write, 1-byte row code): no matrix "
+                                 "bytes, so the kernel is bound by the latency of its gather chains, not HBM"},
             "csr_equivalent_gbs": tm["csr_equiv_bytes"] / (t / 1e3) / 1e9 if t > 0 else None,
             "cg_kernels_us": {k: 1e3 * v[1] / max(1, v[0]) for k, v in kt.items()}}
 

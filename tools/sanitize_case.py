@@ -1,6 +1,7 @@
 """Small driver covering every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck):
-GPU assembly + value-indexed build, all five SpMV variants on an OO2 3-subdomain P2 solve, the NCCL
-path (forced remote), the batched-alpha solver, gravity, and the C1 smoke case."""
+GPU assembly + value-indexed build, every SpMV variant (0-4 and 6 in row order 3; 5, 8 and 9 in row
+order 4; 5 and 6 with the SM-affine persistent schedule) on an OO2 3-subdomain P2 solve, the NCCL path
+(forced remote), the batched-alpha solver, gravity, and the C1 smoke case."""
 import os
 import sys
 
@@ -22,6 +23,19 @@ for v in (0, 1, 2, 3, 4):
     assert st == 0, (v, st)
     o.gravity_z(0.3)
     o.close()
+for order, v, persist in ((3, 6, "0"), (4, 5, "0"), (4, 8, "0"), (4, 9, "0"), (3, 6, "1"), (4, 5, "1")):
+    os.environ["OSM_PERSIST"] = persist
+    o = P.Osm(6, 5, 4, 1.0, 0.8, 0.6, 2)
+    o.set_row_order(order)
+    o.decompose(3)
+    o.set_robin2(10.0, 0.05, 4.0, 0.2)
+    o.assemble()
+    assert o.set_spmv_variant(v) == v, (order, v)
+    o.upload_density(drho)
+    st, rep = o.solve(max_outer=200)
+    assert st == 0, (order, v, persist, st)
+    o.close()
+os.environ.pop("OSM_PERSIST")
 os.environ["OSM_FORCE_REMOTE"] = "1"
 o = P.Osm(6, 5, 4, 1.0, 0.8, 0.6, 2)
 os.environ.pop("OSM_FORCE_REMOTE")

@@ -286,16 +286,36 @@ __device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, con
 // Variant 4: variant 3 with the dictionary staged in shared memory at block start (dictionary
 // lookups leave the L1 tag path; used when the dictionary fits kSmemDict entries).
 constexpr int kSmemDict = 2048;
+
+// Loads of a tile that touch only static data (the matrix copy, the block -> subdomain map, row codes).
+// k_cg_spmv issues them before griddepcontrol.wait, so they overlap the tail of the previous kernel.
+struct TilePre {
+  int ls = 0;                    // local subdomain of the tile
+  int ng = 0;                    // value-indexed: packed groups of the tile
+  const uint32_t* gp = nullptr;  // value-indexed: this row's first packed group
+  uint4 e = {0u, 0u, 0u, 0u};    // value-indexed: that group
+  int tb = -1;                   // matrix-free: the row's table code (-1: decode the lattice point)
+};
+
 template <bool W = false>  // W: wide entries (12-bit index << 20 | 20-bit signed offset)
 __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                                   const double* sdict) {
+                                                   const double* sdict, const TilePre* pre = nullptr) {
   constexpr int T = kRowsPerBlock;
-  const int ng = (A.vtw[blk] + 3) >> 2;
-  const uint32_t* gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
+  int ng;
+  const uint32_t* gp;
+  uint4 e;
+  if (pre) {
+    ng = pre->ng;
+    gp = pre->gp;
+    e = pre->e;
+  } else {
+    ng = (A.vtw[blk] + 3) >> 2;
+    gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
+    if (ng > 0) e = ld_stream4(gp);
+  }
   const double* xr = x + blk * T + threadIdx.x;
   double s = 0.0;
   if (ng == 0) return s;
-  uint4 e = ld_stream4(gp);
   for (int g = 0; g < ng; ++g) {
     double x0, x1, x2, x3, v0, v1, v2, v3;
     if constexpr (W) {
@@ -332,12 +352,12 @@ __device__ __forceinline__ double tile_row_vi_smem(const SellDev& A, int64_t blk
 // iterations).  Table loads are warp-uniform (one broadcast per group); the x gathers of a warp
 // are 32 consecutive rows shifted by one offset: coalesced, with no column indices read.
 __device__ __forceinline__ double tile_row_mf(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                              const MfConst& P) {
+                                              const MfConst& P, const TilePre* pre = nullptr) {
   const int64_t ri = blk * kRowsPerBlock + threadIdx.x;
   double s = 0.0;
 #ifndef OSM_MF_NOCODE
   if (P.valid && A.mf_code) {  // the row's 1-byte table code instead of its lattice arithmetic
-    const int tb = __ldg(A.mf_code + ri);
+    const int tb = pre && pre->tb >= 0 ? pre->tb : __ldg(A.mf_code + ri);
     if (tb == 0xff) return s;  // dummy row (Dirichlet or padding point): like a SELL padding row
     const double* xr = x + ri;
     asm("" : "+l"(xr));
@@ -502,15 +522,39 @@ __device__ __forceinline__ double tile_row_mf_win(const SellDev& A, int64_t blk,
 // V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers);
 // V = 4: value-indexed rows, dictionary in shared memory; V = 5: matrix-free Kuhn stencil.
 template <int V>
+__device__ __forceinline__ TilePre tile_pre(const SellDev& A, const int32_t* __restrict__ blk_sub, int64_t blk,
+                                            const MfArg<V>& mf) {
+  TilePre t;
+  // volatile loads: the compiler must not sink them below the griddepcontrol.wait that follows
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(t.ls) : "l"(blk_sub + blk));
+  if constexpr (V == 6 || V == 7) {
+    t.ng = (A.vtw[blk] + 3) >> 2;
+    t.gp = A.packed + A.poff[blk] + 4 * threadIdx.x;
+    if (t.ng > 0)
+      asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(t.e.x), "=r"(t.e.y), "=r"(t.e.z), "=r"(t.e.w)
+                   : "l"(t.gp));
+  }
+  if constexpr (V == 5) {
+    if (mf.c.valid && A.mf_code) {
+      unsigned short c;
+      asm volatile("ld.global.u8 %0, [%1];" : "=h"(c) : "l"(A.mf_code + blk * kRowsPerBlock + threadIdx.x));
+      t.tb = c;
+    }
+  }
+  return t;
+}
+
+template <int V>
 __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                           unsigned char* smem, const MfArg<V>& mf) {
+                                           unsigned char* smem, const MfArg<V>& mf, const TilePre* pre = nullptr) {
   if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
-  if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c);
+  if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c, pre);
   if constexpr (V == 8) return tile_row_mf_win(A, blk, x, mf.c, smem);
   if constexpr (V == 9) return tile_row_dia(A, blk, x, mf.c);
-  if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict);
-  if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict);
+  if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict, pre);
+  if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict, pre);
   if constexpr (V == 4) {
     double* sd = reinterpret_cast<double*>(smem);
     for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];
@@ -529,15 +573,15 @@ __device__ __forceinline__ void spmv_tile(const SellDev& A, int64_t blk, const i
                                           SubState* __restrict__ st, const double* __restrict__ p,
                                           double* __restrict__ q, double* __restrict__ part, int64_t stride,
                                           int32_t* __restrict__ nactive, const MfArg<V>& mf, double* sm,
-                                          unsigned char* dsm) {
-  const int ls = blk_sub[blk];
+                                          unsigned char* dsm, const TilePre& pre) {
+  const int ls = pre.ls;
   if (!st[ls].active) {  // the previous direction kernel has paid the stopped subdomain's x update
     if (threadIdx.x == 0 && blk == st[ls].blk0) st[ls].xpend = 0;
     return;
   }
   const bool has_row = threadIdx.x < kRowsPerBlock;
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double y = tile_row<V>(A, blk, p, dsm, mf);
+  const double y = tile_row<V>(A, blk, p, dsm, mf, &pre);
   double v[1] = {0.0};
   if (has_row) {
     q[row] = y;
@@ -571,8 +615,10 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
   constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
   __shared__ double sm[NW * 1];
   extern __shared__ __align__(128) unsigned char dsm[];
+  const int64_t blk = blockIdx.x + blk_base;
+  const TilePre pre = tile_pre<V>(A, blk_sub, blk, mf);  // static data: before the dependency wait
   pdl_enter();
-  spmv_tile<V, NW>(A, blockIdx.x + blk_base, blk_sub, st, p, q, part, stride, nactive, mf, sm, dsm);
+  spmv_tile<V, NW>(A, blk, blk_sub, st, p, q, part, stride, nactive, mf, sm, dsm, pre);
 }
 
 // SM-affine persistent SpMV (experimental, OSM_PERSIST=1).  The group's tiles, in region-major /
@@ -608,7 +654,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_cg_spmv_sm(SellDev A, const int
       // the next tile's counter bump is in flight while this tile runs (thread 0 waits on it at the end)
       unsigned nxt = 0;
       if (threadIdx.x == 0) nxt = atomicAdd(&ctr[s], 1u);
-      spmv_tile<V, NW>(A, seq[pos], blk_sub, st, p, q, part, stride, nactive, mf, sm, nullptr);
+      const int64_t blk = seq[pos];
+      spmv_tile<V, NW>(A, blk, blk_sub, st, p, q, part, stride, nactive, mf, sm, nullptr,
+                       tile_pre<V>(A, blk_sub, blk, mf));
       __syncthreads();  // every thread has read pos_sh
       if (threadIdx.x == 0) pos_sh = b + (int)nxt;
       __syncthreads();

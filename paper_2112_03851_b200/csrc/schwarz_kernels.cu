@@ -698,6 +698,24 @@ __device__ __forceinline__ double2 mf_dinv2(uint16_t cc, const MfConst& P) {
   return make_double2(c0 != 0xff ? P.dinv[c0] : 0.0, c1 != 0xff ? P.dinv[c1] : 0.0);
 }
 
+// Loads of static vector data (D^{-1}, row codes) that the vector kernels issue before
+// griddepcontrol.wait; volatile and coherent, so ptxas keeps them above the wait.
+__device__ __forceinline__ double2 ld_pre2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint16_t ld_pre_u16(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.global.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_pre_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 template <int MINB, int V>
 __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* __restrict__ vblk_sub,
                                                            const int32_t* __restrict__ vblk_tile0,
@@ -711,30 +729,31 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
                                                            const __grid_constant__ MfArg<V> mf, int64_t vb_base) {
   constexpr bool MF = V == 5;
   __shared__ double sm[(kVecThreads / 32) * 2];
-  pdl_enter();
   const int64_t vb = blockIdx.x + vb_base;
-  const int ls = vblk_sub[vb];
-  if (!st[ls].active) return;
-  const int nt = vblk_ntile[vb];
-  const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;  // row-pair index
-  const double a = st[ls].alpha;
+  // static data first (block map, D^{-1} or row codes): issued before the dependency wait
+  const int ls = ld_pre_s32(vblk_sub + vb);
+  const int nt = ld_pre_s32(vblk_ntile + vb);
+  const int64_t p0 = (int64_t)ld_pre_s32(vblk_tile0 + vb) * kVecThreads + threadIdx.x;  // row-pair index
   double2 qv[kVecTiles], rv[kVecTiles], dv[kVecTiles];
   bool real[kVecTiles];
   uint16_t cc[kVecTiles];
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j) {
     real[j] = j < nt;
-    if constexpr (MF) {  // codes load alongside the vectors; D^{-1} is looked up after
-      if (j < nt) cc[j] = __ldg(reinterpret_cast<const uint16_t*>(mcode) + p0 + (int64_t)j * kVecThreads);
+    if (j < nt) {
+      if constexpr (MF) cc[j] = ld_pre_u16(mcode + 2 * (p0 + (int64_t)j * kVecThreads));
+      else dv[j] = ld_pre2(dinv + 2 * (p0 + (int64_t)j * kVecThreads));
     }
   }
+  pdl_enter();
+  if (!st[ls].active) return;
+  const double a = st[ls].alpha;
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
       qv[j] = reinterpret_cast<const double2*>(q)[i2];
       rv[j] = reinterpret_cast<const double2*>(r)[i2];
-      if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
     }
   if constexpr (MF) {
 #pragma unroll
@@ -792,34 +811,33 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restric
                                                         double* __restrict__ x, const uint8_t* __restrict__ mcode,
                                                         const __grid_constant__ MfArg<V> mf, int64_t vb_base) {
   constexpr bool MF = V == 5;
-  pdl_enter();
   const int64_t vb = blockIdx.x + vb_base;
-  const int ls = vblk_sub[vb];
-  const bool act = st[ls].active;
-  if (!act && !st[ls].xpend) return;  // stopped in this iteration's update: only x += alpha p is owed
-  const int nt = vblk_ntile[vb];
-  const int64_t p0 = (int64_t)vblk_tile0[vb] * kVecThreads + threadIdx.x;
-  const double beta = st[ls].beta, a = st[ls].alpha;
+  // static data first (block map, D^{-1} or row codes): issued before the dependency wait
+  const int ls = ld_pre_s32(vblk_sub + vb);
+  const int nt = ld_pre_s32(vblk_ntile + vb);
+  const int64_t p0 = (int64_t)ld_pre_s32(vblk_tile0 + vb) * kVecThreads + threadIdx.x;
   double2 rv[kVecTiles], dv[kVecTiles], pv[kVecTiles], xv[kVecTiles];
   bool real[kVecTiles];
   uint16_t cc[kVecTiles];
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j) {
     real[j] = j < nt;
-    if constexpr (MF) {  // codes load alongside the vectors; D^{-1} is looked up after
-      if (act && j < nt) cc[j] = __ldg(reinterpret_cast<const uint16_t*>(mcode) + p0 + (int64_t)j * kVecThreads);
+    if (j < nt) {
+      if constexpr (MF) cc[j] = ld_pre_u16(mcode + 2 * (p0 + (int64_t)j * kVecThreads));
+      else dv[j] = ld_pre2(dinv + 2 * (p0 + (int64_t)j * kVecThreads));
     }
   }
+  pdl_enter();
+  const bool act = st[ls].active;
+  if (!act && !st[ls].xpend) return;  // stopped in this iteration's update: only x += alpha p is owed
+  const double beta = st[ls].beta, a = st[ls].alpha;
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
       const int64_t i2 = p0 + (int64_t)j * kVecThreads;
       pv[j] = reinterpret_cast<const double2*>(p)[i2];
       xv[j] = reinterpret_cast<const double2*>(x)[i2];
-      if (act) {
-        rv[j] = reinterpret_cast<const double2*>(r)[i2];
-        if constexpr (!MF) dv[j] = reinterpret_cast<const double2*>(dinv)[i2];
-      }
+      if (act) rv[j] = reinterpret_cast<const double2*>(r)[i2];
     }
   if constexpr (MF) {
     if (act) {

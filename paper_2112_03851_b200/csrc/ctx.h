@@ -394,6 +394,11 @@ struct Ctx {
   bool dia_ok = false;
   std::vector<double> dia_sub_bytes;  // variant 9 bytes read per SpMV per local subdomain (traffic model)
   uint8_t* d_mf_code = nullptr;   // per internal row: deduplicated table id, 0xff dummy (vector kernels)
+  // D^{-1} codes (osm.cu dcode_build): per row a 1-byte index into the distinct D^{-1} values (0xff:
+  // +0.0, padding rows), so the SELL-path vector kernels read 1 byte instead of 8 per row
+  bool dcode_on = true;           // OSM_DCODE=0 keeps the 8-byte D^{-1} stream
+  uint8_t* d_dcode = nullptr;
+  std::vector<double> h_dcode_tab;  // empty: codes not built (too many distinct values)
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;

@@ -179,6 +179,8 @@ static void free_assembly(Ctx& c) {
   dfree(c.d_mf_win);
   c.mf_win_rows = 0;
   dfree(c.d_mf_code);
+  dfree(c.d_dcode);
+  c.h_dcode_tab.clear();
   dia_free(c);
   c.assembled = false;
   c.density_set = false;
@@ -329,6 +331,38 @@ static void mf_refresh(Ctx& c) {
   } else {
     dfree(c.d_mf_code);
   }
+}
+
+// D^{-1} codes for the vector kernels of the SELL variants.  On the structured mesh the Robin-folded
+// diagonal takes a few distinct values (row kind x parity class), so each row's D^{-1} is replaced by a
+// 1-byte index into a table of its distinct bit patterns (the same doubles: iterations stay bitwise).
+// More than 255 distinct values: no codes, the 8-byte stream stays.  Rebuilt after every Robin fold.
+static void dcode_build(Ctx& c) {
+  c.h_dcode_tab.clear();
+  if (!c.dcode_on || c.nrows_total == 0 || c.nrows_total % 2) return;
+  std::vector<double> dv((size_t)c.nrows_total);
+  OSM_CUDA(cudaMemcpy(dv.data(), c.dinv, sizeof(double) * dv.size(), cudaMemcpyDeviceToHost));
+  std::map<uint64_t, int> idx;
+  std::vector<double> tab;
+  std::vector<uint8_t> code(dv.size());
+  for (size_t i = 0; i < dv.size(); ++i) {
+    uint64_t bits;
+    std::memcpy(&bits, &dv[i], 8);
+    if (bits == 0) {  // +0.0 (padding rows): 0xff decodes to +0.0
+      code[i] = 0xff;
+      continue;
+    }
+    auto it = idx.find(bits);
+    if (it == idx.end()) {
+      if ((int)tab.size() >= kMfMaxTab) return;  // too many distinct values: keep the stream
+      it = idx.emplace(bits, (int)tab.size()).first;
+      tab.push_back(dv[i]);
+    }
+    code[i] = (uint8_t)it->second;
+  }
+  if (!c.d_dcode) c.d_dcode = dalloc<uint8_t>(c.nrows_total);
+  OSM_CUDA(cudaMemcpy(c.d_dcode, code.data(), code.size(), cudaMemcpyHostToDevice));
+  c.h_dcode_tab = tab;
 }
 
 static void dia_free(Ctx& c) {
@@ -879,6 +913,7 @@ static void apply_robin(Ctx& c) {
   if (!c.robin_dirty) return;
   const int nsides = (int)c.sides.size();
   if (nsides == 0) {
+    dcode_build(c);
     c.robin_dirty = false;
     return;
   }
@@ -908,6 +943,7 @@ static void apply_robin(Ctx& c) {
   dfree(d_q);
   vi_apply_robin(c, a, qv);
   vi_sync_host_dict(c);
+  dcode_build(c);
   if (c.sort_key == 4) dia_build(c);
   if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
   c.robin_dirty = false;
@@ -1213,8 +1249,11 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
                           : dia ? c.dia_sub_bytes[ls] : (vi ? 4.0 * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
-    c.traffic[1] += (double)its * 32.0 * S.n;  // update: read r, q, D^-1; write r
-    c.traffic[2] += (double)its * 48.0 * S.n;  // direction: read r, D^-1, p, x; write p, x
+    // D^-1 as an 8-byte stream, or as a 1-byte code (table codes of variant 5, dcode_build otherwise)
+    const bool coded = mf ? c.d_mf_code != nullptr : !c.h_dcode_tab.empty();
+    const double db = coded ? 1.0 : 8.0;
+    c.traffic[1] += (double)its * (24.0 + db) * S.n;  // update: read r, q, D^-1; write r
+    c.traffic[2] += (double)its * (40.0 + db) * S.n;  // direction: read r, D^-1, p, x; write p, x
     c.traffic[3] += (double)(S.sell_entries - S.nnz);
     c.traffic[4] += (double)S.nnz;
     c.traffic[5] += (double)S.n;
@@ -1325,6 +1364,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);
     if (const char* e = std::getenv("OSM_UPD")) c.update_variant = std::atoi(e);
     if (const char* e = std::getenv("OSM_SORT")) c.sort_key = std::atoi(e);
+    if (const char* e = std::getenv("OSM_DCODE")) c.dcode_on = std::atoi(e) != 0;
     spmv_init_attributes();
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "exchange"};

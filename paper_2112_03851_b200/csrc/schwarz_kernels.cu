@@ -1217,39 +1217,53 @@ static bool mf_vectors(const Ctx& c) {
   return (v == 5 || v == 8) && c.h_mf_const && c.h_mf_const->valid && c.d_mf_code;
 }
 
+// SELL variants with D^{-1} codes (osm.cu dcode_build): the vector kernels' table path (V = 5) with the
+// codes of the distinct D^{-1} values in place of the matrix-free table codes.
+static bool dcode_vectors(const Ctx& c) { return !c.h_dcode_tab.empty() && c.d_dcode; }
+static MfArg<5> dcode_arg(const Ctx& c) {
+  MfArg<5> a{};
+  a.c.valid = 1;
+  std::copy(c.h_dcode_tab.begin(), c.h_dcode_tab.end(), a.c.dinv);
+  return a;
+}
+
 template <int MINB, int V>
-static void cg_update_v(Ctx& c, double tol, int maxit) {
+static void cg_update_v(Ctx& c, double tol, int maxit, const uint8_t* code, const MfArg<V>& mf) {
   launch_pdl(c, k_cg_update<MINB, V>, (unsigned)grp_nvb(c), kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
              (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
-             (const double*)c.q, (const double*)c.dinv, c.part_upd, c.nvblk_total, tol, maxit, c.d_nactive,
-             (const uint8_t*)c.d_mf_code, mf_arg<V>(c), grp_vb0(c));
+             (const double*)c.q, (const double*)c.dinv, c.part_upd, c.nvblk_total, tol, maxit, c.d_nactive, code,
+             mf, grp_vb0(c));
 }
 
 void launch_cg_update(Ctx& c, double tol, int maxit) {
   timer_begin(c, T_UPDATE);
   if (mf_vectors(c))
-    cg_update_v<1, 5>(c, tol, maxit);
+    cg_update_v<1, 5>(c, tol, maxit, c.d_mf_code, mf_arg<5>(c));
+  else if (dcode_vectors(c))
+    cg_update_v<1, 5>(c, tol, maxit, c.d_dcode, dcode_arg(c));
   else if (c.update_variant == 1)
-    cg_update_v<8, 0>(c, tol, maxit);
+    cg_update_v<8, 0>(c, tol, maxit, nullptr, mf_arg<0>(c));
   else
-    cg_update_v<1, 0>(c, tol, maxit);
+    cg_update_v<1, 0>(c, tol, maxit, nullptr, mf_arg<0>(c));
   ++c.launches;
   timer_end(c, T_UPDATE);
 }
 
 template <int V>
-static void cg_dir_v(Ctx& c) {
+static void cg_dir_v(Ctx& c, const uint8_t* code, const MfArg<V>& mf) {
   launch_pdl(c, k_cg_dir<V>, (unsigned)grp_nvb(c), kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
              (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, (const SubState*)c.st, (const double*)c.r,
-             (const double*)c.dinv, c.p, c.x, (const uint8_t*)c.d_mf_code, mf_arg<V>(c), grp_vb0(c));
+             (const double*)c.dinv, c.p, c.x, code, mf, grp_vb0(c));
 }
 
 void launch_cg_dir(Ctx& c) {
   timer_begin(c, T_DIR);
   if (mf_vectors(c))
-    cg_dir_v<5>(c);
+    cg_dir_v<5>(c, c.d_mf_code, mf_arg<5>(c));
+  else if (dcode_vectors(c))
+    cg_dir_v<5>(c, c.d_dcode, dcode_arg(c));
   else
-    cg_dir_v<0>(c);
+    cg_dir_v<0>(c, nullptr, mf_arg<0>(c));
   ++c.launches;
   timer_end(c, T_DIR);
 }

@@ -16,18 +16,20 @@ pytestmark = pytest.mark.gpu
 CFG = dict(nx=8, ny=5, nz=4, lx=1.0, ly=0.7, lz=0.5, order=2, nsub=3)
 
 
-def _run(variant, drho, robin):
+def _run(variant, drho, robin, dcode=1):
     import paper_2112_03851_b200 as P
 
-    old = os.environ.get("OSM_SPMV")
-    os.environ["OSM_SPMV"] = str(variant)
+    env = {"OSM_SPMV": str(variant), "OSM_DCODE": str(dcode)}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
     finally:
-        if old is None:
-            del os.environ["OSM_SPMV"]
-        else:
-            os.environ["OSM_SPMV"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
     o.decompose(CFG["nsub"])
     o.set_robin2(*robin)
     o.assemble()
@@ -39,8 +41,9 @@ def _run(variant, drho, robin):
     o.set_robin2(robin[0] * 2, robin[1], robin[2], robin[3] * 0.5)
     st2, _ = o.solve(tol_outer=1e-8, max_outer=300)
     h2 = o.history()
+    tm = o.traffic_model()
     o.close()
-    return st, h, u, st2, h2
+    return st, h, u, st2, h2, tm
 
 
 @pytest.mark.parametrize("robin", [(10.0, 0.0, 3.0, 0.0), (10.0, 0.05, 3.0, 0.2)])
@@ -132,3 +135,21 @@ def test_sm_affine_persistent_spmv_bitwise(monkeypatch):
     for v in (6, 5):
         a, b = out[("0", v)], out[("1", v)]
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+@pytest.mark.parametrize("variant", [2, 6])
+def test_dinv_codes_bitwise_identical(variant):
+    """The vector kernels' 1-byte D^-1 codes (osm.cu dcode_build) hold the same doubles as the 8-byte
+    D^-1 stream (OSM_DCODE=0), so the histories and solutions are bitwise equal, also after the
+    Robin coefficients change (the codes are rebuilt after every fold)."""
+    drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=23)
+    robin = (10.0, 0.05, 3.0, 0.2)
+    a = _run(variant, drho, robin, dcode=1)
+    b = _run(variant, drho, robin, dcode=0)
+    assert a[0] == b[0] == 0 and a[3] == b[3] == 0
+    assert np.array_equal(a[1], b[1])
+    for x, y in zip(a[2], b[2]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[4], b[4])
+    # the coded run really read codes: update bytes 25 vs 32 per row and iteration
+    assert a[5]["update_bytes"] / b[5]["update_bytes"] == pytest.approx(25.0 / 32.0)

@@ -281,8 +281,10 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row
  * order 4, see osm_set_row_order).  Variants 3/4/6 fall back to 2 when the matrix does not
  * admit the value-indexed copy (6 to 3 beyond 2048 values); 5 falls back to 4 without row order 4
- * or when a slab is too thin for the tables.  *active (may be NULL) receives the variant that will actually run.  INVALID_ARG
- * outside 0..9. */
+ * or when a slab is too thin for the tables.  10 (experimental): 3-byte value-indexed entries (an
+ * int16 offset stream and a u8 dictionary-index stream, 8 entries per group; needs <= 256 dictionary
+ * slots and 16-bit offsets, else falls back to 6).  *active (may be NULL) receives the variant that
+ * will actually run.  INVALID_ARG outside 0..10. */
 osm_status osm_set_spmv_variant(osm_ctx* ctx, int variant, int* active);
 
 /* Internal row order of the GPU copy (a permutation private to the library; results are

@@ -128,6 +128,10 @@ template <>
 struct MfArg<7> {  // variant 6 on the wide (20-bit offset) entries
   double dict[kCDict];
 };
+template <>
+struct MfArg<10> {  // variant 10: 3-byte entries, at most 256 dictionary slots
+  double dict[256];
+};
 // Variant 9: value-indexed rows with implicit column offsets (row order 4).  Every row of a
 // (subdomain, kind, class) has its nonzeros at the same internal row offsets, so a row stores only
 // its 16-bit dictionary indices, one per slot of its stencil's offset list (4 slots per 8-byte
@@ -167,6 +171,9 @@ struct SellDev {
   const uint8_t* mf_code;   // per row: deduplicated table id of the constant-bank tables, 0xff dummy row
   const uint2* dia_idx;     // variant 9: per tile, group g of row r at dia_off[tile] + 256 g + r (4 x u16)
   const int64_t* dia_off;
+  const uint4* vi3_off;     // variant 10: 8 int16 offsets per group
+  const uint2* vi3_idx;     //   8 u8 dictionary indices per group
+  const int64_t* vi3_base;  //   per tile: first group slot
 };
 
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
@@ -418,6 +425,13 @@ struct Ctx {
   };
   std::vector<FoldTuple> vi_fold_tuples;
   std::vector<double> h_vi_dict;  // host copy of the dictionary (variant 6 kernel parameter)
+  // variant 10 (experimental): 3-byte entries, 8 per group: int16 offsets (uint4) + u8 dictionary
+  // indices (uint2) in two streams; group G of row r of tile t at vi3_base[t] + 256 G + r
+  bool vi3_ok = false;
+  uint4* vi3_off = nullptr;
+  uint2* vi3_idx = nullptr;
+  int64_t* vi3_base = nullptr;
+  int64_t vi3_groups = 0;
 
   // instrumentation
   bool timing = false;

@@ -1235,7 +1235,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   c.traffic[7] = c.exch_bytes;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
-  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7, mf = sv == 5 || sv == 8, dia = sv == 9;
+  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7 || sv == 10, mf = sv == 5 || sv == 8, dia = sv == 9;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1246,7 +1246,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     const double kept = ls < (int)c.vi_kept.size() ? (double)c.vi_kept[ls] : (double)S.nnz;
     // (variant 5 reads a 1-byte table code per row; variant 9 its 8-byte index groups and the code)
     const double mat = mf ? (c.d_mf_code ? (double)S.npad : 0.0)
-                          : dia ? c.dia_sub_bytes[ls] : (vi ? 4.0 * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
+                          : dia ? c.dia_sub_bytes[ls] : (vi ? (sv == 10 ? 3.0 : 4.0) * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
     // D^-1 as an 8-byte stream, or as a 1-byte code (table codes of variant 5, dcode_build otherwise)
@@ -1837,7 +1837,7 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 9) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..9");
+  if (v < 0 || v > 10) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..10");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);

@@ -161,7 +161,75 @@ void launch_dia_pack(Ctx& c, const int32_t* d_gbeg, const int32_t* d_delta, cons
   ++c.launches;
 }
 
+// Variant 10 (3-byte entries): regroups the 4-entry packed words (dict index << 16 | uint16 offset) into
+// 8-entry groups split in an offset stream and an index stream; entry order within a row is kept,
+// the odd tail group is padded with (0.0, offset 0) entries like the packed rows.
+__global__ void k_vi3_pack(const int32_t* __restrict__ tw, const int64_t* __restrict__ poff,
+                           const uint32_t* __restrict__ packed, const int64_t* __restrict__ base3, uint32_t zero_word,
+                           uint4* __restrict__ off3, uint2* __restrict__ idx3) {
+  const int64_t t = blockIdx.x;
+  const int r = threadIdx.x;
+  const int n4 = (tw[t] + 3) >> 2, n8 = (tw[t] + 7) >> 3;
+  for (int G = 0; G < n8; ++G) {
+    uint32_t w[8];
+    for (int h = 0; h < 2; ++h) {
+      const int g4 = 2 * G + h;
+      uint4 v = make_uint4(zero_word, zero_word, zero_word, zero_word);
+      if (g4 < n4) v = *reinterpret_cast<const uint4*>(packed + poff[t] + 4 * ((int64_t)kRowsPerBlock * g4 + r));
+      w[4 * h] = v.x;
+      w[4 * h + 1] = v.y;
+      w[4 * h + 2] = v.z;
+      w[4 * h + 3] = v.w;
+    }
+    uint4 o;
+    o.x = (w[0] & 0xffffu) | (w[1] << 16);
+    o.y = (w[2] & 0xffffu) | (w[3] << 16);
+    o.z = (w[4] & 0xffffu) | (w[5] << 16);
+    o.w = (w[6] & 0xffffu) | (w[7] << 16);
+    uint2 ix;
+    ix.x = (w[0] >> 16) | ((w[1] >> 16) << 8) | ((w[2] >> 16) << 16) | ((w[3] >> 16) << 24);
+    ix.y = (w[4] >> 16) | ((w[5] >> 16) << 8) | ((w[6] >> 16) << 16) | ((w[7] >> 16) << 24);
+    const int64_t at = base3[t] + (int64_t)kRowsPerBlock * G + r;
+    off3[at] = o;
+    idx3[at] = ix;
+  }
+}
+
+static void vi3_free(Ctx& c) {
+  if (c.vi3_off) cudaFree(c.vi3_off);
+  if (c.vi3_idx) cudaFree(c.vi3_idx);
+  if (c.vi3_base) cudaFree(c.vi3_base);
+  c.vi3_off = nullptr;
+  c.vi3_idx = nullptr;
+  c.vi3_base = nullptr;
+  c.vi3_ok = false;
+  c.vi3_groups = 0;
+}
+
+static void vi3_build(Ctx& c, const std::vector<int32_t>& tw, uint32_t zero_idx) {
+  vi3_free(c);
+  if (c.vi_wide || c.vi_ndict > 256) return;
+  std::vector<int64_t> base(c.nblk_total);
+  int64_t groups = 0;
+  for (int64_t t = 0; t < c.nblk_total; ++t) {
+    base[t] = groups;
+    groups += (int64_t)((tw[t] + 7) >> 3) * kRowsPerBlock;
+  }
+  OSM_CUDA(cudaMalloc(&c.vi3_base, sizeof(int64_t) * c.nblk_total));
+  OSM_CUDA(cudaMemcpy(c.vi3_base, base.data(), sizeof(int64_t) * c.nblk_total, cudaMemcpyHostToDevice));
+  OSM_CUDA(cudaMalloc(&c.vi3_off, sizeof(uint4) * std::max<int64_t>(1, groups)));
+  OSM_CUDA(cudaMalloc(&c.vi3_idx, sizeof(uint2) * std::max<int64_t>(1, groups)));
+  k_vi3_pack<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(c.vi_tw, c.vi_poff, c.vi_packed, c.vi3_base,
+                                                                     zero_idx << 16, c.vi3_off, c.vi3_idx);
+  OSM_CHECK_LAUNCH();
+  ++c.launches;
+  OSM_CUDA(cudaStreamSynchronize(c.stream));
+  c.vi3_groups = groups;
+  c.vi3_ok = true;
+}
+
 void vi_free(Ctx& c) {
+  vi3_free(c);
   if (c.vi_idx) cudaFree(c.vi_idx);
   if (c.vi_dict) cudaFree(c.vi_dict);
   if (c.vi_packed) cudaFree(c.vi_packed);
@@ -324,6 +392,7 @@ void vi_build(Ctx& c, bool per_side) {
   c.vi_per_side = per_side;
   c.vi_wide = wide;
   c.vi_ok = true;
+  vi3_build(c, tw, zero_idx);
 }
 
 // Dictionary tail for the current Robin coefficients: value = K^N + (p m + q s), rounded exactly

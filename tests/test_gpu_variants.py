@@ -50,7 +50,7 @@ def _run(variant, drho, robin, dcode=1):
 def test_variants_bitwise_identical(robin):
     drho = synth.random_field(CFG["nx"], CFG["ny"], CFG["nz"], seed=17)
     ref = _run(2, drho, robin)
-    for v in (0, 1, 3, 4, 6, 7):
+    for v in (0, 1, 3, 4, 6, 7, 10):
         got = _run(v, drho, robin)
         assert got[0] == ref[0] == 0
         assert np.array_equal(got[1], ref[1]), f"variant {v} history differs"

@@ -305,8 +305,11 @@ def main():
                                    for k, b in (("cg_update", "update_bytes"), ("cg_dir", "dir_bytes"))},
                 "kernel_ms": {k: v[1] for k, v in kt.items()}, "kernel_launches": {k: v[0] for k, v in kt.items()},
                 "us_per_launch": 1e3 * spmv_ms / max(1, spmv_launches),
-                "format": "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
-                          "offset) + 16 B per row (p, q); dictionary in the constant bank (kernel parameter)",
+                "format": ("value-indexed SELL-256, 3-byte entries: per 8 entries one 16-B load of int16 column "
+                           "offsets and one 8-B load of u8 dictionary indices, + 16 B per row (p, q); dictionary "
+                           "(<= 256 slots) in the constant bank (kernel parameter)" if default_variant == 10 else
+                           "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
+                           "offset) + 16 B per row (p, q); dictionary in the constant bank (kernel parameter)"),
                 "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
                 "frac_vs_spec_8000": achieved / SPEC_HBM_GBS if achieved else None,
                 "dram_gbs_from_ncu_traffic": (tr / (1e-3 * spmv_ms / max(1, spmv_launches)) / 1e9
@@ -403,8 +406,8 @@ def exchange_block(kt, tm, world):
 
 
 _rows = {}
-HOT_VARIANT = 6
-SPEC_HBM_GBS = 8000.0  # B200 HBM3e specification (SURVEY 8(d) reports against both)  # library default SpMV: value-indexed SELL-256, dictionary in the constant bank
+HOT_VARIANT = 10  # library default SpMV: value-indexed SELL-256 with 3-byte entries (falls back to 6, 7 or 2)
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e specification (SURVEY 8(d) reports against both)
 
 
 def run_batched_alpha(P, stream, torch, B=25, N=30, reps=2):

@@ -270,7 +270,7 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * 0 fp64 SELL-256, LDG rows; 1 fp64 SELL-256, warp-specialized cp.async.bulk pipeline;
  * 2 fp64 SELL-256, LDG rows at 32 registers; 3 value-indexed (16-bit dictionary index + 16-bit
  * column offset); 4 = 3 with the dictionary in shared memory; 6 = 3 with the dictionary in the
- * constant bank as a kernel parameter (default, up to 2048 distinct values); 7 = 6 on wide
+ * constant bank as a kernel parameter (up to 2048 distinct values); 7 = 6 on wide
  * entries (12-bit index, 20-bit offset), selected automatically when offsets exceed int16;
  * 8 = 5 with each tile's x window staged in shared memory by bulk copies (experimental, slower);
  * 9 value-indexed rows with implicit column offsets (row order 4: each row stores one 16-bit
@@ -281,7 +281,7 @@ osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, in
  * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row
  * order 4, see osm_set_row_order).  Variants 3/4/6 fall back to 2 when the matrix does not
  * admit the value-indexed copy (6 to 3 beyond 2048 values); 5 falls back to 4 without row order 4
- * or when a slab is too thin for the tables.  10 (experimental): 3-byte value-indexed entries (an
+ * or when a slab is too thin for the tables.  10 (default): 3-byte value-indexed entries (an
  * int16 offset stream and a u8 dictionary-index stream, 8 entries per group; needs <= 256 dictionary
  * slots and 16-bit offsets, else falls back to 6).  *active (may be NULL) receives the variant that
  * will actually run.  INVALID_ARG outside 0..10. */

@@ -372,13 +372,14 @@ struct Ctx {
                     // 3 class, length, then (K, I, J) with J fastest (default); 4: the matrix-free
                     // class-major lattice layout of MfSub (whole subdomain, dummy rows included)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
-  int spmv_variant = 6;  // 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
+  int spmv_variant = 10;  // default 10 (falls back to 6, 7, 3 or 2 when its format does not apply); 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
                          // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary
-                         // in shared memory (default; falls back to 3, then 2, when it does not apply),
+                         // in shared memory (falls back to 3, then 2, when it does not apply),
                          // 5: matrix-free Kuhn stencil (row order 4 only; else as 6), 6: 3 with the
-                         // dictionary in the constant bank (default; else 3), 7: 6 on wide entries
+                         // dictionary in the constant bank (else 3), 7: 6 on wide entries
                          // (chosen automatically when offsets need 20 bits), 8: 5 with the x window staged
-                         // in shared memory by bulk copies
+                         // in shared memory by bulk copies, 9: implicit offsets (experimental),
+                         // 10: 6 with 3-byte entries (int16 offset + u8 index streams; <= 256 slots)
 
   // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
   bool mf_ok = false;

@@ -294,6 +294,7 @@ struct TilePre {
   int ng = 0;                    // value-indexed: packed groups of the tile
   const uint32_t* gp = nullptr;  // value-indexed: this row's first packed group
   uint4 e = {0u, 0u, 0u, 0u};    // value-indexed: that group
+  uint2 e2 = {0u, 0u};           // variant 10: that group's dictionary indices
   int tb = -1;                   // matrix-free: the row's table code (-1: decode the lattice point)
 };
 
@@ -363,15 +364,22 @@ __device__ __forceinline__ uint4 ld_stream4u(const uint4* p) {
   return v;
 }
 __device__ __forceinline__ double tile_row_vi3(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                               const double* dict) {
+                                               const double* dict, const TilePre* pre = nullptr) {
   constexpr int T = kRowsPerBlock;
-  const int ng = (A.vtw[blk] + 7) >> 3;
+  const int ng = pre ? pre->ng : (A.vtw[blk] + 7) >> 3;
   const int64_t b = A.vi3_base[blk] + threadIdx.x;
   const double* xr = x + blk * T + threadIdx.x;
   double s = 0.0;
   if (ng == 0) return s;
-  uint4 o = ld_stream4u(A.vi3_off + b);
-  uint2 ix = ld_stream2u(A.vi3_idx + b);
+  uint4 o;
+  uint2 ix;
+  if (pre) {  // first group loaded before griddepcontrol.wait (tile_pre)
+    o = pre->e;
+    ix = pre->e2;
+  } else {
+    o = ld_stream4u(A.vi3_off + b);
+    ix = ld_stream2u(A.vi3_idx + b);
+  }
   for (int g = 0; g < ng; ++g) {
     const double x0 = __ldg(xr + (int16_t)(o.x & 0xffffu)), x1 = __ldg(xr + (int16_t)(o.x >> 16));
     const double x2 = __ldg(xr + (int16_t)(o.y & 0xffffu)), x3 = __ldg(xr + (int16_t)(o.y >> 16));
@@ -585,6 +593,18 @@ __device__ __forceinline__ TilePre tile_pre(const SellDev& A, const int32_t* __r
                    : "=r"(t.e.x), "=r"(t.e.y), "=r"(t.e.z), "=r"(t.e.w)
                    : "l"(t.gp));
   }
+  if constexpr (V == 10) {
+    t.ng = (A.vtw[blk] + 7) >> 3;
+    t.gp = reinterpret_cast<const uint32_t*>(A.vi3_off + A.vi3_base[blk] + threadIdx.x);
+    if (t.ng > 0) {
+      asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(t.e.x), "=r"(t.e.y), "=r"(t.e.z), "=r"(t.e.w)
+                   : "l"(t.gp));
+      asm volatile("ld.global.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
+                   : "=r"(t.e2.x), "=r"(t.e2.y)
+                   : "l"(A.vi3_idx + A.vi3_base[blk] + threadIdx.x));
+    }
+  }
   if constexpr (V == 5) {
     if (mf.c.valid && A.mf_code) {
       unsigned short c;
@@ -605,7 +625,7 @@ __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const 
   if constexpr (V == 9) return tile_row_dia(A, blk, x, mf.c);
   if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict, pre);
   if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict, pre);
-  if constexpr (V == 10) return tile_row_vi3(A, blk, x, mf.dict);
+  if constexpr (V == 10) return tile_row_vi3(A, blk, x, mf.dict, pre);
   if constexpr (V == 4) {
     double* sd = reinterpret_cast<double*>(smem);
     for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];

@@ -316,8 +316,8 @@ def main():
                                               if tr and spmv_ms > 0 else None),
                 "exchange": exchange_block(kt, tm, world),
                 "limiter": "latency of the dependent load chains (packed entry -> x gather -> FMA), not HBM, L2 or "
-                           "the L1 pipes (ncu: l1tex 59% of peak, issue 51%, dram 48%, xbar->L1 25%; "
-                           "profiles/r01m_ncu_summary.md; DESIGN.md 'SM-affine persistent SpMV')"}
+                           "the L1 pipes (ncu, variant 10: l1tex 63% of peak, issue 57%, dram 40%; "
+                           "profiles/r01r_ncu_summary.md; DESIGN.md 'SM-affine persistent SpMV')"}
 
     # Whole PCG hot loop against the HBM roofline: algorithmic bytes of the three CG kernels (SpMV in
     # its own format + update + direction) of one solve, over the timed step (everything included).

@@ -138,3 +138,10 @@ def test_c5_sampled_slab():
     r = b - Ks @ u
     assert np.linalg.norm(r) <= 1.05e-10 * np.linalg.norm(b)
     o.close()
+
+
+def test_c3_runs_the_default_spmv(c3):
+    """bench.py's C3 launch configuration runs SpMV variant 10 (3-byte value-indexed entries), not a
+    silent fallback to variant 6: the library reports 10 as the active variant."""
+    cfg, o, prob = c3
+    assert o.set_spmv_variant(10) == 10

@@ -910,13 +910,6 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restric
       xv[j] = reinterpret_cast<const double2*>(x)[i2];
       if (act) rv[j] = reinterpret_cast<const double2*>(r)[i2];
     }
-  if constexpr (MF) {
-    if (act) {
-#pragma unroll
-      for (int j = 0; j < kVecTiles; ++j)
-        if (real[j]) dv[j] = mf_dinv2(cc[j], mf.c);
-    }
-  }
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
     if (real[j]) {
@@ -925,6 +918,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_dir(const int32_t* __restric
       xv[j].y = fma(a, pv[j].y, xv[j].y);
       reinterpret_cast<double2*>(x)[i2] = xv[j];
       if (act) {
+        if constexpr (MF) dv[j] = mf_dinv2(cc[j], mf.c);  // decoded at use: fewer live registers
         pv[j].x = fma(beta, pv[j].x, dv[j].x * rv[j].x);
         pv[j].y = fma(beta, pv[j].y, dv[j].y * rv[j].y);
         reinterpret_cast<double2*>(p)[i2] = pv[j];

@@ -826,11 +826,6 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
       qv[j] = reinterpret_cast<const double2*>(q)[i2];
       rv[j] = reinterpret_cast<const double2*>(r)[i2];
     }
-  if constexpr (MF) {
-#pragma unroll
-    for (int j = 0; j < kVecTiles; ++j)
-      if (real[j]) dv[j] = mf_dinv2(cc[j], mf.c);
-  }
   double v[2] = {0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < kVecTiles; ++j)
@@ -839,6 +834,7 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
       rv[j].x = fma(-a, qv[j].x, rv[j].x);
       rv[j].y = fma(-a, qv[j].y, rv[j].y);
       reinterpret_cast<double2*>(r)[i2] = rv[j];
+      if constexpr (MF) dv[j] = mf_dinv2(cc[j], mf.c);  // decoded at use: fewer live registers
       const double z0 = dv[j].x * rv[j].x, z1 = dv[j].y * rv[j].y;
       v[0] += rv[j].x * z0 + rv[j].y * z1;
       v[1] += rv[j].x * rv[j].x + rv[j].y * rv[j].y;

@@ -24,8 +24,8 @@ def test_reference_arm_json_line():
 
 
 def test_committed_gpu_bench_line_has_contract_keys():
-    """The latest committed GPU bench line (profiles/r01s_bench.json) carries every contract key."""
-    line = json.load(open(os.path.join(ROOT, "profiles", "r01s_bench.json")))
+    """The latest committed GPU bench line (profiles/r01t_bench.json) carries every contract key."""
+    line = json.load(open(os.path.join(ROOT, "profiles", "r01t_bench.json")))
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in line, k

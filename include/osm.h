@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define OSM_ABI_VERSION 1
+#define OSM_ABI_VERSION 2
 
 typedef enum osm_status {
   OSM_OK = 0,
@@ -71,15 +71,30 @@ typedef struct osm_mesh_desc {
   int order;
 } osm_mesh_desc;
 
+/* In-process transport (PAPER.md:157-158 one subdomain block per processor): the
+ * ranks are host threads of ONE process, each driving its own context (on the same or on different
+ * devices).  The trace exchange, the residual allgather and the Phi reduce become device-to-device
+ * copies ordered by CUDA events, with host barriers between the phases; no kernel waits on another
+ * rank's kernel.  It runs every nranks > 1 code path of the library without NCCL (tests, and
+ * single-process multi-GPU use).  Create one hub for nranks ranks, pass it in osm_dist_desc.hub of
+ * every rank's osm_create (made from its own thread), and make every collective call from the rank's
+ * own thread.  A rank whose collective call fails releases the others (they return OSM_ERR_STATE);
+ * a barrier that waits 600 s fails the same way.  Destroy the hub after every context attached to it. */
+typedef struct osm_hub osm_hub;
+osm_status osm_hub_create(int nranks, osm_hub** out);
+void osm_hub_destroy(osm_hub* hub);
+
 /* Distribution: this process is `rank` of `nranks` (one process per GPU),
  * driving CUDA device `device`.  nccl_uid: 128-byte ncclUniqueId made by
  * osm_nccl_unique_id() on rank 0 and broadcast by the caller (e.g. with
- * torch.distributed); NULL when nranks == 1.  stream: a cudaStream_t to run
- * on, or NULL for a library-owned stream. */
+ * torch.distributed); NULL when nranks == 1 or when hub is given.  hub: an
+ * osm_hub (in-process ranks) instead of NCCL; NULL otherwise.  stream: a
+ * cudaStream_t to run on, or NULL for a library-owned stream.  (ABI 2 added hub.) */
 typedef struct osm_dist_desc {
   int rank, nranks, device;
   const void* nccl_uid;
   void* stream;
+  osm_hub* hub;
 } osm_dist_desc;
 
 /* Solve options.  tol_outer: stop when h(n) = ||f - K u~||_2/||f||_2 <= tol_outer

@@ -40,13 +40,14 @@ class Problem:
 
 
 def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=None, monolithic=True,
-                  load_free=None) -> Problem:
+                  load_free=None, plane_ops=None) -> Problem:
     """Assemble every K_s^N, b_s, interface maps, M_Gamma and the monolithic K, f.
 
     ``only``: assemble just these subdomains (others are None); ``monolithic=False`` skips K, f
     (used for bounded timing samples of large workloads).  ``load_free``: a global free-DOF load
     vector instead of a density: b_s takes it at the slab's points, halved on the slab's interface
-    planes (the library's osm_upload_load_vector rule), and f = load_free.
+    planes (the library's osm_upload_load_vector rule), and f = load_free.  ``plane_ops``: (M_Gamma,
+    S_Gamma) already built for this box (they depend on the box only).
     """
     sls = slabs(box, nsub)
     full = slabs(box, 1)[0]
@@ -77,8 +78,7 @@ def build_problem(box: Box, nsub: int, drho=None, load_fn=None, quad=None, only=
                 if idx is not None:
                     b[idx] *= 0.5
             sub.b = b
-    MG = fe.interface_mass(box)
-    SG = fe.interface_stiffness(box)
+    MG, SG = plane_ops if plane_ops is not None else (fe.interface_mass(box), fe.interface_stiffness(box))
     if not monolithic:
         return Problem(box, nsub, subs, MG, SG, None, None)
     K = fe.assemble_stiffness(box, full)

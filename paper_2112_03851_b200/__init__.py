@@ -34,7 +34,7 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
                "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector", "osm_solve_batch2",
-               "osm_set_row_order"]
+               "osm_set_row_order", "osm_hub_create", "osm_hub_destroy"]
 
 
 class MeshDesc(C.Structure):
@@ -44,7 +44,7 @@ class MeshDesc(C.Structure):
 
 class DistDesc(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("device", C.c_int), ("nccl_uid", C.c_void_p),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("hub", C.c_void_p)]
 
 
 class SolveOpts(C.Structure):
@@ -118,6 +118,8 @@ _sigs = {
     "osm_set_spmv_variant": (C.c_int, [_P, C.c_int, _pint]),
     "osm_set_row_order": (C.c_int, [_P, C.c_int]),
     "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
+    "osm_hub_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "osm_hub_destroy": (None, [_P]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
 for _name, (_res, _args) in _sigs.items():
@@ -227,14 +229,34 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class Hub:
+    """In-process transport for `nranks` ranks that are threads of this process (osm_hub_create).
+
+    Pass it as ``Osm(..., rank=r, nranks=n, hub=hub)`` from each rank's own thread; close it after
+    every context attached to it is closed."""
+
+    def __init__(self, nranks):
+        h = _P()
+        _check(_lib.osm_hub_create(nranks, C.byref(h)))
+        self._h = h
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.osm_hub_destroy(self._h)
+            self._h = None
+
+
 class Osm:
-    """One optimized-Schwarz context (one per process / GPU).  Mirrors include/osm.h."""
+    """One optimized-Schwarz context (one per process / GPU, or one per thread with a Hub).  Mirrors
+    include/osm.h."""
 
     def __init__(self, nx, ny, nz, lx, ly, lz, order, rank=0, nranks=1, device=0, nccl_uid: bytes | None = None,
-                 stream: int | None = None):
+                 stream: int | None = None, hub: Hub | None = None):
         self.mesh = MeshDesc(nx, ny, nz, lx, ly, lz, order)
         self._uid = C.create_string_buffer(nccl_uid, 128) if nccl_uid else None
-        dist = DistDesc(rank, nranks, device, C.cast(self._uid, C.c_void_p) if self._uid else None, stream)
+        dist = DistDesc(rank, nranks, device, C.cast(self._uid, C.c_void_p) if self._uid else None, stream,
+                        hub._h if hub is not None else None)
         h = _P()
         _check(_lib.osm_create(C.byref(self.mesh), C.byref(dist), C.byref(h)))
         self._h = h
@@ -471,12 +493,12 @@ class Osm:
 
 
 def setup(cfg: dict, drho, alpha=None, rank=0, nranks=1, device=0, nccl_uid=None, row_order=None,
-          spmv=None) -> Osm:
+          spmv=None, hub=None) -> Osm:
     """Create, decompose, assemble, set alpha (both sides) and upload the density of a config dict.
     row_order / spmv optionally select the internal row order and SpMV variant (row_order=4, spmv=5:
     the matrix-free Kuhn-stencil path)."""
     o = Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], rank, nranks, device,
-            nccl_uid)
+            nccl_uid, hub=hub)
     if row_order is not None:
         o.set_row_order(row_order)
     o.decompose(cfg["nsub"])

@@ -8,6 +8,7 @@
 
 #include "common.h"
 #include "lattice.h"
+#include "transport.h"
 
 namespace osm {
 
@@ -257,7 +258,8 @@ struct Ctx {
   int rank = 0, nranks = 1, device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  ncclComm_t comm = nullptr;
+  Transport* tp = nullptr;  // inter-rank transport (NCCL or the in-process hub); null for one rank
+  osm_hub* hub = nullptr;
   int nsub = 0;
   std::vector<int64_t> cstart;  // slab cell starts
   int s_begin = 0, s_end = 0;   // local subdomains [s_begin, s_end)
@@ -311,6 +313,7 @@ struct Ctx {
   // vectors (device, nrows_total)
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *b = nullptr, *ut = nullptr;
   double* drho = nullptr;  // cell density (device, nx ny nz)
+  double* d_gz = nullptr;  // gravity-anomaly output (device, nx ny; rank 0)
   // interface arrays (device, nsides * nG)
   double *lam_all = nullptr, *unbr_all = nullptr, *wif_all = nullptr;
   SideDev* d_sides = nullptr;

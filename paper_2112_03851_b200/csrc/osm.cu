@@ -952,65 +952,22 @@ static void apply_robin(Ctx& c) {
 // ------------------------------------------------------------------ exchange
 // part 1: [g | u] both directions for every remote side; part 2: the right slab's
 // interface-row residual w to the owner (left slab).
-static void exchange_calls(Ctx& c, int part);
 static void exchange(Ctx& c, int part) {
-  if (!c.comm) return;
+  if (!c.tp) return;
   bool any = false;
   for (const Side& sd : c.sides) any = any || sd.remote;
-  if (!any) return;
-  timer_begin(c, T_OUTER_MISC);  // NCCL trace exchange, timed on the library stream
-  exchange_calls(c, part);
+  if (!any && !c.hub) return;  // (hub ranks always meet at the exchange barriers)
+  timer_begin(c, T_OUTER_MISC);  // trace exchange, timed on the library stream
+  c.tp->exchange(c, part);
   timer_end(c, T_OUTER_MISC);
   for (const Side& sd : c.sides)  // bytes this rank sends (traffic[7])
     if (sd.remote && (part == 1 || sd.which == 1)) c.exch_bytes += (part == 1 ? 16.0 : 8.0) * c.nG;
 }
 
-static void exchange_calls(Ctx& c, int part) {
-  const int64_t nG = c.nG;
-  if (c.force_remote) {
-    // every side talks to its own rank: NCCL matches the j-th send with the j-th receive, so each
-    // receive is posted into the partner of the j-th sender
-    OSM_NCCL(ncclGroupStart());
-    for (const Side& sd : c.sides) {
-      if (part == 1) OSM_NCCL(ncclSend(sd.out, 2 * nG, ncclDouble, c.rank, c.comm, c.stream));
-      else if (sd.which == 1) OSM_NCCL(ncclSend(sd.out + 2 * nG, nG, ncclDouble, c.rank, c.comm, c.stream));
-    }
-    for (const Side& sd : c.sides) {
-      const Side& dst = c.sides[sd.partner];
-      if (part == 1) OSM_NCCL(ncclRecv(dst.inbuf, 2 * nG, ncclDouble, c.rank, c.comm, c.stream));
-      else if (sd.which == 1) OSM_NCCL(ncclRecv(dst.inbuf + 2 * nG, nG, ncclDouble, c.rank, c.comm, c.stream));
-    }
-    OSM_NCCL(ncclGroupEnd());
-    return;
-  }
-  OSM_NCCL(ncclGroupStart());
-  for (const Side& sd : c.sides) {
-    if (!sd.remote) continue;
-    if (part == 1) {
-      OSM_NCCL(ncclSend(sd.out, 2 * nG, ncclDouble, sd.peer, c.comm, c.stream));
-      OSM_NCCL(ncclRecv(sd.inbuf, 2 * nG, ncclDouble, sd.peer, c.comm, c.stream));
-    } else if (sd.which == 1) {
-      OSM_NCCL(ncclSend(sd.out + 2 * nG, nG, ncclDouble, sd.peer, c.comm, c.stream));
-    } else {
-      OSM_NCCL(ncclRecv(sd.inbuf + 2 * nG, nG, ncclDouble, sd.peer, c.comm, c.stream));
-    }
-  }
-  OSM_NCCL(ncclGroupEnd());
-}
-
 // Per-subdomain values (local, in subdomain order) -> all nsub values on every rank.
 static std::vector<double> allgather_sub(Ctx& c, const std::vector<double>& local, int width) {
-  const int nloc = c.s_end - c.s_begin;
-  if (!c.comm) return local;
-  double* d = dalloc<double>((int64_t)c.nsub * width);
-  OSM_CUDA(cudaMemcpyAsync(d + (int64_t)c.s_begin * width, local.data(), sizeof(double) * nloc * width,
-                           cudaMemcpyHostToDevice, c.stream));
-  OSM_NCCL(ncclAllGather(d + (int64_t)c.s_begin * width, d, (size_t)nloc * width, ncclDouble, c.comm, c.stream));
-  std::vector<double> all((size_t)c.nsub * width);
-  OSM_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, c.stream));
-  OSM_CUDA(cudaStreamSynchronize(c.stream));
-  dfree(d);
-  return all;
+  if (!c.tp) return local;
+  return c.tp->allgather_host(c, local, width);
 }
 
 // Glued residual pipeline: sum over global free rows of (f - K u~)^2,
@@ -1284,18 +1241,22 @@ struct osm_ctx {
   }                                                 \
   catch (const Error& e) {                          \
     g_last_error = e.what();                        \
+    hub_poison_current();                           \
     return e.status;                                \
   }                                                 \
   catch (const std::exception& e) {                 \
     g_last_error = e.what();                        \
+    hub_poison_current();                           \
     return OSM_ERR_CUDA;                            \
   }                                                 \
   catch (...) {                                     \
     g_last_error = "unknown error";                 \
+    hub_poison_current();                           \
     return OSM_ERR_CUDA;                            \
   }
 
 static Ctx& ctx_of(osm_ctx* c) {
+  hub_set_current(nullptr);  // set again by the collective calls (solve, solution, gravity)
   if (!c) fail(OSM_ERR_INVALID_ARG, "NULL context");
   OSM_CUDA(cudaSetDevice(c->c.device));
   return c->c;
@@ -1328,10 +1289,11 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
   if (m.order != 1 && m.order != 2) fail(OSM_ERR_INVALID_ARG, "order must be 1 or 2");
   if (m.order * m.nx + 1 < 3 || m.order * m.ny + 1 < 3 || m.order * m.nz + 1 < 3)
     fail(OSM_ERR_GRID_TOO_SMALL, "fewer than 3 lattice points on an axis: no interior");
-  osm_dist_desc d{0, 1, 0, nullptr, nullptr};
+  osm_dist_desc d{0, 1, 0, nullptr, nullptr, nullptr};
   if (dist) d = *dist;
   if (d.nranks < 1 || d.rank < 0 || d.rank >= d.nranks) fail(OSM_ERR_INVALID_ARG, "bad rank/nranks");
-  if (d.nranks > 1 && !d.nccl_uid) fail(OSM_ERR_INVALID_ARG, "nccl_uid required when nranks > 1");
+  if (d.nranks > 1 && !d.nccl_uid && !d.hub) fail(OSM_ERR_INVALID_ARG, "nccl_uid or hub required when nranks > 1");
+  if (d.nccl_uid && d.hub) fail(OSM_ERR_INVALID_ARG, "nccl_uid and hub are exclusive");
   auto* h = new osm_ctx();
   Ctx& c = h->c;
   try {
@@ -1370,14 +1332,13 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "exchange"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
     if (const char* e = std::getenv("OSM_FORCE_REMOTE")) c.force_remote = std::atoi(e) != 0 && c.nranks == 1;
-    if (c.nranks > 1) {
-      ncclUniqueId id;
-      std::memcpy(&id, d.nccl_uid, sizeof(id));
-      OSM_NCCL(ncclCommInitRank(&c.comm, c.nranks, id, c.rank));
+    if (d.hub) {
+      c.hub = d.hub;
+      c.tp = make_hub_transport(c, d.hub);
+    } else if (c.nranks > 1) {
+      c.tp = make_nccl_transport(c, d.nccl_uid, false);
     } else if (c.force_remote) {  // debug: a 1-rank communicator so the NCCL path runs on one GPU
-      ncclUniqueId id;
-      OSM_NCCL(ncclGetUniqueId(&id));
-      OSM_NCCL(ncclCommInitRank(&c.comm, 1, id, 0));
+      c.tp = make_nccl_transport(c, nullptr, true);
     }
   } catch (...) {
     osm_destroy(h);
@@ -1398,6 +1359,7 @@ void osm_destroy(osm_ctx* h) {
   } catch (...) {
   }
   dfree(c.drho);
+  dfree(c.d_gz);
   dfree(c.d_nactive);
   dfree(c.d_flags);
   if (c.h_nactive) cudaFreeHost(c.h_nactive);
@@ -1412,7 +1374,8 @@ void osm_destroy(osm_ctx* h) {
     if (gs) cudaStreamDestroy(gs);
   for (auto& t : c.timers)
     for (auto& e : t.ev) cudaEventDestroy(e);
-  if (c.comm) ncclCommDestroy(c.comm);
+  delete c.tp;
+  c.tp = nullptr;
   if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
   delete h;
 }
@@ -1532,6 +1495,7 @@ osm_status osm_upload_density_device(osm_ctx* h, const double* drho, double G) {
 osm_status osm_solve(osm_ctx* h, const osm_solve_opts* o, osm_report* rep) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
+  hub_set_current(c.hub);  // [collective]: a failure here releases the other hub ranks
   if (!o) fail(OSM_ERR_INVALID_ARG, "NULL options");
   return solve(c, *o, rep);
   OSM_API_END
@@ -1566,12 +1530,13 @@ static void gather_phi(Ctx& c, int64_t N) {
   if (!c.phi) c.phi = dalloc<double>(N);
   OSM_CUDA(cudaMemsetAsync(c.phi, 0, sizeof(double) * N, c.stream));
   for (const Sub& S : c.subs) launch_scatter_phi(c, S, c.nranks > 1 ? 1 : 0);
-  if (c.nranks > 1) OSM_NCCL(ncclReduce(c.phi, c.phi, N, ncclDouble, ncclSum, 0, c.comm, c.stream));
+  if (c.nranks > 1) c.tp->reduce_phi(c, c.phi, N);
 }
 
 osm_status osm_get_solution(osm_ctx* h, double* phi, int64_t* n) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
+  hub_set_current(c.hub);  // [collective]: a failure here releases the other hub ranks
   if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
   const int o = c.mesh.order;
   const int64_t N = (o * c.mesh.nx + 1) * (o * c.mesh.ny + 1) * (o * c.mesh.nz + 1);
@@ -1592,6 +1557,7 @@ osm_status osm_get_solution(osm_ctx* h, double* phi, int64_t* n) {
 osm_status osm_gravity_z(osm_ctx* h, double z0, double* gz, int64_t* n) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
+  hub_set_current(c.hub);  // [collective]: a failure here releases the other hub ranks
   if (!n) fail(OSM_ERR_INVALID_ARG, "NULL size");
   const int64_t M = c.mesh.nx * c.mesh.ny;
   if (!gz && c.rank == 0) {
@@ -1604,11 +1570,9 @@ osm_status osm_gravity_z(osm_ctx* h, double z0, double* gz, int64_t* n) {
   const int64_t N = (o * c.mesh.nx + 1) * (o * c.mesh.ny + 1) * (o * c.mesh.nz + 1);
   gather_phi(c, N);
   if (c.rank == 0) {
-    double* d = dalloc<double>(M);
-    gravity_z(c, z0, d);
-    OSM_CUDA(cudaMemcpyAsync(gz, d, sizeof(double) * M, cudaMemcpyDeviceToHost, c.stream));
-    OSM_CUDA(cudaStreamSynchronize(c.stream));
-    dfree(d);
+    if (!c.d_gz) c.d_gz = dalloc<double>(M);  // persistent (freed with the context)
+    gravity_z(c, z0, c.d_gz);
+    OSM_CUDA(cudaMemcpyAsync(gz, c.d_gz, sizeof(double) * M, cudaMemcpyDeviceToHost, c.stream));
   }
   OSM_CUDA(cudaStreamSynchronize(c.stream));
   *n = M;

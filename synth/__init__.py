@@ -109,9 +109,20 @@ CONFIGS = {
     "C3": dict(nx=64, ny=64, nz=64, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
                order=2, nsub=8, field="chicxulub", alpha=(0.1, 5.0e-4),
                robin=(2.307568271474025e-4, 1.7725347224902227e-4, 1181.9035996235004, 834.7590599290618)),
+    # C5 transmission: OO2 (p1, p2, q1, q2) from a 3-point probe on the GPU path (tools/c5_probe.py,
+    # profiles/r01_c5_probe*.log): 15 outer iterations to 1e-8 at S = 8, 27 at S = 64.
     "C5": dict(nx=192, ny=192, nz=192, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2],
-               order=2, nsub=8, field="chicxulub", alpha=None),
+               order=2, nsub=8, field="chicxulub", alpha=None, robin=(2.0e-4, 5.0e-5, 700.0, 300.0)),
 }
+
+
+# A small case with a non-monotone Schwarz history (growth of h at every even n), for the divergence
+# rule "h grew for diverge_window consecutive iterations": the paper box at
+# 16 x 8 x 2 P1 cells, S = 8, OO0 nearly Neumann on the right sides (p2 = 1e-6).
+CONFIGS["DIV"] = dict(nx=16, ny=8, nz=2, lx=PAPER_BOX_M[0], ly=PAPER_BOX_M[1], lz=PAPER_BOX_M[2], order=1,
+                      nsub=8, field="chicxulub", alpha=(1e-2, 1e-6))
+
+C5_ROBIN = (2.0e-4, 5.0e-5, 700.0, 300.0)
 
 
 def robin(cfg: dict):

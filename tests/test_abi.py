@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s), s
     assert sorted(P.ABI_SYMBOLS) == declared_symbols()
-    assert P.abi_version() == 1
+    assert P.abi_version() == 2
 
 
 def test_no_oracle_in_product_path():

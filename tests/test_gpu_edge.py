@@ -146,3 +146,34 @@ def test_gravity_anomaly_matches_oracle(order):
         go = gravity.gravity_z(prob.box, phi_or, z0)
         assert np.abs(g - go).max() <= 1e-9 * np.abs(go).max(), z0
     o.close()
+
+
+def test_diverged_status_matches_oracle():
+    """SPEC.md:443 / SURVEY Q22 (row a7): h(n) grew for diverge_window consecutive iterations ->
+    OSM_ERR_DIVERGED at the same n as the oracle.  synth.CONFIGS["DIV"] has growth at every even n
+    (tests/test_oracle_pins.py pins the oracle side): window 1 fires at n = 2; window 2 never fires,
+    so max_outer = 12 ends NOT_CONVERGED with the same 12-entry history."""
+    import paper_2112_03851_b200 as P
+    from oracle import mesh, schwarz
+
+    from parity_util import history_ok
+
+    cfg = synth.CONFIGS["DIV"]
+    drho = synth.density(cfg)
+    box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+    prob = schwarz.build_problem(box, cfg["nsub"], drho=drho)
+    A = schwarz.robin_operators(prob, *synth.alphas(cfg))
+    o = P.setup(cfg, drho)
+    st, rep = o.solve(tol_outer=1e-8, max_outer=40, diverge_window=1)
+    orep = schwarz.schwarz(prob, A, tol_outer=1e-8, max_outer=40, diverge_window=1)
+    assert orep.diverged and orep.outer_iters == 2
+    assert st == P.OSM_ERR_DIVERGED and rep.outer_iters == 2 and not rep.converged
+    ok, d = history_ok(o.history(), orep.h)
+    assert ok and len(o.history()) == 2, d.max()
+    st, rep = o.solve(tol_outer=1e-8, max_outer=12, diverge_window=2)
+    orep = schwarz.schwarz(prob, A, tol_outer=1e-8, max_outer=12, diverge_window=2)
+    assert not orep.diverged and orep.outer_iters == 12
+    assert st == P.OSM_NOT_CONVERGED and rep.outer_iters == 12
+    ok, d = history_ok(o.history(), orep.h)
+    assert ok, d.max()
+    o.close()

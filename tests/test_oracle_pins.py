@@ -488,3 +488,145 @@ def test_load_free_split_is_monolithic():
     us = schwarz.monolithic(prob)
     assert np.linalg.norm(rep.ut - us) / np.linalg.norm(us) < 1e-9
     assert sum(sub.b.sum() for sub in prob.subs) == pytest.approx(b.sum(), rel=1e-12)
+
+
+# ---------------------------------------------------------------- conventions with no other pin
+def test_interface_map_hand_decoded():
+    """the map of Gamma lists the plane's interior points j fastest, then k, as
+    local indices of each side.  Hand decode for P1, 4 x 3 x 3 cells, S = 2 (lattice 5 x 4 x 4):
+    Gamma is the plane I = 2; its interior points (J, K) in map order are (1,1), (2,1), (1,2), (2,2).
+    Left slab: free I in [1, 2], local = (I - 1) + 2 ((J - 1) + 2 (K - 1)) -> 1, 3, 5, 7.
+    Right slab: free I in [2, 3], local = (I - 2) + 2 ((J - 1) + 2 (K - 1)) -> 0, 2, 4, 6.
+    (k fastest would give 1, 5, 3, 7.)"""
+    box = mesh.Box(4, 3, 3, 1.0, 1.0, 1.0, 1)
+    sl = mesh.slabs(box, 2)
+    l, r = mesh.interface_map(box, sl[0], sl[1])
+    assert list(l) == [1, 3, 5, 7] and list(r) == [0, 2, 4, 6]
+    # P2, 2 x 2 x 2 cells, S = 2: lattice 5^3, Gamma at I = 2; left free I in [1, 2], right in [2, 3];
+    # interior plane points J, K in 1..3 -> 9 points, j fastest
+    box = mesh.Box(2, 2, 2, 1.0, 1.0, 1.0, 2)
+    sl = mesh.slabs(box, 2)
+    l, r = mesh.interface_map(box, sl[0], sl[1])
+    JK = [(j, k) for k in (1, 2, 3) for j in (1, 2, 3)]
+    assert list(l) == [1 + 2 * ((j - 1) + 3 * (k - 1)) for j, k in JK]
+    assert list(r) == [0 + 2 * ((j - 1) + 3 * (k - 1)) for j, k in JK]
+
+
+def test_glue_hand_value():
+    """interface DOFs are duplicated and glued by averaging.  u_left = 1, u_right = 3 gives
+    u~ = 2 on the interface plane and keeps 1 / 3 elsewhere (P1, 4 x 3 x 3 cells, S = 2: global free
+    lattice 3 x 2 x 2, plane I = 2 is global free column i = 1)."""
+    box = mesh.Box(4, 3, 3, 1.0, 1.0, 1.0, 1)
+    prob = schwarz.build_problem(box, 2, drho=np.zeros(36))
+    ut = schwarz.glue(prob, [np.full(prob.subs[0].b.size, 1.0), np.full(prob.subs[1].b.size, 3.0)])
+    g = ut.reshape(2, 2, 3)  # (K, J, I) over the free points, I fastest
+    assert np.all(g[:, :, 0] == 1.0) and np.all(g[:, :, 1] == 2.0) and np.all(g[:, :, 2] == 3.0)
+
+
+def _plane_faces(box, ci):
+    """Faces of the Kuhn tets of cells (ci, cj, ck) lying on the plane x = (ci + 1) h_x, derived from
+    kuhn_tet_vertices alone: the tet's vertices with local x = 1.  Returns (cell, perm, face vertex
+    indices) -- independent of fe.interface_mass's own triangle split."""
+    out = []
+    for ck in range(box.nz):
+        for cj in range(box.ny):
+            for perm in mesh.PERMS:
+                V = mesh.kuhn_tet_vertices(perm)
+                on = [a for a in range(4) if V[a, 0] == 1]
+                if len(on) == 3:
+                    out.append(((ci, cj, ck), perm, on))
+    return out
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_plane_operators_from_kuhn_faces(order):
+    """M_Gamma and S_Gamma rebuilt from the x = const faces of the Kuhn tets:
+    v^T M v = int_Gamma v_h^2 and v^T S v = int_Gamma |grad_tau v_h|^2, where v_h is evaluated with the
+    3-D P2/P1 basis of the tet that owns each face (nodes off the face vanish there), v is indexed by
+    the points of the interface map (decoded to (J, K) through the slab's lattice coordinates), and the
+    faces come from kuhn_tet_vertices.  A different diagonal split, a transposed (j, k) order or a
+    wrong plane table fails it.  The faces seen from the right slab's cells (x = 0 faces) must be the
+    same triangles (conformity)."""
+    rng = np.random.default_rng(11)
+    box = mesh.Box(4, 4, 3, 1.0, 0.7, 0.45, order) if order == 1 else mesh.Box(4, 3, 2, 1.0, 0.7, 0.45, order)
+    sl = mesh.slabs(box, 2)
+    lmap, _ = mesh.interface_map(box, sl[0], sl[1])
+    I, J, K = mesh.slab_lattice_coords(sl[0])
+    Jm, Km = J[lmap], K[lmap]
+    _, Ny, Nz = box.lattice
+    vals = np.zeros((Ny, Nz))
+    v = rng.standard_normal(lmap.size)
+    vals[Jm, Km] = v
+    h = box.h
+    bary, w = quadrature.tri_rule(6)
+    ci = sl[0].c1 - 1
+    faces = _plane_faces(box, ci)
+    assert len(faces) == 2 * box.ny * box.nz
+    # the right slab's cells see the same triangles on their x = 0 faces
+    tris_l, tris_r = set(), set()
+    for (c, perm, on) in faces:
+        V = mesh.kuhn_tet_vertices(perm)
+        tris_l.add(frozenset((c[1] + V[a, 1], c[2] + V[a, 2]) for a in on))
+    for ck in range(box.nz):
+        for cj in range(box.ny):
+            for perm in mesh.PERMS:
+                V = mesh.kuhn_tet_vertices(perm)
+                on = [a for a in range(4) if V[a, 0] == 0]
+                if len(on) == 3:
+                    tris_r.add(frozenset((cj + V[a, 1], ck + V[a, 2]) for a in on))
+    assert tris_l == tris_r
+    mass, stiff = 0.0, 0.0
+    for (c, perm, on) in faces:
+        V = mesh.kuhn_tet_vertices(perm)
+        X = V.astype(float) * h
+        g, _ = fe.tet_geometry(X)
+        offs = mesh.local_lattice_offsets(perm, order)
+        nodal = np.array([vals[order * c[1] + offs[a, 1], order * c[2] + offs[a, 2]]
+                          if order * c[0] + offs[a, 0] == order * (ci + 1) else 0.0 for a in range(len(offs))])
+        Y = X[on][:, 1:]
+        area = 0.5 * abs((Y[1, 0] - Y[0, 0]) * (Y[2, 1] - Y[0, 1]) - (Y[2, 0] - Y[0, 0]) * (Y[1, 1] - Y[0, 1]))
+        for lam3, wq in zip(bary, w):
+            lam4 = np.zeros(4)
+            lam4[on] = lam3
+            phi = fe.basis_values(order, lam4[None, :])[0]
+            grads = g if order == 1 else fe.p2_basis_gradients(g, lam4)
+            mass += area * wq * (phi @ nodal) ** 2
+            gt = (nodal @ grads)[1:]  # tangential (y, z) part of the 3-D gradient on x = const
+            stiff += area * wq * (gt @ gt)
+    M, S = fe.interface_mass(box), fe.interface_stiffness(box)
+    assert abs(v @ (M @ v) - mass) <= 1e-13 * mass
+    assert abs(v @ (S @ v) - stiff) <= 1e-12 * stiff
+
+
+# Deterministic non-monotone history for the divergence rule (SPEC.md:443, SURVEY Q22): the paper box
+# 16 x 8 x 2 cells, P1, S = 8, Chicxulub field, OO0 with p1 = 1e-2, p2 = 1e-6 (nearly Neumann on the
+# right side).  Its history alternates: h(1) = 0.283 < h(2) = 0.541 > h(3) = 0.262 < h(4) = 0.476 ...
+# (growth at every even n), so the rule "h grew for w consecutive iterations" fires at n = 2 for w = 1
+# and never for w = 2.
+DIV_CASE = synth.CONFIGS["DIV"]
+
+
+def _div_prob():
+    c = DIV_CASE
+    box = mesh.Box(c["nx"], c["ny"], c["nz"], c["lx"], c["ly"], c["lz"], c["order"])
+    prob = schwarz.build_problem(box, c["nsub"], drho=synth.density(c))
+    al, ar = synth.alphas(c)
+    return prob, schwarz.robin_operators(prob, al, ar)
+
+
+def test_divergence_rule_window_one_fires_at_n2():
+    prob, A = _div_prob()
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-8, max_outer=40, diverge_window=1)
+    assert rep.diverged and not rep.converged and rep.outer_iters == 2
+    assert rep.h[1] > rep.h[0]
+
+
+def test_divergence_rule_needs_consecutive_growth():
+    prob, A = _div_prob()
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-8, max_outer=12, diverge_window=2)
+    assert not rep.diverged and not rep.converged and rep.outer_iters == 12
+    h = np.array(rep.h)
+    grows = h[1:] > h[:-1]
+    assert list(np.nonzero(grows)[0] + 2) == [2, 4, 6, 8, 10, 12]  # alternating: never twice in a row
+    off = schwarz.schwarz(prob, A, tol_outer=1e-8, max_outer=12, diverge_window=0)
+    assert not off.diverged and off.h == rep.h

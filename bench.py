@@ -162,9 +162,13 @@ def main():
     ap.add_argument("--alpha", default=None, help="alpha or alpha_1:alpha_2 (two-sided)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=200)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (192^3, 56 M DOF) block")
+    ap.add_argument("--no-cpu-full", action="store_true", help="skip the oracle's measured time-to-tolerance")
     ap.add_argument("--timing-steps", type=int, default=1)
     args = ap.parse_args()
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -341,6 +345,12 @@ def main():
     if world == 1:
         batched = run_batched_alpha(P, stream, torch)
 
+    # C5 (BASELINE configs[4], the north_star's >= 50 M-DOF target): S = 8 fixed at every N (strong
+    # scaling); one instrumented warm-up solve (per-kernel events) + one timed solve
+    c5 = None
+    if not args.no_c5:
+        c5 = run_c5(P, args, stream, torch, rank, world, dist, local_rank)
+
     # e2e through the C ABI with host buffers: pinned drho H2D + solve + Phi D2H, every step
     h_drho = torch.from_numpy(drho).pin_memory()
     phi = torch.empty(int(np.prod(osm.lattice)), dtype=torch.float64).pin_memory() if rank == 0 else None
@@ -376,14 +386,16 @@ def main():
         cpu = {"value": n_s / t_iter, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{args.ref_iters} oracle Jacobi-PCG iterations on subdomain 1 of {args.config} "
                          f"(scipy CSR, 1 thread)", "seconds_per_cg_iteration": t_iter, "sample_rows": n_s,
-               "time_to_tol_s_extrapolated": t_iter / n_s * (cg_work / args.steps)}
+               "time_to_tol_s_extrapolated": t_iter / n_s * (cg_work / args.steps), "host": host_info()}
+        if not args.no_cpu_full:
+            cpu["measured"] = oracle_time_to_tol(args.config)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(args, cfg),
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
             "roofline": roofline, "roofline_cg_step": cg_roofline, "roofline_fp64_sell": roofline_fp64,
-            "matrix_free": matrix_free, "batched_alpha": batched,
+            "matrix_free": matrix_free, "batched_alpha": batched, "c5": c5,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)
@@ -488,15 +500,114 @@ def run_matrix_free(P, args, cfg, d_drho, stream, peak, torch):
             "cg_kernels_us": {k: 1e3 * v[1] / max(1, v[0]) for k, v in kt.items()}}
 
 
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def oracle_time_to_tol(config):
+    """The oracle, as it stands, solved to h <= 1e-8 on the host cores in the paper's shape (one
+    process per subdomain; oracle.slabwise = oracle.schwarz distributed):
+    C1 single-thread, and the bench workload with min(S, nproc) single-threaded processes.  Measured
+    wall seconds of the iteration (||f|| and every outer iteration; the workers' assembly excluded)."""
+    from oracle import mesh, slabwise
+
+    out = {}
+    for name in ("C1", config):
+        cfg = dict(synth.CONFIGS[name])
+        box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+        S = cfg["nsub"]
+        nproc = 1 if name == "C1" else min(S, os.cpu_count() or 1)
+        tstart = time.perf_counter()
+        rep = slabwise.schwarz_slabwise(box, S, synth.density(cfg), synth.robin(cfg), tol_outer=1e-8, max_outer=1000,
+                                        nproc=nproc)
+        out[name] = {"time_to_tol_s": rep.seconds, "wall_incl_assembly_s": time.perf_counter() - tstart,
+                     "outer_iters": rep.outer_iters, "inner_total": int(sum(map(sum, rep.inner))),
+                     "converged": rep.converged, "processes": nproc, "threads_per_process": 1}
+    return out
+
+
+def run_c5(P, args, stream, torch, rank, world, dist, local_rank):
+    """C5: 192^3 P2 cells on the paper box (56,181,887 DOF), S = 8 x-slabs split over the N ranks, OO2
+    (synth.C5_ROBIN), solved to h <= 1e-8.  Warm-up = one instrumented solve (kernel events on the
+    library stream: per-kernel times and the SpMV roofline in its own bytes); then one timed solve
+    (CUDA events on the library stream, max over ranks)."""
+    cfg = dict(synth.CONFIGS["C5"])
+    uid = None
+    if world > 1:
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    t0 = time.perf_counter()
+    o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], 2, rank=rank, nranks=world,
+              device=local_rank, nccl_uid=uid, stream=stream.cuda_stream)
+    o.decompose(cfg["nsub"])
+    o.set_robin2(*synth.robin(cfg))
+    o.assemble()
+    d = torch.from_numpy(synth.density(cfg)).to(f"cuda:{local_rank}")
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    S = cfg["nsub"]
+    o.set_kernel_timing(True)
+    o.upload_density_device(d.data_ptr())
+    st, rep = o.solve(tol_outer=1e-8, max_outer=200)
+    kt, tm = o.kernel_timing(), o.traffic_model()
+    o.set_kernel_timing(False)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    o.upload_density_device(d.data_ptr())
+    st, rep = o.solve(tol_outer=1e-8, max_outer=200)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    work = local_cg_work(o, S, rank, world)
+    if dist is not None:
+        t = torch.tensor([ms, work], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:])
+        ms, work = float(t[0].item()), float(t[1].item())
+    peak, _ = hbm_peak()
+    n, spmv_ms = kt["cg_spmv"]
+    cg_ms = sum(kt[k][1] for k in ("cg_spmv", "cg_update", "cg_dir"))
+    gbs = tm["spmv_bytes"] / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
+    out = {"workload": "C5: P2 192x192x192 Kuhn box 250x250x15 km, chicxulub density, 8 x-slab subdomains "
+                       f"over {world} GPU(s), OO2 {synth.C5_ROBIN}",
+           "dof": 56181887, "status": int(st), "time_to_tol_s": ms / 1e3, "outer_iters": rep.outer_iters,
+           "inner_total": rep.inner_total, "value": work / (ms / 1e3), "unit": UNIT, "setup_s": setup,
+           "spmv_variant": o.set_spmv_variant(HOT_VARIANT),
+           "roofline": {"bound": "hbm", "kernel": "k_cg_spmv (rank 0, instrumented warm-up solve)",
+                        "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak if gbs else None,
+                        "us_per_launch": 1e3 * spmv_ms / max(1, n)},
+           "cg_kernels_gbs": {k: (tm[b] / (kt[k][1] / 1e3) / 1e9 if kt[k][1] > 0 else None)
+                              for k, b in (("cg_update", "update_bytes"), ("cg_dir", "dir_bytes"))},
+           "kernel_share_of_cg": {k: kt[k][1] / cg_ms for k in ("cg_spmv", "cg_update", "cg_dir")},
+           "timing": "one timed solve after one instrumented warm-up solve; CUDA events, max over ranks"}
+    o.close()
+    del d
+    torch.cuda.empty_cache()
+    return out
+
+
 def local_cg_work(osm, S, rank, world):
     """sum over local subdomains s and outer iterations n of n_s x PCG iterations (DOF x CG-iter)."""
     lo, hi = rank * S // world, (rank + 1) * S // world
     its = osm.inner_iters().astype(np.int64)
     w = 0
     for s in range(lo, hi):
-        if s not in _rows:
-            _rows[s] = osm.local_solution_size(s)
-        w += _rows[s] * int(np.clip(its[:, s], 0, None).sum())
+        key = (id(osm), osm.lattice, s)  # per context: C3, C5 and the matrix-free contexts differ
+        if key not in _rows:
+            _rows[key] = osm.local_solution_size(s)
+        w += _rows[key] * int(np.clip(its[:, s], 0, None).sum())
     return float(w)
 
 

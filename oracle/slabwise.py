@@ -33,6 +33,7 @@ from __future__ import annotations
 import json
 import multiprocessing as mp
 import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -194,6 +195,7 @@ class SlabwiseReport:
     lam: dict | None = None
     u: dict | None = None  # final u_s (if keep_u)
     phi: np.ndarray | None = None  # Phi on the full lattice (if want_phi)
+    seconds: float = 0.0  # wall time of ||f|| and the outer iterations (assembly excluded)
 
 
 def schwarz_slabwise(box: Box, nsub: int, drho, robin, tol_outer=1e-8, max_outer=500, tol_inner=1e-10,
@@ -273,6 +275,7 @@ def schwarz_slabwise(box: Box, nsub: int, drho, robin, tol_outer=1e-8, max_outer
         for i in range(nsub - 1):
             l, r = interface_map(box, sls[i], sls[i + 1])
             right_of[i], left_of[i + 1] = l, r
+        t_loop = time.perf_counter()
         fnorm = float(np.sqrt(resid_sq(None)))
         opts = dict(warm_start=warm_start, tol_inner=tol_inner, max_inner=max_inner)
         grow = 0
@@ -320,6 +323,7 @@ def schwarz_slabwise(box: Box, nsub: int, drho, robin, tol_outer=1e-8, max_outer
                 rep.diverged = True
                 break
         rep.lam = lam
+        rep.seconds = time.perf_counter() - t_loop
         if keep_u or want_phi:
             if planes is None:  # resumed at the end: rebuild the glued planes from the stored u
                 uu = gather("u", None)

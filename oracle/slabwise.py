@@ -94,6 +94,23 @@ def slab_global_residual(prob: schwarz.Problem, u: list, fnorm2: float | None = 
 
 
 # ---------------------------------------------------------------- worker process
+def _assemble_child(conn, box, nsub, s, drho, robin, plane_ops):
+    """K_s = K_s^N + sum P^T A P (schwarz.subdomain_operator) and the plane rows of K_s^N for slab s."""
+    pl, ql, pr, qr = robin
+    prob = schwarz.build_problem(box, nsub, drho=drho, only=[s], monolithic=False, plane_ops=plane_ops)
+    A = schwarz.robin_operators(prob, pl, pr, ql, qr)
+    sub = prob.subs[s]
+    Ks = schwarz.subdomain_operator(prob, s, A)
+    # K_s^N is needed only for the residual; K_s equals it off the interface planes, so keep only
+    # the plane rows of K_s^N (the residual of the other rows is taken from K_s)
+    planes = [idx for idx in (sub.left, sub.right) if idx is not None]
+    rows = np.concatenate(planes) if planes else np.zeros(0, dtype=np.int64)
+    KNp = (rows, sub.KN[rows, :] if rows.size else None)
+    sub.KN = None
+    conn.send((sub, Ks, KNp))
+    conn.close()
+
+
 def _worker(conn, box: Box, nsub: int, owned: list, drho, robin, ckpt, asm_sem):
     """Owns subdomains ``owned``: assembles them, then serves 'solve' / 'resid' / 'u' requests."""
     from threadpoolctl import threadpool_limits
@@ -106,21 +123,18 @@ def _worker(conn, box: Box, nsub: int, owned: list, drho, robin, ckpt, asm_sem):
     Ks, KNplane, u, subs = {}, {}, {}, {}
     for s in owned:  # one slab at a time: only K_s and the plane rows of K_s^N stay resident
         with asm_sem:  # bounds the number of concurrent assemblies (their transient memory)
-            prob = schwarz.build_problem(box, nsub, drho=drho, only=[s], monolithic=False, plane_ops=plane_ops)
-        A = schwarz.robin_operators(prob, pl, pr, ql, qr)
-        sub = prob.subs[s]
-        Ks[s] = schwarz.subdomain_operator(prob, s, A)
-        # K_s^N is needed only for the residual; K_s equals it off the interface planes, so keep only
-        # the plane rows of K_s^N (the residual of the other rows is taken from K_s)
-        planes = [idx for idx in (sub.left, sub.right) if idx is not None]
-        rows = np.concatenate(planes) if planes else np.zeros(0, dtype=np.int64)
-        KNplane[s] = (rows, sub.KN[rows, :] if rows.size else None)
+            # assembled in a short-lived child process, so that the assembly's transient memory is
+            # returned to the OS (a long-lived worker's heap would keep it)
+            a, b = mp.get_context("fork").Pipe()
+            ch = mp.get_context("fork").Process(target=_assemble_child,
+                                                args=(b, box, nsub, s, drho, robin, plane_ops))
+            ch.start()
+            sub, Ks[s], KNplane[s] = a.recv()
+            ch.join()
         u[s] = np.zeros(sub.b.size)
         if ckpt is not None and os.path.exists(os.path.join(ckpt, f"u_{s}.npy")):
             u[s] = np.load(os.path.join(ckpt, f"u_{s}.npy"))
-        sub.KN = None  # free the full Neumann matrix
         subs[s] = sub
-        del prob
     conn.send(("ready", {s: (subs[s].b.size, subs[s].slab.I_range) for s in owned}))
     while True:
         msg, arg = conn.recv()

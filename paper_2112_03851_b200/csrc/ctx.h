@@ -118,10 +118,6 @@ struct MfArg<5> {
 // shared memory (variant 4).
 constexpr int kCDict = 2048;
 template <>
-struct MfArg<8> {  // variant 5 with the x window staged in shared memory: delta[] holds window offsets
-  MfConst c;
-};
-template <>
 struct MfArg<6> {
   double dict[kCDict];
 };
@@ -133,21 +129,6 @@ template <>
 struct MfArg<10> {  // variant 10: 3-byte entries, at most 256 dictionary slots
   double dict[256];
 };
-// Variant 9: value-indexed rows with implicit column offsets (row order 4).  Every row of a
-// (subdomain, kind, class) has its nonzeros at the same internal row offsets, so a row stores only
-// its 16-bit dictionary indices, one per slot of its stencil's offset list (4 slots per 8-byte
-// group); the offset lists and the dictionary are kernel parameters.
-struct MfDia {
-  int32_t valid;
-  int32_t gbeg[kMfMaxTab + 1];  // slot groups of offset list tb: [gbeg[tb], gbeg[tb+1])
-  int4 delta[kMfMaxGroups];     // 4 internal row offsets per group
-  double dict[kCDict];
-};
-template <>
-struct MfArg<9> {
-  MfDia c;
-};
-
 struct SellDev {
   const double* val;
   const int32_t* col;
@@ -164,14 +145,8 @@ struct SellDev {
   const int32_t* mf_begin;  // table t = entries [mf_begin[t], mf_begin[t+1]), padded to a multiple of 4
   const int4* mf_delta;     // 4 row offsets per group
   const double* mf_val;     // values (exact copies of the assembled, Robin-folded SELL entries)
-  // variant 8: per deduplicated table tb, the merged x window [mf_win_begin[tb], mf_win_begin[tb+1]) as
-  // (first row offset a, rows len, shared-memory row base) triples
-  const int32_t* mf_win_begin;
-  const int3* mf_win;
   int64_t nrows;            // rows of the concatenated vectors (bulk-copy bounds)
   const uint8_t* mf_code;   // per row: deduplicated table id of the constant-bank tables, 0xff dummy row
-  const uint2* dia_idx;     // variant 9: per tile, group g of row r at dia_off[tile] + 256 g + r (4 x u16)
-  const int64_t* dia_off;
   const uint4* vi3_off;     // variant 10: 8 int16 offsets per group
   const uint2* vi3_idx;     //   8 u8 dictionary indices per group
   const int64_t* vi3_base;  //   per tile: first group slot
@@ -356,12 +331,6 @@ struct Ctx {
   int vec_tiles = kVecTiles;  // tiles per vector block (update/dir kernels), chosen at assembly
   int vt_override = 0;         // OSM_VT
   bool groups_forced = false;  // OSM_GROUPS given: no size-based reduction
-  // SM-affine persistent SpMV (experimental, OSM_PERSIST=1): tiles in region-major, class-minor order,
-  // one contiguous range per SM and group; per-(group, SM) tile counters + one exit counter per group
-  bool persist = false;
-  int nsm = 148;
-  int32_t* d_tseq = nullptr;
-  uint32_t* d_sm_ctr = nullptr;
   int want_groups = 8;  // OSM_GROUPS = 1, 2, 4 or 8 (capped by the local subdomain count)
 
   // CUDA graph of one chunk of PCG iterations (spmv, update, dir) x kCgChunk, with PDL edges
@@ -375,14 +344,13 @@ struct Ctx {
                     // 3 class, length, then (K, I, J) with J fastest (default); 4: the matrix-free
                     // class-major lattice layout of MfSub (whole subdomain, dummy rows included)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
-  int spmv_variant = 10;  // default 10 (falls back to 6, 7, 3 or 2 when its format does not apply); 0: LDG rows, 2: LDG rows at 32 regs (8 blocks/SM), 1: warp-specialized cp.async.bulk
-                         // pipeline, 3: value-indexed SELL (packed index + offset), 4: 3 with the dictionary
-                         // in shared memory (falls back to 3, then 2, when it does not apply),
-                         // 5: matrix-free Kuhn stencil (row order 4 only; else as 6), 6: 3 with the
-                         // dictionary in the constant bank (else 3), 7: 6 on wide entries
-                         // (chosen automatically when offsets need 20 bits), 8: 5 with the x window staged
-                         // in shared memory by bulk copies, 9: implicit offsets (experimental),
-                         // 10: 6 with 3-byte entries (int16 offset + u8 index streams; <= 256 slots)
+  int spmv_variant = 10;  // SpMV variant (falls back when its format does not apply, spmv_variant_of):
+                          // 2: fp64 SELL rows (LDG streams, 32 registers, 8 blocks/SM);
+                          // 3: value-indexed SELL (packed 16-bit index + offset, dictionary through L1);
+                          // 5: matrix-free Kuhn stencil (row order 4 only; else as 6);
+                          // 6: 3 with the dictionary in the constant bank; 7: 6 on wide entries (chosen
+                          // automatically when offsets need 20 bits);
+                          // 10 (default): 6 with 3-byte entries (int16 offset + u8 index streams; <= 256 slots)
 
   // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
   bool mf_ok = false;
@@ -394,16 +362,6 @@ struct Ctx {
   int64_t mf_entries = 0;         // including padding
   std::vector<int32_t> h_mf_begin, h_mf_delta;
   MfConst* h_mf_const = nullptr;  // host copy of the kernel-parameter tables (valid = 0: global tables)
-  MfConst* h_mf_win_const = nullptr;  // variant 8: the same tables with window offsets in delta[]
-  int32_t* d_mf_win_begin = nullptr;
-  int3* d_mf_win = nullptr;
-  int mf_win_rows = 0;            // largest window (rows) = shared memory of variant 8 / 8 B
-  MfDia* h_dia = nullptr;         // variant 9 kernel parameter (offset lists + dictionary)
-  uint2* d_dia_idx = nullptr;     // variant 9 per-row dictionary indices
-  int64_t* d_dia_off = nullptr;
-  int64_t dia_groups = 0;         // stored 8-byte groups (4 slots each)
-  bool dia_ok = false;
-  std::vector<double> dia_sub_bytes;  // variant 9 bytes read per SpMV per local subdomain (traffic model)
   uint8_t* d_mf_code = nullptr;   // per internal row: deduplicated table id, 0xff dummy (vector kernels)
   // D^{-1} codes (osm.cu dcode_build): per row a 1-byte index into the distinct D^{-1} values (0xff:
   // +0.0, padding rows), so the SELL-path vector kernels read 1 byte instead of 8 per row
@@ -487,11 +445,9 @@ void batch_local_solution(Ctx& c, int b, int s, double* u, int64_t* n);
 void batch_free(Ctx& c);
 double fnorm2_of(Ctx& c);  // ||f||^2 of the glued global system (osm.cu)
 
-void spmv_init_attributes();
 void gravity_z(Ctx& c, double z0, double* d_out);  // gravity.cu (uses c.phi)
 void vi_build(Ctx& c, bool per_side = false);
 void vi_free(Ctx& c);
-void launch_dia_pack(Ctx& c, const int32_t* d_gbeg, const int32_t* d_delta, const uint8_t* d_real, int32_t* d_bad);
 void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side);
 int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)
 

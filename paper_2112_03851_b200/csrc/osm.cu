@@ -90,7 +90,6 @@ static void timers_collect(Ctx& c) {
 }
 
 // ------------------------------------------------------------------ teardown
-static void dia_free(Ctx& c);
 
 static void drop_graph(Ctx& c) {
   if (c.cg_graph) cudaGraphExecDestroy(c.cg_graph);
@@ -103,8 +102,6 @@ static void drop_graph(Ctx& c) {
 
 static void free_assembly(Ctx& c) {
   drop_graph(c);
-  dfree(c.d_tseq);
-  dfree(c.d_sm_ctr);
   batch_free(c);
   vi_free(c);
   for (auto& s : c.subs) {
@@ -173,15 +170,9 @@ static void free_assembly(Ctx& c) {
   c.mf_entries = 0;
   delete c.h_mf_const;
   c.h_mf_const = nullptr;
-  delete c.h_mf_win_const;
-  c.h_mf_win_const = nullptr;
-  dfree(c.d_mf_win_begin);
-  dfree(c.d_mf_win);
-  c.mf_win_rows = 0;
   dfree(c.d_mf_code);
   dfree(c.d_dcode);
   c.h_dcode_tab.clear();
-  dia_free(c);
   c.assembled = false;
   c.density_set = false;
 }
@@ -216,51 +207,6 @@ static void vi_sync_host_dict(Ctx& c) {
   drop_graph(c);
 }
 
-// Variant 8 windows: for every deduplicated table, the union over its entries e of the row ranges
-// [delta_e, delta_e + 256) of a 256-row tile, merged into intervals (16-byte aligned), laid out back
-// to back in shared memory; the table's delta_e are replaced by the shared-memory row of delta_e.
-static void mf_windows(Ctx& c, int ntab) {
-  dfree(c.d_mf_win_begin);
-  dfree(c.d_mf_win);
-  c.mf_win_rows = 0;
-  const MfConst& P = *c.h_mf_const;
-  if (!c.h_mf_win_const) c.h_mf_win_const = new MfConst();
-  MfConst& W = *c.h_mf_win_const;
-  W = P;
-  std::vector<int32_t> wbeg(1, 0);
-  std::vector<int3> win;
-  for (int tb = 0; tb < ntab; ++tb) {
-    const int e0 = 4 * P.gbeg[tb], e1 = 4 * P.gbeg[tb + 1];
-    std::vector<int> ds;
-    for (int e = e0; e < e1; ++e) ds.push_back((&P.delta[0].x)[e]);
-    std::sort(ds.begin(), ds.end());
-    std::vector<std::pair<int, int>> iv;  // merged [a, b)
-    for (int d : ds) {
-      const int a = d & ~1, b = (d + kRowsPerBlock + 1) & ~1;  // even bounds: 16-byte copies
-      if (!iv.empty() && a <= iv.back().second) iv.back().second = std::max(iv.back().second, b);
-      else iv.push_back({a, b});
-    }
-    int base = 0;
-    for (auto& ab : iv) {
-      win.push_back(make_int3(ab.first, ab.second - ab.first, base));
-      base += ab.second - ab.first;
-    }
-    c.mf_win_rows = std::max(c.mf_win_rows, base);
-    for (int e = e0; e < e1; ++e) {
-      const int d = (&P.delta[0].x)[e];
-      for (size_t i = 0; i < iv.size(); ++i)
-        if (d >= iv[i].first && d + kRowsPerBlock <= iv[i].second) {
-          (&W.delta[0].x)[e] = win[win.size() - iv.size() + i].z + (d - iv[i].first);
-          break;
-        }
-    }
-    wbeg.push_back((int32_t)win.size());
-  }
-  c.d_mf_win_begin = dupload(c, wbeg);
-  c.d_mf_win = dupload(c, win);
-}
-
-// Copy the table values from the (folded) SELL and verify the tables against every row.
 static void mf_refresh(Ctx& c) {
   launch_mf_refresh(c);
   OSM_CUDA(cudaMemsetAsync(c.d_flags + 3, 0, sizeof(int32_t), c.stream));
@@ -319,7 +265,6 @@ static void mf_refresh(Ctx& c) {
     P.tabid[t] = (int16_t)it->second;  // t = (ls * 3 + kind) * ncls + class, as mf_table_of
   }
   P.valid = 1;
-  mf_windows(c, nt);
   // per-row table codes for the vector kernels (D^{-1} from the tables, dummy rows skipped)
   if (nt <= 255) {
     if (!c.d_mf_code) c.d_mf_code = dalloc<uint8_t>(c.nrows_total);
@@ -363,96 +308,6 @@ static void dcode_build(Ctx& c) {
   if (!c.d_dcode) c.d_dcode = dalloc<uint8_t>(c.nrows_total);
   OSM_CUDA(cudaMemcpy(c.d_dcode, code.data(), code.size(), cudaMemcpyHostToDevice));
   c.h_dcode_tab = tab;
-}
-
-static void dia_free(Ctx& c) {
-  dfree(c.d_dia_idx);
-  dfree(c.d_dia_off);
-  delete c.h_dia;
-  c.h_dia = nullptr;
-  c.dia_groups = 0;
-  c.dia_ok = false;
-  c.dia_sub_bytes.clear();
-}
-
-// Value-indexed rows with implicit column offsets (SpMV variant 9, row order 4).  The offset list of
-// a row is the nonzero part of its (subdomain, kind, class) stencil table (MfConst.delta, padding
-// slots aside); the row stores one 16-bit dictionary index per slot, taken from its own assembled,
-// Robin-folded SELL entries by k_dia_pack.  Rebuilt whenever the tables or the dictionary slots
-// change (assembly, osm_set_robin).
-static void dia_build(Ctx& c) {
-  dia_free(c);
-  const bool dbg = std::getenv("OSM_DEBUG") != nullptr;
-  if (!c.mf_ok || !c.h_mf_const || !c.h_mf_const->valid || !c.d_mf_code || !c.vi_ok || !c.vi_idx ||
-      c.vi_ndict > kCDict) {
-    if (dbg)
-      std::fprintf(stderr, "dia: prerequisites mf_ok %d const %d code %d vi_ok %d vi_idx %d ndict %lld\n", (int)c.mf_ok,
-                   c.h_mf_const && c.h_mf_const->valid, c.d_mf_code != nullptr, (int)c.vi_ok, c.vi_idx != nullptr,
-                   (long long)c.vi_ndict);
-    return;
-  }
-  const MfConst& P = *c.h_mf_const;
-  int ntab = 0;  // deduplicated tables (some may be empty)
-  for (size_t t = 0; t + 1 < c.h_mf_begin.size(); ++t) ntab = std::max(ntab, P.tabid[t] + 1);
-  std::vector<uint8_t> code(c.nrows_total);
-  OSM_CUDA(cudaMemcpy(code.data(), c.d_mf_code, c.nrows_total, cudaMemcpyDeviceToHost));
-  std::vector<int64_t> doff(c.nblk_total);
-  const int nloc = c.s_end - c.s_begin;
-  c.dia_sub_bytes.assign(nloc, 0.0);
-  int64_t groups = 0;
-  std::vector<int> tsub(c.nblk_total, 0);
-  for (int ls = 0; ls < nloc; ++ls)
-    for (int64_t k = 0; k < c.subs[ls].nblk; ++k) tsub[c.subs[ls].blk0 + k] = ls;
-  for (int64_t t = 0; t < c.nblk_total; ++t) {
-    int w = 0;
-    for (int l = 0; l < kRowsPerBlock; ++l) {
-      const int tb = code[t * kRowsPerBlock + l];
-      if (tb == 0xff) continue;
-      if (tb >= ntab) {
-        if (dbg) std::fprintf(stderr, "dia: code %d >= ntab %d\n", tb, ntab);
-        return;
-      }
-      const int g = P.gbeg[tb + 1] - P.gbeg[tb];
-      w = std::max(w, g);
-      c.dia_sub_bytes[tsub[t]] += 8.0 * g;  // the row's index groups
-    }
-    c.dia_sub_bytes[tsub[t]] += kRowsPerBlock;  // 1-byte codes
-    doff[t] = groups;
-    groups += (int64_t)w * kRowsPerBlock;
-  }
-  const int nslot = 4 * P.gbeg[ntab];
-  std::vector<int32_t> gbeg(P.gbeg, P.gbeg + ntab + 1), delta(std::max(1, nslot));
-  std::vector<uint8_t> real(std::max(1, nslot));
-  for (int k = 0; k < nslot; ++k) {
-    delta[k] = (&P.delta[0].x)[k];
-    real[k] = P.val[k] != 0.0;  // the tables hold only nonzero values; +0.0 marks padding
-  }
-  c.d_dia_off = dupload(c, doff);
-  c.d_dia_idx = dalloc<uint2>(std::max<int64_t>(1, groups));
-  int32_t* d_gbeg = dupload(c, gbeg);
-  int32_t* d_delta = dupload(c, delta);
-  uint8_t* d_real = dupload(c, real);
-  OSM_CUDA(cudaMemsetAsync(c.d_flags + 3, 0, sizeof(int32_t), c.stream));
-  launch_dia_pack(c, d_gbeg, d_delta, d_real, c.d_flags + 3);
-  int32_t bad = 0;
-  OSM_CUDA(cudaMemcpyAsync(&bad, c.d_flags + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
-  OSM_CUDA(cudaStreamSynchronize(c.stream));
-  dfree(d_gbeg);
-  dfree(d_delta);
-  dfree(d_real);
-  drop_graph(c);
-  if (bad) {
-    if (dbg) std::fprintf(stderr, "dia: %d rows do not match their offset lists\n", bad);
-    dia_free(c);
-    return;
-  }
-  c.h_dia = new MfDia();
-  std::memset(c.h_dia, 0, sizeof(MfDia));
-  c.h_dia->valid = 1;
-  std::copy(gbeg.begin(), gbeg.end(), c.h_dia->gbeg);
-  std::copy(P.delta, P.delta + P.gbeg[ntab], c.h_dia->delta);
-  c.dia_groups = groups;
-  c.dia_ok = true;
 }
 
 // Matrix-free Kuhn-stencil tables (SpMV variant 5, row order 4).  For every
@@ -790,10 +645,7 @@ static void assemble(Ctx& c) {
   }
   vi_build(c);  // value-indexed hot copy (from the unfolded K^N values)
   vi_sync_host_dict(c);
-  if (c.sort_key == 4) {
-    mf_build(c, h_iperm, h_len, h_soff);
-    dia_build(c);
-  }
+  if (c.sort_key == 4) mf_build(c, h_iperm, h_len, h_soff);
 
   // --- reductions and device side table
   c.part = dalloc<double>(3 * c.nblk_total);
@@ -831,49 +683,6 @@ static void assemble(Ctx& c) {
     c.g_nblk[g] = (s1 < nloc ? c.subs[s1].blk0 : c.nblk_total) - c.subs[s0].blk0;
     c.g_vb0[g] = hst[s0].vblk0;
     c.g_nvb[g] = (s1 < nloc ? hst[s1].vblk0 : c.nvblk_total) - hst[s0].vblk0;
-  }
-  if (c.persist) {  // tile order of the SM-affine SpMV: per group, by (region of the first row, class)
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    c.nsm = sms;
-    std::vector<int32_t> seq(c.nblk_total);
-    std::vector<std::tuple<int64_t, int64_t, int64_t, int64_t, int32_t>> key;  // (sub, region a, b, d; tile)
-    for (int g = 0; g < c.ngroups; ++g) {
-      key.clear();
-      for (int64_t t = c.g_blk0[g]; t < c.g_blk0[g] + c.g_nblk[g]; ++t) {
-        int ls = 0;
-        while (ls + 1 < nloc && c.subs[ls + 1].blk0 <= t) ++ls;
-        const Sub& S = c.subs[ls];
-        const auto& perm = h_perm[ls];
-        int64_t a = INT64_MAX, b = 0, d = 0;  // the first real row's position on the class sub-lattice
-        for (int l = 0; l < kRowsPerBlock; ++l) {
-          const int32_t lc = perm[(t - S.blk0) * kRowsPerBlock + l];
-          if (lc < 0) continue;
-          const int64_t I = S.g.I_lo + lc % S.g.nI, t2 = lc / S.g.nI, J = 1 + t2 % S.g.nJ, K = 1 + t2 / S.g.nJ;
-          if (c.sort_key == 4) {
-            a = I / o, b = K / o, d = J / o;
-          } else {
-            a = K / o, b = I / o, d = J / o;
-          }
-          break;
-        }
-        key.emplace_back(ls, a, b, d, (int32_t)t);  // stable sort: equal regions keep the class order
-      }
-      std::vector<size_t> ix(key.size());
-      std::iota(ix.begin(), ix.end(), 0);
-      std::stable_sort(ix.begin(), ix.end(), [&](size_t i, size_t j) {
-        const auto& A = key[i];
-        const auto& B = key[j];
-        return std::make_tuple(std::get<0>(A), std::get<1>(A), std::get<2>(A), std::get<3>(A)) <
-               std::make_tuple(std::get<0>(B), std::get<1>(B), std::get<2>(B), std::get<3>(B));
-      });
-      for (size_t k = 0; k < ix.size(); ++k) seq[c.g_blk0[g] + (int64_t)k] = std::get<4>(key[ix[k]]);
-    }
-    dfree(c.d_tseq);
-    dfree(c.d_sm_ctr);
-    c.d_tseq = dupload(c, seq);
-    c.d_sm_ctr = dalloc<uint32_t>((int64_t)Ctx::kMaxGroups * (c.nsm + 1));
-    OSM_CUDA(cudaMemsetAsync(c.d_sm_ctr, 0, sizeof(uint32_t) * Ctx::kMaxGroups * (c.nsm + 1), c.stream));
   }
   if (c.h_st) cudaFreeHost(c.h_st);
   OSM_CUDA(cudaMallocHost((void**)&c.h_st, sizeof(SubState) * std::max(1, nloc)));
@@ -944,7 +753,6 @@ static void apply_robin(Ctx& c) {
   vi_apply_robin(c, a, qv);
   vi_sync_host_dict(c);
   dcode_build(c);
-  if (c.sort_key == 4) dia_build(c);
   if (flags[0]) fail(OSM_ERR_PRECOND, "non-positive diagonal entry after the Robin term");
   c.robin_dirty = false;
 }
@@ -1192,7 +1000,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   c.traffic[7] = c.exch_bytes;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
-  const bool vi = sv == 3 || sv == 4 || sv == 6 || sv == 7 || sv == 10, mf = sv == 5 || sv == 8, dia = sv == 9;
+  const bool vi = sv == 3 || sv == 6 || sv == 7 || sv == 10, mf = sv == 5;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1201,9 +1009,9 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     // value-indexed 4 B/entry (index + offset; the dictionary is on chip), or matrix-free 0 B/entry
     // (tables in the constant bank); vectors p, q 16 B/row
     const double kept = ls < (int)c.vi_kept.size() ? (double)c.vi_kept[ls] : (double)S.nnz;
-    // (variant 5 reads a 1-byte table code per row; variant 9 its 8-byte index groups and the code)
+    // (variant 5 reads a 1-byte table code per row)
     const double mat = mf ? (c.d_mf_code ? (double)S.npad : 0.0)
-                          : dia ? c.dia_sub_bytes[ls] : (vi ? (sv == 10 ? 3.0 : 4.0) * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
+                          : (vi ? (sv == 10 ? 3.0 : 4.0) * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
     // D^-1 as an 8-byte stream, or as a 1-byte code (table codes of variant 5, dcode_build otherwise)
@@ -1319,7 +1127,6 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
       c.want_groups = std::max(1, std::atoi(e));
       c.groups_forced = true;
     }
-    if (const char* e = std::getenv("OSM_PERSIST")) c.persist = std::atoi(e) != 0;
     if (const char* e = std::getenv("OSM_VT")) c.vt_override = std::atoi(e);
     if (const char* e = std::getenv("OSM_SIGMA")) c.sigma = std::atoi(e);
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
@@ -1327,7 +1134,6 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_UPD")) c.update_variant = std::atoi(e);
     if (const char* e = std::getenv("OSM_SORT")) c.sort_key = std::atoi(e);
     if (const char* e = std::getenv("OSM_DCODE")) c.dcode_on = std::atoi(e) != 0;
-    spmv_init_attributes();
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "exchange"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];
@@ -1801,7 +1607,8 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v < 0 || v > 10) fail(OSM_ERR_INVALID_ARG, "SpMV variant must be 0..10");
+  if (v != 2 && v != 3 && v != 5 && v != 6 && v != 7 && v != 10)
+    fail(OSM_ERR_INVALID_ARG, "SpMV variant must be one of 2, 3, 5, 6, 7, 10");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);

@@ -144,111 +144,6 @@ __device__ __forceinline__ double tile_row_ldg(const SellDev& A, int64_t blk, co
   return s;
 }
 
-// Variant 1 (bulk async copy): one elected thread streams the tile's value/column chunks
-// (CH entries x 256 rows, contiguous) into an NST-stage shared-memory ring with
-// cp.async.bulk completing on mbarriers (SASS UBLKCP); all warps only read shared memory
-// and gather x.  The copy engine keeps the HBM stream in flight independently of the
-// warps' gather latency.  Every thread of the block must call this (block barriers).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Warp-specialized pipeline: warps 0..7 consume (row = threadIdx.x < 256), warp 8 produces.
-// full[st]: the stage's bytes have landed (tx count); empty[st]: all 8 consumer warps are done.
-constexpr int kBulkCH = 4;   // entries per stage
-constexpr int kBulkNST = 2;  // stages (24 KB ring: leaves L1 room for the x window)
-constexpr int kBulkStageBytes = kBulkCH * kRowsPerBlock * 12;
-constexpr int kBulkSmem = kBulkNST * kBulkStageBytes + 2 * kBulkNST * 8;
-constexpr int kBulkThreads = kRowsPerBlock + 32;
-
-__device__ __forceinline__ double tile_row_bulk(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                                unsigned char* smem) {
-  constexpr int T = kRowsPerBlock;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkNST * kBulkStageBytes);
-  uint64_t* empty = full + kBulkNST;
-  const int w = A.twidth[blk];
-  const int64_t off = A.toff[blk];
-  const int nch = (w + kBulkCH - 1) / kBulkCH;
-  if (threadIdx.x == T) {
-    for (int i = 0; i < kBulkNST; ++i) {
-      mbar_init_n(&full[i], 1);
-      mbar_init_n(&empty[i], kSlicesPerBlock);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x >= T) {  // producer warp: one elected lane streams the chunks
-    if (threadIdx.x == T) {
-      for (int ch = 0; ch < nch; ++ch) {
-        const int st = ch % kBulkNST;
-        if (ch >= kBulkNST) mbar_wait(&empty[st], (uint32_t)(((ch / kBulkNST) - 1) & 1));
-        const int kk = min(kBulkCH, w - ch * kBulkCH);
-        double* sv = reinterpret_cast<double*>(smem + st * kBulkStageBytes);
-        int32_t* sc = reinterpret_cast<int32_t*>(smem + st * kBulkStageBytes + kBulkCH * T * 8);
-        const uint32_t bv = (uint32_t)kk * T * 8, bc = (uint32_t)kk * T * 4;
-        mbar_expect(&full[st], bv + bc);
-        bulk_g2s(sv, A.val + off + (int64_t)ch * kBulkCH * T, bv, &full[st]);
-        bulk_g2s(sc, A.col + off + (int64_t)ch * kBulkCH * T, bc, &full[st]);
-      }
-    }
-    return 0.0;
-  }
-  for (int ch = 0; ch < nch; ++ch) {
-    const int st = ch % kBulkNST;
-    mbar_wait(&full[st], (uint32_t)((ch / kBulkNST) & 1));
-    const double* sv = reinterpret_cast<const double*>(smem + st * kBulkStageBytes);
-    const int32_t* sc = reinterpret_cast<const int32_t*>(smem + st * kBulkStageBytes + kBulkCH * T * 8);
-    const int kk = min(kBulkCH, w - ch * kBulkCH);
-    if (kk == kBulkCH) {
-      int32_t cj[kBulkCH];
-      double vj[kBulkCH], xv[kBulkCH];
-#pragma unroll
-      for (int j = 0; j < kBulkCH; ++j) {
-        cj[j] = sc[j * T + threadIdx.x];
-        vj[j] = sv[j * T + threadIdx.x];
-      }
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);  // stage data is in registers now
-#pragma unroll
-      for (int j = 0; j < kBulkCH; ++j) xv[j] = __ldg(x + cj[j]);
-#pragma unroll
-      for (int j = 0; j < kBulkCH; ++j) s = fma(vj[j], xv[j], s);
-    } else {
-      for (int j = 0; j < kk; ++j) s = fma(sv[j * T + threadIdx.x], __ldg(x + sc[j * T + threadIdx.x]), s);
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);
-    }
-  }
-  return s;
-}
-
 // Variant 3 (value-indexed): each entry is one 32-bit word (dictionary index << 16 | 16-bit
 // column offset), 4 entries of a row per 16-byte load; the dictionary (tens to thousands of
 // distinct values) is read through L1.  The next group's load is issued before the current
@@ -282,10 +177,6 @@ __device__ __forceinline__ double tile_row_vi(const SellDev& A, int64_t blk, con
   }
   return s;
 }
-
-// Variant 4: variant 3 with the dictionary staged in shared memory at block start (dictionary
-// lookups leave the L1 tag path; used when the dictionary fits kSmemDict entries).
-constexpr int kSmemDict = 2048;
 
 // Loads of a tile that touch only static data (the matrix copy, the block -> subdomain map, row codes).
 // k_cg_spmv issues them before griddepcontrol.wait, so they overlap the tail of the previous kernel.
@@ -367,7 +258,8 @@ __device__ __forceinline__ double tile_row_vi3(const SellDev& A, int64_t blk, co
                                                const double* dict, const TilePre* pre = nullptr) {
   constexpr int T = kRowsPerBlock;
   const int ng = pre ? pre->ng : (A.vtw[blk] + 7) >> 3;
-  const int64_t b = A.vi3_base[blk] + threadIdx.x;
+  // the row's group index: from tile_pre's pointer when given (no dependent load after the wait)
+  const int64_t b = pre ? reinterpret_cast<const uint4*>(pre->gp) - A.vi3_off : A.vi3_base[blk] + threadIdx.x;
   const double* xr = x + blk * T + threadIdx.x;
   double s = 0.0;
   if (ng == 0) return s;
@@ -464,121 +356,9 @@ __device__ __forceinline__ double tile_row_mf(const SellDev& A, int64_t blk, con
   return s;
 }
 
-__device__ __forceinline__ uint2 ld_stream2(const uint2* p) {
-  uint2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-  return v;
-}
-
-// Variant 9: value-indexed rows with implicit column offsets (row order 4, see MfDia).  The row's
-// 1-byte code selects its offset list (constant bank); the row's own 16-bit dictionary indices
-// stream in 8-byte groups of 4, coalesced across the warp, and no longer gate the x gathers (their
-// addresses come from the offset list).  Same FMA chain as the SELL variants.
-__device__ __forceinline__ double tile_row_dia(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                               const MfDia& P) {
-  const int64_t ri = blk * kRowsPerBlock + threadIdx.x;
-  double s = 0.0;
-  const int tb = __ldg(A.mf_code + ri);
-  if (tb == 0xff) return s;  // dummy row
-  const double* xr = x + ri;
-  asm("" : "+l"(xr));
-  const uint2* ip = A.dia_idx + A.dia_off[blk] + threadIdx.x;
-  const int g0 = P.gbeg[tb], ng = P.gbeg[tb + 1] - g0;
-  if (ng == 0) return s;
-  uint2 e = ld_stream2(ip);
-  for (int j = 0; j < ng; ++j) {
-    const int4 d = P.delta[g0 + j];
-    const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
-    const double v0 = P.dict[e.x & 0xffffu], v1 = P.dict[e.x >> 16], v2 = P.dict[e.y & 0xffffu],
-                 v3 = P.dict[e.y >> 16];
-    if (j + 1 < ng) e = ld_stream2(ip + (int64_t)kRowsPerBlock * (j + 1));
-    s = fma(v0, x0, s);
-    s = fma(v1, x1, s);
-    s = fma(v2, x2, s);
-    s = fma(v3, x3, s);
-  }
-  return s;
-}
-
-// Variant 8: variant 5 with the tile's x window staged in shared memory.  When all real rows of
-// the tile share one table (all but the tiles straddling a class or plane boundary), one thread
-// issues the bulk copies (cp.async.bulk, one per merged window interval, completing on an
-// mbarrier) and every gather becomes a shared-memory read at the entry's window offset; the FMA
-// chain is the same, so the iterations are still bitwise identical.  Straddling tiles use the
-// global-table gathers of variant 5.  Every thread of the block must call this (block barriers).
-__device__ __forceinline__ double tile_row_mf_win(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                                  const MfConst& P, unsigned char* smem) {
-  __shared__ uint64_t bar;
-  __shared__ int tlo, thi;
-  const int ls = A.blk_sub[blk];
-  const MfSub& M = A.mf_sub[ls];
-  const int64_t r0 = blk * kRowsPerBlock;
-  const int64_t ri = r0 + threadIdx.x;
-  const int t = mf_table_of(M, ri - M.row0);
-  if (threadIdx.x == 0) {
-    tlo = 0x7fffffff;
-    thi = -1;
-  }
-  __syncthreads();
-  if (t >= 0) {
-    atomicMin(&tlo, t);
-    atomicMax(&thi, t);
-  }
-  __syncthreads();
-  double s = 0.0;
-  if (thi < 0) return s;  // dummy rows only
-  if (tlo != thi) {       // straddling tile
-    if (t < 0) return s;
-    const double* xr = x + ri;
-    const double2* vv = reinterpret_cast<const double2*>(A.mf_val);
-    for (int g = A.mf_begin[t] >> 2; g < (A.mf_begin[t + 1] >> 2); ++g) {
-      const int4 d = A.mf_delta[g];
-      const double2 v01 = vv[2 * g], v23 = vv[2 * g + 1];
-      const double x0 = __ldg(xr + d.x), x1 = __ldg(xr + d.y), x2 = __ldg(xr + d.z), x3 = __ldg(xr + d.w);
-      s = fma(v01.x, x0, s);
-      s = fma(v01.y, x1, s);
-      s = fma(v23.x, x2, s);
-      s = fma(v23.y, x3, s);
-    }
-    return s;
-  }
-  const int tb = P.tabid[tlo];
-  double* xs = reinterpret_cast<double*>(smem);
-  if (threadIdx.x == 0) {
-    mbar_init_n(&bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int w0 = A.mf_win_begin[tb], w1 = A.mf_win_begin[tb + 1];
-    uint32_t bytes = 0;
-    for (int i = w0; i < w1; ++i) {
-      const int3 w = A.mf_win[i];
-      const int64_t lo = max(r0 + w.x, (int64_t)0), hi = min(r0 + w.x + w.y, A.nrows);
-      if (hi > lo) bytes += (uint32_t)(hi - lo) * 8u;
-    }
-    mbar_expect(&bar, bytes);
-    for (int i = w0; i < w1; ++i) {
-      const int3 w = A.mf_win[i];
-      const int64_t lo = max(r0 + w.x, (int64_t)0), hi = min(r0 + w.x + w.y, A.nrows);
-      if (hi > lo) bulk_g2s(xs + w.z + (lo - (r0 + w.x)), x + lo, (uint32_t)(hi - lo) * 8u, &bar);
-    }
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  if (t < 0) return s;
-  const double* xt = xs + threadIdx.x;
-  for (int g = P.gbeg[tb]; g < P.gbeg[tb + 1]; ++g) {
-    const int4 d = P.delta[g];  // window offsets
-    const double x0 = xt[d.x], x1 = xt[d.y], x2 = xt[d.z], x3 = xt[d.w];
-    s = fma(P.val[4 * g], x0, s);
-    s = fma(P.val[4 * g + 1], x1, s);
-    s = fma(P.val[4 * g + 2], x2, s);
-    s = fma(P.val[4 * g + 3], x3, s);
-  }
-  return s;
-}
-
-// V = 0: LDG rows; V = 2: LDG rows with registers capped at 32 (8 blocks / 64 warps per SM);
-// V = 1: warp-specialized bulk-copy pipeline; V = 3: value-indexed rows (32 registers);
-// V = 4: value-indexed rows, dictionary in shared memory; V = 5: matrix-free Kuhn stencil.
+// V = 2: fp64 SELL rows (LDG streams, registers capped at 32: 8 blocks / 64 warps per SM);
+// V = 3: value-indexed rows, dictionary through L1; V = 5: matrix-free Kuhn stencil; V = 6/7:
+// value-indexed rows (normal / wide entries), dictionary in the constant bank; V = 10: 3-byte entries.
 template <int V>
 __device__ __forceinline__ TilePre tile_pre(const SellDev& A, const int32_t* __restrict__ blk_sub, int64_t blk,
                                             const MfArg<V>& mf) {
@@ -617,24 +397,15 @@ __device__ __forceinline__ TilePre tile_pre(const SellDev& A, const int32_t* __r
 
 template <int V>
 __device__ __forceinline__ double tile_row(const SellDev& A, int64_t blk, const double* __restrict__ x,
-                                           unsigned char* smem, const MfArg<V>& mf, const TilePre* pre = nullptr) {
-  if constexpr (V == 1) return tile_row_bulk(A, blk, x, smem);
+                                           const MfArg<V>& mf, const TilePre* pre = nullptr) {
   if constexpr (V == 3) return tile_row_vi(A, blk, x);
   if constexpr (V == 5) return tile_row_mf(A, blk, x, mf.c, pre);
-  if constexpr (V == 8) return tile_row_mf_win(A, blk, x, mf.c, smem);
-  if constexpr (V == 9) return tile_row_dia(A, blk, x, mf.c);
   if constexpr (V == 6) return tile_row_vi_smem<false>(A, blk, x, mf.dict, pre);
   if constexpr (V == 7) return tile_row_vi_smem<true>(A, blk, x, mf.dict, pre);
   if constexpr (V == 10) return tile_row_vi3(A, blk, x, mf.dict, pre);
-  if constexpr (V == 4) {
-    double* sd = reinterpret_cast<double*>(smem);
-    for (int i = threadIdx.x; i < A.ndict; i += blockDim.x) sd[i] = A.dict[i];
-    __syncthreads();
-    return tile_row_vi_smem(A, blk, x, sd);
-  }
   return tile_row_ldg<4>(A, blk, x);
 }
-#define OSM_SPMV_BOUNDS(V) __launch_bounds__((V) == 1 ? kBulkThreads : kThreads, ((V) >= 2) ? 8 : 1)
+#define OSM_SPMV_BOUNDS(V) __launch_bounds__(kThreads, 8)
 
 // ---------------------------------------------------------------- PCG kernels
 
@@ -644,7 +415,7 @@ __device__ __forceinline__ void spmv_tile(const SellDev& A, int64_t blk, const i
                                           SubState* __restrict__ st, const double* __restrict__ p,
                                           double* __restrict__ q, double* __restrict__ part, int64_t stride,
                                           int32_t* __restrict__ nactive, const MfArg<V>& mf, double* sm,
-                                          unsigned char* dsm, const TilePre& pre) {
+                                          const TilePre& pre) {
   const int ls = pre.ls;
   if (!st[ls].active) {  // the previous direction kernel has paid the stopped subdomain's x update
     if (threadIdx.x == 0 && blk == st[ls].blk0) st[ls].xpend = 0;
@@ -652,7 +423,7 @@ __device__ __forceinline__ void spmv_tile(const SellDev& A, int64_t blk, const i
   }
   const bool has_row = threadIdx.x < kRowsPerBlock;
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double y = tile_row<V>(A, blk, p, dsm, mf, &pre);
+  const double y = tile_row<V>(A, blk, p, mf, &pre);
   double v[1] = {0.0};
   if (has_row) {
     q[row] = y;
@@ -683,77 +454,12 @@ __global__ void OSM_SPMV_BOUNDS(V) k_cg_spmv(SellDev A, const int32_t* __restric
                                                       double* __restrict__ q, double* __restrict__ part,
                                                       int64_t stride, int32_t* __restrict__ nactive,
                                                       const __grid_constant__ MfArg<V> mf, int64_t blk_base) {
-  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  constexpr int NW = kSlicesPerBlock;
   __shared__ double sm[NW * 1];
-  extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x + blk_base;
   const TilePre pre = tile_pre<V>(A, blk_sub, blk, mf);  // static data: before the dependency wait
   pdl_enter();
-  spmv_tile<V, NW>(A, blk, blk_sub, st, p, q, part, stride, nactive, mf, sm, dsm, pre);
-}
-
-// SM-affine persistent SpMV (experimental, OSM_PERSIST=1).  The group's tiles, in region-major /
-// class-minor order (seq), are cut into one contiguous range per SM; a block takes tiles from the range
-// of the SM it runs on, so the blocks resident on one SM work on the same few regions in all classes
-// and share their x lines in L1.  Exhausted ranges are skipped; other SMs' ranges are stolen at the
-// end.  Each tile is computed exactly as k_cg_spmv computes it (same partials, bitwise).
-__device__ __forceinline__ unsigned smid_reg() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-template <int V>
-__global__ void __launch_bounds__(kThreads, 8) k_cg_spmv_sm(SellDev A, const int32_t* __restrict__ blk_sub,
-                                                           SubState* __restrict__ st, const double* __restrict__ p,
-                                                           double* __restrict__ q, double* __restrict__ part,
-                                                           int64_t stride, int32_t* __restrict__ nactive,
-                                                           const __grid_constant__ MfArg<V> mf,
-                                                           const int32_t* __restrict__ seq, int nseq, int nsm,
-                                                           uint32_t* __restrict__ ctr) {
-  constexpr int NW = kSlicesPerBlock;
-  __shared__ double sm[NW];
-  __shared__ int pos_sh, found_sh;
-  pdl_enter();
-  const int me = (int)(smid_reg() % (unsigned)nsm);
-  int s = me;
-  for (;;) {
-    const int b = (int)((int64_t)s * nseq / nsm), e = (int)((int64_t)(s + 1) * nseq / nsm);
-    if (threadIdx.x == 0) pos_sh = b + (int)atomicAdd(&ctr[s], 1u);
-    __syncthreads();
-    int pos = pos_sh;
-    while (pos < e) {
-      // the next tile's counter bump is in flight while this tile runs (thread 0 waits on it at the end)
-      unsigned nxt = 0;
-      if (threadIdx.x == 0) nxt = atomicAdd(&ctr[s], 1u);
-      const int64_t blk = seq[pos];
-      spmv_tile<V, NW>(A, blk, blk_sub, st, p, q, part, stride, nactive, mf, sm, nullptr,
-                       tile_pre<V>(A, blk_sub, blk, mf));
-      __syncthreads();  // every thread has read pos_sh
-      if (threadIdx.x == 0) pos_sh = b + (int)nxt;
-      __syncthreads();
-      pos = pos_sh;
-    }
-    // steal: the nearest SM range (in SM order after this one) with tiles left
-    if (threadIdx.x == 0) found_sh = nsm;
-    __syncthreads();
-    for (int k = threadIdx.x + 1; k < nsm; k += blockDim.x) {
-      const int s2 = (me + k) % nsm;
-      const int b2 = (int)((int64_t)s2 * nseq / nsm), e2 = (int)((int64_t)(s2 + 1) * nseq / nsm);
-      if (b2 + (int)__ldcg(&ctr[s2]) < e2) atomicMin(&found_sh, k);
-    }
-    __syncthreads();
-    const int f = found_sh;
-    __syncthreads();
-    if (f >= nsm) break;
-    s = (me + f) % nsm;
-  }
-  if (threadIdx.x == 0) {  // the last block out resets the counters for the next launch
-    __threadfence();
-    if (atomicAdd(&ctr[nsm], 1u) == gridDim.x - 1) {
-      for (int k = 0; k <= nsm; ++k) ctr[k] = 0;
-      __threadfence();
-    }
-  }
+  spmv_tile<V, NW>(A, blk, blk_sub, st, p, q, part, stride, nactive, mf, sm, pre);
 }
 
 // r -= alpha q ; z = D^{-1} r ; r.z, r.r ; stop test ||r|| <= tol ||rhs||; beta.  (x += alpha p moves to
@@ -932,13 +638,12 @@ __global__ void OSM_SPMV_BOUNDS(V) k_warm(SellDev A, const int32_t* __restrict__
                                                    double* __restrict__ r, double* __restrict__ p,
                                                    double* __restrict__ part, int64_t stride, double tol,
                                                    int32_t* __restrict__ nactive, const __grid_constant__ MfArg<V> mf) {
-  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  constexpr int NW = kSlicesPerBlock;
   __shared__ double sm[NW * 3];
-  extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double ax = tile_row<V>(A, blk, x, dsm, mf);
+  const double ax = tile_row<V>(A, blk, x, mf);
   double v[3] = {0.0, 0.0, 0.0};
   if (threadIdx.x < kRowsPerBlock) {
     const int sl = islot[row];
@@ -1033,13 +738,12 @@ __global__ void OSM_SPMV_BOUNDS(V) k_resid(SellDev A, const int32_t* __restrict_
                                                     const double* __restrict__ b, const int32_t* __restrict__ islot,
                                                     double* __restrict__ wif_all, double* __restrict__ part,
                                                     int64_t stride, const __grid_constant__ MfArg<V> mf) {
-  constexpr int NW = V == 1 ? kBulkThreads / 32 : kSlicesPerBlock;
+  constexpr int NW = kSlicesPerBlock;
   __shared__ double sm[NW * 1];
-  extern __shared__ __align__(128) unsigned char dsm[];
   const int64_t blk = blockIdx.x;
   const int ls = blk_sub[blk];
   const int64_t row = blk * kRowsPerBlock + threadIdx.x;
-  const double ax = tile_row<V>(A, blk, ut, dsm, mf);
+  const double ax = tile_row<V>(A, blk, ut, mf);
   double v[1] = {0.0};
   if (threadIdx.x < kRowsPerBlock) {
     const double w = b[row] - ax;
@@ -1103,28 +807,16 @@ SellDev sell_of(const Ctx& c) {
   return SellDev{c.sell_val,  c.sell_col,   c.sell_soff,  c.sell_swidth,
                  c.vi_packed, c.vi_poff,     c.vi_tw,      c.vi_dict,    (int)c.vi_ndict,
                  c.blk_sub,   c.d_mf_sub,    c.d_mf_begin, reinterpret_cast<const int4*>(c.d_mf_delta),
-                 c.d_mf_val,  c.d_mf_win_begin, c.d_mf_win, c.nrows_total,
+                 c.d_mf_val,  c.nrows_total,
                  c.h_mf_const && c.h_mf_const->valid ? c.d_mf_code : nullptr,
-                 c.d_dia_idx, c.d_dia_off, c.vi3_off,    c.vi3_idx,  c.vi3_base};
+                 c.vi3_off,    c.vi3_idx,  c.vi3_base};
 }
 
 }  // namespace
 
-constexpr int kMfWinSmemMax = 200 * 1024;  // variant 8 window (bytes); larger windows fall back to 5
-
 int spmv_variant_of(const Ctx& c) {
   int v = c.spmv_variant;
-  if (v == 9) {
-    if (c.dia_ok && c.h_dia && c.vi_ndict <= kCDict) return 9;
-    v = 6;
-  }
-  if (v == 8) {
-    if (c.mf_ok && c.h_mf_win_const && c.h_mf_win_const->valid && c.d_mf_win &&
-        c.mf_win_rows * 8 <= kMfWinSmemMax)
-      return 8;
-    v = 5;
-  }
-  if (v == 10) {  // 3-byte entries (experimental)
+  if (v == 10) {  // 3-byte entries
     if (c.vi_ok && c.vi3_ok && c.vi_ndict <= 256) return 10;
     v = 6;
   }
@@ -1132,35 +824,13 @@ int spmv_variant_of(const Ctx& c) {
     if (c.mf_ok) return 5;
     v = 6;
   }
-  if (v < 3) return v;
+  if (v == 2) return 2;
   // value-indexed family
   if (!c.vi_ok) return 2;
   if (c.vi_wide) return c.vi_ndict <= kCDict ? 7 : 2;  // wide entries: constant-bank kernel only
   if (v == 7) v = 6;
   if (v == 6) return c.vi_ndict <= kCDict ? 6 : 3;
-  if (v == 4) return c.vi_ndict <= kSmemDict ? 4 : 3;
   return 3;
-}
-
-static int spmv_smem(const Ctx& c) {
-  const int v = spmv_variant_of(c);
-  if (v == 8) return 8 * c.mf_win_rows;
-  return v == 1 ? kBulkSmem : (v == 4 ? (int)(sizeof(double) * c.vi_ndict) : 0);
-}
-
-// dynamic shared memory above the 48 KB default needs the per-kernel opt-in
-template <typename K>
-static void smem_optin(K kern, int bytes) {
-  if (bytes > 48 * 1024) OSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-}
-
-void spmv_init_attributes() {
-  static bool done = false;
-  if (done) return;
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
-  OSM_CUDA(cudaFuncSetAttribute(k_warm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
-  OSM_CUDA(cudaFuncSetAttribute(k_resid<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
-  done = true;
 }
 
 template <int V>
@@ -1169,25 +839,16 @@ static MfArg<V> mf_arg(const Ctx& c) {
   if constexpr (V == 5) {
     if (c.h_mf_const) a.c = *c.h_mf_const;
   }
-  if constexpr (V == 8) {
-    if (c.h_mf_win_const) a.c = *c.h_mf_win_const;
-  }
   if constexpr (V == 6 || V == 7)
     std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.dict);
   if constexpr (V == 10)
     std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(256, c.h_vi_dict.size()), a.dict);
-  if constexpr (V == 9) {
-    if (c.h_dia) a.c = *c.h_dia;
-    std::copy(c.h_vi_dict.begin(), c.h_vi_dict.begin() + std::min<size_t>(kCDict, c.h_vi_dict.size()), a.c.dict);
-  }
   return a;
 }
 
 template <int V>
 static void warm_v(Ctx& c, double tol) {
-  const unsigned thr = V == 1 ? kBulkThreads : kThreads;
-  if constexpr (V == 8) smem_optin(k_warm<8>, spmv_smem(c));
-  k_warm<V><<<(unsigned)c.nblk_total, thr, spmv_smem(c), c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
+  k_warm<V><<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(sell_of(c), c.blk_sub, c.st, c.x, c.b, c.islot,
                                                                       c.lam_all, c.dinv, c.r, c.p, c.part,
                                                                       c.nblk_total, tol, c.d_nactive, mf_arg<V>(c));
 }
@@ -1195,17 +856,12 @@ static void warm_v(Ctx& c, double tol) {
 void launch_warm(Ctx& c, double tol, int) {
   timer_begin(c, T_WARM);
   switch (spmv_variant_of(c)) {
-    case 0: warm_v<0>(c, tol); break;
-    case 1: warm_v<1>(c, tol); break;
-    case 2: warm_v<2>(c, tol); break;
     case 3: warm_v<3>(c, tol); break;
     case 5: warm_v<5>(c, tol); break;
     case 6: warm_v<6>(c, tol); break;
     case 7: warm_v<7>(c, tol); break;
     case 10: warm_v<10>(c, tol); break;
-    case 8: warm_v<8>(c, tol); break;
-    case 9: warm_v<9>(c, tol); break;
-    default: warm_v<4>(c, tol); break;
+    default: warm_v<2>(c, tol); break;
   }
   OSM_CHECK_LAUNCH();
   ++c.launches;
@@ -1243,37 +899,19 @@ static void launch_pdl(const Ctx& c, void (*kern)(KArgs...), unsigned grid, unsi
 
 template <int V>
 static void cg_spmv_v(Ctx& c) {
-  if constexpr (V == 5 || V == 6) {
-    if (c.persist && c.d_tseq) {
-      const int g = c.grp_cur >= 0 ? c.grp_cur : 0;
-      const int nt = (int)grp_nblk(c);
-      const unsigned grid = (unsigned)std::min<int64_t>(nt, 8LL * c.nsm);
-      launch_pdl(c, k_cg_spmv_sm<V>, grid, kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub, c.st,
-                 (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c),
-                 (const int32_t*)(c.d_tseq + grp_blk0(c)), nt, c.nsm, c.d_sm_ctr + (int64_t)g * (c.nsm + 1));
-      return;
-    }
-  }
-  if constexpr (V == 8) smem_optin(k_cg_spmv<8>, spmv_smem(c));
-  launch_pdl(c, k_cg_spmv<V>, (unsigned)grp_nblk(c), V == 1 ? kBulkThreads : kThreads, (size_t)spmv_smem(c),
-             sell_of(c), (const int32_t*)c.blk_sub, c.st, (const double*)c.p, c.q,
-             c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c), grp_blk0(c));
+  launch_pdl(c, k_cg_spmv<V>, (unsigned)grp_nblk(c), kThreads, (size_t)0, sell_of(c), (const int32_t*)c.blk_sub, c.st,
+             (const double*)c.p, c.q, c.part, c.nblk_total, c.d_nactive, mf_arg<V>(c), grp_blk0(c));
 }
 
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
   switch (spmv_variant_of(c)) {
-    case 0: cg_spmv_v<0>(c); break;
-    case 1: cg_spmv_v<1>(c); break;
-    case 2: cg_spmv_v<2>(c); break;
     case 3: cg_spmv_v<3>(c); break;
     case 5: cg_spmv_v<5>(c); break;
     case 6: cg_spmv_v<6>(c); break;
     case 7: cg_spmv_v<7>(c); break;
     case 10: cg_spmv_v<10>(c); break;
-    case 8: cg_spmv_v<8>(c); break;
-    case 9: cg_spmv_v<9>(c); break;
-    default: cg_spmv_v<4>(c); break;
+    default: cg_spmv_v<2>(c); break;
   }
   ++c.launches;
   timer_end(c, T_SPMV);
@@ -1362,25 +1000,19 @@ void launch_glue(Ctx& c, int zero) {
 
 template <int V>
 static void resid_v(Ctx& c) {
-  if constexpr (V == 8) smem_optin(k_resid<8>, spmv_smem(c));
-  k_resid<V><<<(unsigned)c.nblk_total, V == 1 ? kBulkThreads : kThreads, spmv_smem(c), c.stream>>>(
+  k_resid<V><<<(unsigned)c.nblk_total, kThreads, 0, c.stream>>>(
       sell_of(c), c.blk_sub, c.st, c.ut, c.b, c.islot, c.wif_all, c.part, c.nblk_total, mf_arg<V>(c));
 }
 
 void launch_resid(Ctx& c) {
   timer_begin(c, T_RESID);
   switch (spmv_variant_of(c)) {
-    case 0: resid_v<0>(c); break;
-    case 1: resid_v<1>(c); break;
-    case 2: resid_v<2>(c); break;
     case 3: resid_v<3>(c); break;
     case 5: resid_v<5>(c); break;
     case 6: resid_v<6>(c); break;
     case 7: resid_v<7>(c); break;
     case 10: resid_v<10>(c); break;
-    case 8: resid_v<8>(c); break;
-    case 9: resid_v<9>(c); break;
-    default: resid_v<4>(c); break;
+    default: resid_v<2>(c); break;
   }
   OSM_CHECK_LAUNCH();
   ++c.launches;

@@ -104,6 +104,14 @@ __global__ void k_vi_kept(int64_t ntile, const int64_t* __restrict__ toff, const
   if (threadIdx.x == 0) vtw[t] = wmax;
 }
 
+// K^N values back at the Robin fold positions (the dictionary is built from the unfolded matrix).
+__global__ void k_vi_unfold(int64_t nfold, const int64_t* __restrict__ pos, const double* __restrict__ kn,
+                            double* __restrict__ val) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nfold || pos[e] < 0) return;
+  val[pos[e]] = kn[e];
+}
+
 __global__ void k_vi_fold_slots(int64_t nfold, const int64_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                 uint16_t* __restrict__ vidx) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -111,55 +119,7 @@ __global__ void k_vi_fold_slots(int64_t nfold, const int64_t* __restrict__ pos, 
   vidx[pos[e]] = (uint16_t)slot[e];
 }
 
-// Variant 9 copy: one thread per row of tile t.  The row's nonzero SELL entries (current, Robin-folded
-// values; exact zeros and padding skipped) are matched in order against the slots of its offset list
-// (code[row] = list id; real[] marks the non-padding slots); each matched slot takes the entry's
-// dictionary index, the others the index of 0.0.  An entry with no slot left sets *bad.
-__global__ void k_dia_pack(const int64_t* __restrict__ toff, const int32_t* __restrict__ twidth,
-                           const int32_t* __restrict__ col, const double* __restrict__ sval,
-                           const uint16_t* __restrict__ vidx, uint32_t zero_idx, const uint8_t* __restrict__ code,
-                           const int32_t* __restrict__ gbeg, const int32_t* __restrict__ delta,
-                           const uint8_t* __restrict__ real, const int64_t* __restrict__ doff,
-                           uint16_t* __restrict__ out, int32_t* __restrict__ bad) {
-  const int64_t t = blockIdx.x;
-  const int r = threadIdx.x;
-  const int64_t row = t * kRowsPerBlock + r;
-  const int tb = code[row];
-  if (tb == 0xff) return;
-  const int s0 = 4 * gbeg[tb], ns = 4 * (gbeg[tb + 1] - gbeg[tb]);
-  auto at = [&](int j) -> uint16_t& { return out[4 * (doff[t] + (int64_t)kRowsPerBlock * (j >> 2) + r) + (j & 3)]; };
-  for (int j = 0; j < ns; ++j) at(j) = (uint16_t)zero_idx;
-  const int w = twidth[t];
-  const int64_t base = toff[t] + r;
-  int j = 0;
-  for (int k = 0; k < w; ++k) {
-    const int64_t i = base + (int64_t)kRowsPerBlock * k;
-    if (sval[i] == 0.0) continue;
-    const int32_t d = col[i] - (int32_t)row;
-    while (j < ns && !(real[s0 + j] && delta[s0 + j] == d)) ++j;
-    if (j == ns) {
-      atomicAdd(bad, 1);
-      return;
-    }
-    at(j++) = vidx[i];
-  }
-}
-
 }  // namespace
-
-void launch_dia_pack(Ctx& c, const int32_t* d_gbeg, const int32_t* d_delta, const uint8_t* d_real, int32_t* d_bad) {
-  uint32_t zero_idx = 0;
-  {
-    std::vector<double> hd(c.vi_nbase);
-    OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * c.vi_nbase, cudaMemcpyDeviceToHost));
-    zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
-  }
-  k_dia_pack<<<(unsigned)c.nblk_total, kRowsPerBlock, 0, c.stream>>>(
-      c.sell_soff, c.sell_swidth, c.sell_col, c.sell_val, c.vi_idx, zero_idx, c.d_mf_code, d_gbeg, d_delta, d_real,
-      c.d_dia_off, reinterpret_cast<uint16_t*>(c.d_dia_idx), d_bad);
-  OSM_CHECK_LAUNCH();
-  ++c.launches;
-}
 
 // Variant 10 (3-byte entries): regroups the 4-entry packed words (dict index << 16 | uint16 offset) into
 // 8-entry groups split in an offset stream and an index stream; entry order within a row is kept,
@@ -254,10 +214,20 @@ void vi_build(Ctx& c, bool per_side) {
   vi_free(c);
   const int64_t n = c.sell_total;
   if (n == 0) return;
-  // 1. distinct K^N values
+  // 1. distinct K^N values, from the UNFOLDED matrix: c.sell_val holds K^N + p M + q S on the fold
+  // positions once a Robin term has been applied (a per-side rebuild from vi_apply_robin), and those
+  // folded values must not enter the base dictionary (the fold positions get tuple slots below)
+  double* unf = nullptr;
+  OSM_CUDA(cudaMalloc(&unf, sizeof(double) * n));
+  OSM_CUDA(cudaMemcpyAsync(unf, c.sell_val, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  if (c.nfold) {
+    k_vi_unfold<<<(unsigned)ceil_div(c.nfold, 256), 256, 0, c.stream>>>(c.nfold, c.fold_pos, c.fold_kn, unf);
+    OSM_CHECK_LAUNCH();
+    ++c.launches;
+  }
   double* tmp = nullptr;
   OSM_CUDA(cudaMalloc(&tmp, sizeof(double) * (n + 1)));
-  OSM_CUDA(cudaMemcpyAsync(tmp, c.sell_val, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  OSM_CUDA(cudaMemcpyAsync(tmp, unf, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   OSM_CUDA(cudaMemsetAsync(tmp + n, 0, sizeof(double), c.stream));  // 0.0 is always in the dictionary
   thrust::device_ptr<double> tp(tmp);
   thrust::sort(thrust::cuda::par.on(c.stream), tp, tp + n + 1);
@@ -286,6 +256,7 @@ void vi_build(Ctx& c, bool per_side) {
   const int64_t ndict = nd + (int64_t)tuples.size();
   if (ndict > 65536) {  // too many distinct values: stay on the fp64 SELL path
     cudaFree(tmp);
+    cudaFree(unf);
     return;
   }
   c.vi_fold_tuples.assign(tuples.size(), {});
@@ -308,7 +279,7 @@ void vi_build(Ctx& c, bool per_side) {
                              c.stream));
   // 3. indices (from the unfolded K^N SELL values), then fold positions -> tuple slots
   OSM_CUDA(cudaMalloc(&c.vi_idx, sizeof(uint16_t) * n));
-  k_vi_index<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(n, c.sell_val, tmp, (int)nd, c.vi_idx);
+  k_vi_index<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(n, unf, tmp, (int)nd, c.vi_idx);
   OSM_CHECK_LAUNCH();
   ++c.launches;
   if (c.nfold) {
@@ -332,6 +303,7 @@ void vi_build(Ctx& c, bool per_side) {
   OSM_CUDA(cudaStreamSynchronize(c.stream));
   OSM_CUDA(cudaMemsetAsync(c.d_flags + 2, 0, sizeof(int32_t), c.stream));
   cudaFree(tmp);
+  cudaFree(unf);
   const int32_t maxoff = flags[2];
   bool wide = false;
   if (maxoff > 32767) {
@@ -384,10 +356,8 @@ void vi_build(Ctx& c, bool per_side) {
   OSM_CHECK_LAUNCH();
   ++c.launches;
   OSM_CUDA(cudaStreamSynchronize(c.stream));
-  if (c.sort_key != 4) {  // row order 4 keeps the indices for the implicit-offset copy (variant 9)
-    cudaFree(c.vi_idx);
-    c.vi_idx = nullptr;
-  }
+  cudaFree(c.vi_idx);
+  c.vi_idx = nullptr;
   c.vi_words = words;
   c.vi_per_side = per_side;
   c.vi_wide = wide;

@@ -122,7 +122,7 @@ def test_c5_sampled_slab():
     p1, p2, q1, q2 = 2e-4, 5e-5, 700.0, 300.0
     o.set_robin2(p1, q1, p2, q2)
     o.assemble()
-    assert o.set_spmv_variant(4) == 4  # the value-indexed path applies at S = 64
+    assert o.set_spmv_variant(10) == 10  # the 3-byte value-indexed path applies at S = 64
     o.upload_density(drho)
     st, rep = o.solve(tol_outer=1e-8, max_outer=1)
     box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], 2)

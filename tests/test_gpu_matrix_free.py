@@ -50,14 +50,7 @@ def test_matrix_free_bitwise_equals_sell_and_meets_oracle(q):
     robin = _robin(10.0, q[0], 3.0, q[1], S - 1)
     mf = _solve(CFG, drho, robin, 5)
     ref = _solve(CFG, drho, robin, 2)
-    win = _solve(CFG, drho, robin, 8)  # x window staged in shared memory by bulk copies
-    dia = _solve(CFG, drho, robin, 9)  # value-indexed rows with implicit offsets
-    assert mf["active"] == 5 and ref["active"] == 2 and win["active"] == 8 and dia["active"] == 9
-    assert np.array_equal(win["h"], ref["h"]) and np.array_equal(win["h2"], ref["h2"])
-    assert np.array_equal(dia["h"], ref["h"]) and np.array_equal(dia["h2"], ref["h2"])
-    assert np.array_equal(dia["inner"], ref["inner"])
-    for a, b in zip(dia["u"], ref["u"]):
-        assert np.array_equal(a, b)
+    assert mf["active"] == 5 and ref["active"] == 2
     assert mf["st"] == ref["st"] == 0 and mf["st2"] == 0
     assert np.array_equal(mf["h"], ref["h"])
     assert np.array_equal(mf["inner"], ref["inner"])
@@ -93,7 +86,7 @@ def test_thin_slabs_fall_back_or_verify():
     drho = synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=29)
     robin = _robin(8.0, 0.0, 8.0, 0.0, cfg["nsub"] - 1)
     mf = _solve(cfg, drho, robin, 5)
-    assert mf["active"] in (2, 3, 4, 5, 6, 7) and mf["st"] == 0
+    assert mf["active"] in (2, 3, 5, 6, 7) and mf["st"] == 0
     prob, rep = oracle_run(cfg, drho, robin[0], robin[2])
     ok, d = history_ok(mf["h"], rep.h)
     assert ok and len(mf["h"]) == len(rep.h), d.max()
@@ -106,7 +99,7 @@ def test_matrix_free_c3_full_solve_bitwise():
     cfg = dict(synth.CONFIGS["C3"])
     drho = synth.density(cfg)
     hs = []
-    for v in (5, 2, 9):
+    for v in (5, 2):
         o = P.setup(cfg, drho, row_order=4, spmv=v)
         assert o.set_spmv_variant(v) == v
         st, rep = o.solve(tol_outer=1e-8, max_outer=100)
@@ -115,8 +108,6 @@ def test_matrix_free_c3_full_solve_bitwise():
         o.close()
     assert np.array_equal(hs[0][0], hs[1][0]) and np.array_equal(hs[0][1], hs[1][1])
     assert np.array_equal(hs[0][2], hs[1][2])
-    assert np.array_equal(hs[2][0], hs[1][0]) and np.array_equal(hs[2][1], hs[1][1])
-    assert np.array_equal(hs[2][2], hs[1][2])
     assert hs[0][0][-1] <= 1e-8
 
 
@@ -137,7 +128,7 @@ def test_matrix_free_more_layouts(case):
     import paper_2112_03851_b200 as P
 
     out = []
-    for v in (5, 2, 9):
+    for v in (5, 2):
         o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
         o.set_row_order(4)
         o.decompose(cfg["nsub"])
@@ -149,11 +140,9 @@ def test_matrix_free_more_layouts(case):
         st, rep = o.solve(tol_outer=1e-8, max_outer=400)
         out.append((active, st, o.history(), [o.local_solution(s) for s in range(cfg["nsub"])]))
         o.close()
-    (a5, st5, h5, u5), (a2, st2, h2, u2), (a9, st9, h9, u9) = out
-    assert a5 == 5 and a2 == 2 and a9 == 9 and st5 == st2 == st9 == 0
-    assert np.array_equal(h5, h2) and np.array_equal(h9, h2)
-    for a, b in zip(u9, u2):
-        assert np.array_equal(a, b)
+    (a5, st5, h5, u5), (a2, st2, h2, u2) = out
+    assert a5 == 5 and a2 == 2 and st5 == st2 == 0
+    assert np.array_equal(h5, h2)
     for a, b in zip(u5, u2):
         assert np.array_equal(a, b)
     if cfg["nsub"] > 1:

@@ -34,13 +34,32 @@ def _run(cmd):
     return r.stdout + r.stderr
 
 
+def gen_kuhn_slots(force: bool = False) -> str:
+    """Generated header kuhn_slots.h: the P2 Kuhn stencil slots per parity class, computed by the
+    library's own host geometry (csrc/gen_kuhn_slots.cpp + lattice.cpp) for the brick SpMV."""
+    out = os.path.join(OBJ, "kuhn_slots.h")
+    deps = [os.path.join(CSRC, f) for f in ("gen_kuhn_slots.cpp", "lattice.cpp", "lattice.h")]
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+        return out
+    exe = os.path.join(OBJ, "gen_kuhn_slots")
+    _run([os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-I", CSRC, "-I", INCLUDE, "-I", "/usr/local/cuda/include",
+          deps[0], deps[1], "-o", exe])
+    r = subprocess.run([exe], capture_output=True, text=True, check=True)
+    with open(out + ".tmp", "w") as f:
+        f.write(r.stdout)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     inc, lib = nccl_dirs()
     os.makedirs(OBJ, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
-    headers = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "osm.h")]
+    gen_kuhn_slots(force)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) +
+                  [f for f in glob.glob(os.path.join(CSRC, "*.cpp")) if not os.path.basename(f).startswith("gen_")])
+    headers = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "osm.h"), os.path.join(OBJ, "kuhn_slots.h")]
     newest_header = max(os.path.getmtime(h) for h in headers)
-    flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", inc,
+    flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", OBJ, "-I", inc,
              "--expt-relaxed-constexpr"] + ARCH
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]

@@ -1,6 +1,7 @@
 // Internal context of libosm: per-GPU subdomain store, interface sides and the
 // launchers of the device kernels (assemble.cu, schwarz_kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <nccl.h>
 
 #include <string>
@@ -152,6 +153,66 @@ struct SellDev {
   const int64_t* vi3_base;  //   per tile: first group slot
 };
 
+// ---- brick SpMV (variant 11, row order 6; brick.cu)
+// One lattice parity class of one local subdomain: class-local ranges (inclusive) and its dense array
+// (jj fastest, padded to nJp; then ii; then kk) at internal row row0 + base.
+struct BrickClass {
+  int32_t iilo, iihi, jjlo, jjhi, kklo, kkhi;
+  int32_t nIc, nJp, nKc;
+  int64_t base;
+};
+struct BrickSub {
+  BrickClass cls[8];
+  int64_t row0;              // first internal row of the subdomain
+  int64_t nrows;             // class-array rows (before the padding to 256)
+  int32_t I_lo, nI, nJ;      // contract geometry (lattice of a contract local index)
+  int32_t nbj, nbi, nbk;     // bricks along jj, ii, kk
+  int64_t brick0, nbrick;    // the subdomain's bricks (global brick index on this GPU)
+};
+struct BrickInfo {
+  int32_t ls;
+  int16_t bj, bi, bk, pad;
+};
+struct BrickDev {
+  BrickInfo* info = nullptr;
+  BrickSub* sub = nullptr;
+  uint32_t* stream = nullptr;    // u8 dictionary indices, 4 slots per word
+  CUtensorMap* tmap = nullptr;   // (local subdomain, class) TMA maps of p
+};
+constexpr int kBrickMaxGroups = 24;
+// Kernel parameter (constant bank): brick shape, per-class slot groups and shared-memory offsets of
+// the slots (relative to the point's own element), the dictionary.
+struct BrickArg {
+  int32_t BJ, BI, BK, npb;            // brick extents (class-local points) and points per class box
+  int32_t box_elems, box_stride, box_bytes;
+  int32_t stage_bytes;                // one stage of the persistent kernel: p boxes + index stream
+  int32_t dict_n;
+  int64_t brick_words;                // stream words per brick
+  int32_t ngrp[8], goff[8];           // slot groups per class, first group of the class in a brick
+  int32_t jsh[8];                     // class box column of jj = -1 (0 or 1: even TMA start)
+  int32_t wrange[9];                  // Kuhn kernel: warp w computes chunks [wrange[w], wrange[w+1])
+  int32_t soff[8 * 4 * kBrickMaxGroups];
+  double dict[256];
+};
+// Build-time view (brick.cu).
+struct BrickBuildDev {
+  int o;
+  int64_t nrows;
+  const int32_t* row_sub;  // internal row -> local subdomain (-1: none)
+  const int32_t* perm;     // internal row -> contract local (-1: pad / dummy)
+  const BrickSub* sub;
+  int32_t BJ, BI, BK, npb;
+  int64_t brick_words;
+  int32_t ngrp[8], goff[8];
+};
+__host__ __device__ inline void brick_lattice_of(const BrickSub& B, int32_t lc, int& I, int& J, int& K) {
+  I = B.I_lo + lc % B.nI;
+  const int32_t t = lc / B.nI;
+  J = 1 + t % B.nJ;
+  K = 1 + t / B.nJ;
+}
+__host__ __device__ inline int brick_class(int o, int I, int J, int K) { return (I % o) + o * ((J % o) + o * (K % o)); }
+
 // Per-subdomain device scalars of the batched PCG / Schwarz kernels.
 struct SubState {
   double rho;      // r.z
@@ -170,6 +231,8 @@ struct SubState {
   int32_t zero_rhs;
   uint32_t cnt;    // last-block counter
   int32_t xpend;   // the PCG stopped in this iteration's update: the direction kernel still owes x += alpha p
+  int64_t brick0;  // brick SpMV (variant 11): first brick and bricks of the subdomain
+  int64_t nbrick;
 };
 
 // Device view of one interface side (grid.y of the interface kernels).
@@ -340,7 +403,9 @@ struct Ctx {
   bool use_graph = true;
   bool force_remote = false;  // debug: every side goes through NCCL (peer = own rank), see osm_create
   int update_variant = 0;  // 0: k_cg_update at 96 regs, 1: capped for 8 blocks/SM
-  int sort_key = 3;  // SELL row order inside sigma windows: 0 length desc, 1 parity class, 2 class then length,
+  int sort_key = 3;  // 6: brick layout of the brick SpMV (variant 11): per subdomain, one dense array per
+                    // lattice parity class (brick.cu); else the SELL row order inside sigma windows:
+                    // 0 length desc, 1 parity class, 2 class then length,
                     // 3 class, length, then (K, I, J) with J fastest (default); 4: the matrix-free
                     // class-major lattice layout of MfSub (whole subdomain, dummy rows included)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
@@ -368,6 +433,15 @@ struct Ctx {
   bool dcode_on = true;           // OSM_DCODE=0 keeps the 8-byte D^{-1} stream
   uint8_t* d_dcode = nullptr;
   std::vector<double> h_dcode_tab;  // empty: codes not built (too many distinct values)
+
+  // brick SpMV (variant 11, row order 6; brick.cu)
+  bool brick_ok = false;
+  BrickDev brick;
+  BrickArg h_brick_arg{};
+  std::vector<BrickSub> h_brick_sub;
+  int64_t brick_total = 0;
+  int brick_kernel = 0;          // 4 / 9: the P2 Kuhn kernel with compile-time slots for that BI; 0 generic
+  double* part_brick = nullptr;  // one p.q partial per brick
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;
@@ -449,6 +523,10 @@ void gravity_z(Ctx& c, double z0, double* d_out);  // gravity.cu (uses c.phi)
 void vi_build(Ctx& c, bool per_side = false);
 void vi_free(Ctx& c);
 void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector<double>& q_side);
+void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx);  // brick.cu (row order 6)
+void brick_free(Ctx& c);
+void brick_geometry(const Ctx& c, int ls, BrickSub& B);
+void launch_cg_spmv_brick(Ctx& c, cudaStream_t s);
 int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)
 
 // timing helpers (osm.cu)

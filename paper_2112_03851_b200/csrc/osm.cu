@@ -102,6 +102,7 @@ static void drop_graph(Ctx& c) {
 
 static void free_assembly(Ctx& c) {
   drop_graph(c);
+  brick_free(c);
   batch_free(c);
   vi_free(c);
   for (auto& s : c.subs) {
@@ -450,10 +451,13 @@ static void assemble(Ctx& c) {
 
     // SELL-32-sigma: within windows of kSigma rows, sort rows by length (descending, stable)
     const bool mf_layout = c.sort_key == 4;
+    const bool brick_layout = c.sort_key == 6;
     const int64_t mf_nIs = (int64_t)o * (S.g.c1 - S.g.c0) + 1;
     const int64_t mf_hI = (mf_nIs + o - 1) / o, mf_hJ = (S.g.Ny + o - 1) / o, mf_hK = (S.g.Nz + o - 1) / o;
     const int64_t mf_rows = (int64_t)o * o * o * mf_hI * mf_hJ * mf_hK;
-    S.npad = round_up(mf_layout ? mf_rows : S.n, kRowsPerBlock);
+    BrickSub bsub;
+    if (brick_layout) brick_geometry(c, ls, bsub);
+    S.npad = round_up(mf_layout ? mf_rows : (brick_layout ? bsub.nrows : S.n), kRowsPerBlock);
     if (S.npad >= (int64_t)INT32_MAX) fail(OSM_ERR_INVALID_ARG, "subdomain too large for int32 local indices");
     h_len[ls] = len;
     S.row0 = row0;
@@ -490,7 +494,18 @@ static void assemble(Ctx& c) {
         iperm[lc] = (int32_t)li;
       }
     }
-    for (int64_t w0 = 0; w0 < (mf_layout ? 0 : S.n); w0 += sigma) {
+    if (brick_layout) {  // one dense array per parity class (brick.cu); J pad rows: perm -1
+      for (int64_t lc = 0; lc < S.n; ++lc) {
+        const int64_t I = S.g.I_lo + lc % S.g.nI, t = lc / S.g.nI, J = 1 + t % S.g.nJ, K = 1 + t / S.g.nJ;
+        const int cc = brick_class(o, (int)I, (int)J, (int)K);
+        const BrickClass& C = bsub.cls[cc];
+        const int64_t ii = I / o - S.g.I_lo / o, jj = J / o - 1 / o, kk = K / o - 1 / o;
+        const int64_t li = C.base + (jj - C.jjlo) + (int64_t)C.nJp * ((ii - C.iilo) + (int64_t)C.nIc * (kk - C.kklo));
+        perm[li] = (int32_t)lc;
+        iperm[lc] = (int32_t)li;
+      }
+    }
+    for (int64_t w0 = 0; w0 < (mf_layout || brick_layout ? 0 : S.n); w0 += sigma) {
       const int64_t w1 = std::min<int64_t>(S.n, w0 + sigma);
       idx.resize(w1 - w0);
       std::iota(idx.begin(), idx.end(), (int32_t)w0);
@@ -666,6 +681,10 @@ static void assemble(Ctx& c) {
     for (int j = 0; j < ls; ++j) v0 += ceil_div(c.subs[j].nblk, c.vec_tiles);
     hst[ls].vblk0 = v0;
     hst[ls].nvblk = (int32_t)ceil_div(c.subs[ls].nblk, c.vec_tiles);
+    if (c.brick_ok) {
+      hst[ls].brick0 = c.h_brick_sub[ls].brick0;
+      hst[ls].nbrick = c.h_brick_sub[ls].nbrick;
+    }
   }
   OSM_CUDA(cudaMemcpyAsync(c.st, hst.data(), sizeof(SubState) * nloc, cudaMemcpyHostToDevice, c.stream));
   // two subdomain groups for the two-stream PCG (halves of the local subdomains, in block order)
@@ -849,7 +868,10 @@ static void enqueue_group_chunk(Ctx& c, int g, double tol, int maxit) {
   c.launches += 3 * kCgChunk;
 }
 
-static bool group_streams(const Ctx& c) { return c.ngroups > 1 && !c.timing && c.use_graph; }
+// (the brick SpMV is one persistent launch over every local subdomain: no group streams)
+static bool group_streams(const Ctx& c) {
+  return c.ngroups > 1 && !c.timing && c.use_graph && spmv_variant_of(c) != 11;
+}
 
 static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
   if (group_streams(c)) {
@@ -1000,7 +1022,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
   c.traffic[7] = c.exch_bytes;
   const int nloc = c.s_end - c.s_begin;
   const int sv = spmv_variant_of(c);
-  const bool vi = sv == 3 || sv == 6 || sv == 7 || sv == 10, mf = sv == 5;
+  const bool vi = sv == 3 || sv == 6 || sv == 7 || sv == 10, mf = sv == 5, br = sv == 11;
   for (int ls = 0; ls < nloc; ++ls) {
     const Sub& S = c.subs[ls];
     int64_t its = 0;
@@ -1010,7 +1032,9 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     // (tables in the constant bank); vectors p, q 16 B/row
     const double kept = ls < (int)c.vi_kept.size() ? (double)c.vi_kept[ls] : (double)S.nnz;
     // (variant 5 reads a 1-byte table code per row)
+    // (variant 11: its u8 index stream, 1 byte per (class-box point, slot), padding included)
     const double mat = mf ? (c.d_mf_code ? (double)S.npad : 0.0)
+                     : br ? 4.0 * (double)c.h_brick_arg.brick_words * (double)c.h_brick_sub[ls].nbrick
                           : (vi ? (sv == 10 ? 3.0 : 4.0) * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent
@@ -1607,8 +1631,8 @@ osm_status osm_get_batch_local_solution(osm_ctx* h, int b, int s, double* u, int
 osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (v != 2 && v != 3 && v != 5 && v != 6 && v != 7 && v != 10)
-    fail(OSM_ERR_INVALID_ARG, "SpMV variant must be one of 2, 3, 5, 6, 7, 10");
+  if (v != 2 && v != 3 && v != 5 && v != 6 && v != 7 && v != 10 && v != 11)
+    fail(OSM_ERR_INVALID_ARG, "SpMV variant must be one of 2, 3, 5, 6, 7, 10, 11");
   c.spmv_variant = v;
   drop_graph(c);  // captured launches embed the old kernel
   if (active) *active = spmv_variant_of(c);
@@ -1619,7 +1643,7 @@ osm_status osm_set_spmv_variant(osm_ctx* h, int v, int* active) {
 osm_status osm_set_row_order(osm_ctx* h, int order) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);
-  if (order < 0 || order > 4) fail(OSM_ERR_INVALID_ARG, "row order must be 0..4");
+  if (order < 0 || order > 6 || order == 5) fail(OSM_ERR_INVALID_ARG, "row order must be 0..4 or 6");
   if (c.assembled) fail(OSM_ERR_STATE, "osm_set_row_order must precede osm_assemble");
   c.sort_key = order;
   return OSM_OK;

@@ -814,8 +814,10 @@ SellDev sell_of(const Ctx& c) {
 
 }  // namespace
 
-int spmv_variant_of(const Ctx& c) {
-  int v = c.spmv_variant;
+// The tile-kernel variant (SELL formats) for v; 11 (bricks) is not a tile format: its warm-start and
+// residual products use the best SELL format of the same layout.
+static int tile_variant_for(const Ctx& c, int v) {
+  if (v == 11) v = 10;
   if (v == 10) {  // 3-byte entries
     if (c.vi_ok && c.vi3_ok && c.vi_ndict <= 256) return 10;
     v = 6;
@@ -832,6 +834,13 @@ int spmv_variant_of(const Ctx& c) {
   if (v == 6) return c.vi_ndict <= kCDict ? 6 : 3;
   return 3;
 }
+
+int spmv_variant_of(const Ctx& c) {
+  if (c.spmv_variant == 11 && c.brick_ok) return 11;
+  return tile_variant_for(c, c.spmv_variant);
+}
+
+static int tile_variant_of(const Ctx& c) { return tile_variant_for(c, c.spmv_variant); }
 
 template <int V>
 static MfArg<V> mf_arg(const Ctx& c) {
@@ -855,7 +864,7 @@ static void warm_v(Ctx& c, double tol) {
 
 void launch_warm(Ctx& c, double tol, int) {
   timer_begin(c, T_WARM);
-  switch (spmv_variant_of(c)) {
+  switch (tile_variant_of(c)) {
     case 3: warm_v<3>(c, tol); break;
     case 5: warm_v<5>(c, tol); break;
     case 6: warm_v<6>(c, tol); break;
@@ -906,6 +915,7 @@ static void cg_spmv_v(Ctx& c) {
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
   switch (spmv_variant_of(c)) {
+    case 11: launch_cg_spmv_brick(c, launch_stream(c)); break;
     case 3: cg_spmv_v<3>(c); break;
     case 5: cg_spmv_v<5>(c); break;
     case 6: cg_spmv_v<6>(c); break;
@@ -1006,7 +1016,7 @@ static void resid_v(Ctx& c) {
 
 void launch_resid(Ctx& c) {
   timer_begin(c, T_RESID);
-  switch (spmv_variant_of(c)) {
+  switch (tile_variant_of(c)) {
     case 3: resid_v<3>(c); break;
     case 5: resid_v<5>(c); break;
     case 6: resid_v<6>(c); break;

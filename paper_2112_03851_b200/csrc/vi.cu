@@ -356,12 +356,13 @@ void vi_build(Ctx& c, bool per_side) {
   OSM_CHECK_LAUNCH();
   ++c.launches;
   OSM_CUDA(cudaStreamSynchronize(c.stream));
-  cudaFree(c.vi_idx);
-  c.vi_idx = nullptr;
   c.vi_words = words;
   c.vi_per_side = per_side;
   c.vi_wide = wide;
   c.vi_ok = true;
+  if (c.sort_key == 6) brick_build(c, c.vi_idx, zero_idx);  // the brick copy reads the per-entry indices
+  cudaFree(c.vi_idx);
+  c.vi_idx = nullptr;
   vi3_build(c, tw, zero_idx);
 }
 

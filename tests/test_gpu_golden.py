@@ -76,7 +76,7 @@ def _c3_osm(P, cfg, drho, row_order=None):
     return o
 
 
-@pytest.mark.parametrize("variant,row_order", [(10, None), (2, None), (7, 4), (5, 4)])
+@pytest.mark.parametrize("variant,row_order", [(10, None), (2, None), (7, 4), (5, 4), (11, 6)])
 def test_c3_full_solve_matches_oracle(c3_inputs, variant, row_order):
     """C3 to h <= 1e-8 (P:165 PCG eps, P:215 outer stop) in bench.py's launch configuration (variant
     10), with the fp64 SELL (2), and in row order 4 with the wide value-indexed entries (7: 12-bit

@@ -339,6 +339,21 @@ osm_status osm_cmaes_tell(osm_cmaes* es, const double* f);
 osm_status osm_cmaes_state(osm_cmaes* es, double* mean, double* sigma, double* cov, double* best_x, double* best_f,
                            int* generation);
 osm_status osm_cmaes_should_stop(osm_cmaes* es, int max_iter, double ftol, int* stop);
+/* Dimension n and population lambda of the handle (0 for NULL). */
+void osm_cmaes_dims(const osm_cmaes* es, int* n, int* lambda);
+
+/* [collective] CMA-ES over the batched-alpha solver (population
+ * lambda = 25 at P:95, stopping rule P:171): es must have n = 1 (x = log alpha, both sides) or n = 2
+ * (x = (log alpha_left, log alpha_right)), lambda <= 64, and was made by osm_cmaes_create.  Each
+ * generation g asks lambda candidates from the caller's standard normals z[g][lambda][n] (host), solves
+ * all of them in ONE batched solve (osm_solve_batch semantics: OO0, every interface the same pair,
+ * n_outer outer iterations, tol_inner 1e-10, warm start) and tells es the costs
+ * cost_b = (h_b(n_outer) / h_b(k0))^(1/(n_outer - k0)) (the empirical contraction, SURVEY 8(d) C4;
+ * 1 when a history is unusable).  costs[g][lambda] (host, may be NULL) receives them.  Stops after gens
+ * generations or when osm_cmaes_should_stop(es, max_iter, ftol) says so; *gens_done = generations run.
+ * INVALID_ARG on bad sizes; STATE without interfaces. */
+osm_status osm_cmaes_batch_optimize(osm_ctx* ctx, osm_cmaes* es, int gens, const double* z, int n_outer, int k0,
+                                    int max_iter, double ftol, double* costs, int* gens_done);
 
 #ifdef __cplusplus
 }

@@ -45,3 +45,33 @@ def gravity_z(box: Box, phi_full: np.ndarray, z0: float) -> np.ndarray:
             gradphi = nodal @ grads
             out[ci + box.nx * cj] = -gradphi[2]
     return out
+
+
+def direct_gz(box: Box, drho: np.ndarray, px, py, pz, nq: int = 3, G: float = fe.G_NEWTON) -> np.ndarray:
+    """Free-space vertical anomaly by direct integration ("Phi(x) = G int rho(x') / ||x - x'||
+    dx'"; SPEC.md:186-200 direct_integration_potential): g_z = -dPhi/dz = G sum_cells drho_c
+    int_cell (z - z') / |x - x'|^3 dx', each cell integrated with an nq^3-point Gauss rule (the same
+    cell-constant density the FE problem sees).  Probe points must lie outside the anomaly's cells."""
+    g, w = np.polynomial.legendre.leggauss(nq)
+    t, wt = 0.5 * (g + 1.0), 0.5 * w
+    h = box.h
+    ck, cj, ci = np.meshgrid(np.arange(box.nz), np.arange(box.ny), np.arange(box.nx), indexing="ij")
+    d = np.asarray(drho, dtype=np.float64).reshape(box.nz, box.ny, box.nx)
+    m = d != 0
+    ci, cj, ck, dv = ci[m], cj[m], ck[m], d[m]
+    px, py, pz = (np.atleast_1d(np.asarray(v, dtype=np.float64)) for v in (px, py, pz))
+    out = np.zeros(px.size)
+    vol = h[0] * h[1] * h[2]
+    for a in range(nq):
+        for b in range(nq):
+            for c in range(nq):
+                xs = (ci + t[a]) * h[0]
+                ys = (cj + t[b]) * h[1]
+                zs = (ck + t[c]) * h[2]
+                wq = wt[a] * wt[b] * wt[c] * vol * dv
+                dx = px[:, None] - xs[None, :]
+                dy = py[:, None] - ys[None, :]
+                dz = pz[:, None] - zs[None, :]
+                r3 = (dx * dx + dy * dy + dz * dz) ** 1.5
+                out += (wq[None, :] * dz / r3).sum(axis=1)
+    return G * out

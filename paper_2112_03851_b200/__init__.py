@@ -34,7 +34,8 @@ ABI_SYMBOLS = ["osm_abi_version", "osm_last_error", "osm_nccl_unique_id", "osm_c
                "osm_plan", "osm_set_robin2", "osm_get_interface_stiffness", "osm_rate_max", "osm_rate_curve",
                "osm_cmaes_create", "osm_cmaes_destroy", "osm_cmaes_ask", "osm_cmaes_tell", "osm_cmaes_state",
                "osm_cmaes_should_stop", "osm_gravity_z", "osm_set_spmv_variant", "osm_upload_load_vector", "osm_solve_batch2",
-               "osm_set_row_order", "osm_hub_create", "osm_hub_destroy"]
+               "osm_set_row_order", "osm_hub_create", "osm_hub_destroy", "osm_cmaes_dims",
+               "osm_cmaes_batch_optimize"]
 
 
 class MeshDesc(C.Structure):
@@ -119,6 +120,8 @@ _sigs = {
     "osm_set_row_order": (C.c_int, [_P, C.c_int]),
     "osm_gravity_z": (C.c_int, [_P, C.c_double, _pd, _pi64]),
     "osm_hub_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "osm_cmaes_dims": (None, [_P, _pint, _pint]),
+    "osm_cmaes_batch_optimize": (C.c_int, [_P, _P, C.c_int, _pd, C.c_int, C.c_int, C.c_int, C.c_double, _pd, _pint]),
     "osm_hub_destroy": (None, [_P]),
     "osm_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, _pint, _pint, C.POINTER(PlanSide), C.c_int, _pint]),
 }
@@ -199,6 +202,17 @@ class CMAES:
         _check(_lib.osm_cmaes_state(self._h, _ptr(m, C.c_double), C.byref(sig), _ptr(cov, C.c_double),
                                     _ptr(bx, C.c_double), C.byref(bf), C.byref(g)))
         return dict(mean=m, sigma=sig.value, C=cov, best_x=bx, best_f=bf.value, generation=g.value)
+
+    def optimize_batched(self, osm, z, n_outer=30, k0=5, max_iter=7200, ftol=5e-11):
+        """CMA-ES over the batched-alpha solver of `osm` (osm_cmaes_batch_optimize): z is a (gens, lambda, n)
+        array of standard normals; returns (costs [gens_done, lambda], gens_done)."""
+        z = np.ascontiguousarray(z, dtype=np.float64).reshape(-1, self.lam, self.n)
+        gens = z.shape[0]
+        costs = np.zeros((gens, self.lam))
+        done = C.c_int()
+        _check(_lib.osm_cmaes_batch_optimize(osm._h, self._h, gens, _ptr(z, C.c_double), n_outer, k0, max_iter,
+                                             float(ftol), _ptr(costs, C.c_double), C.byref(done)))
+        return costs[: done.value], done.value
 
     def should_stop(self, max_iter=7200, ftol=5e-11):
         st = C.c_int()

@@ -164,6 +164,11 @@ osm_status osm_cmaes_create(int n, int lambda, const double* mean, double sigma0
 
 void osm_cmaes_destroy(osm_cmaes* e) { delete e; }
 
+void osm_cmaes_dims(const osm_cmaes* es, int* n, int* lambda) {
+  if (n) *n = es ? es->n : 0;
+  if (lambda) *lambda = es ? es->lam : 0;
+}
+
 osm_status osm_cmaes_ask(osm_cmaes* e, const double* z, double* x) {
   API_BEGIN
   if (!e || !z || !x) fail(OSM_ERR_INVALID_ARG, "NULL argument");

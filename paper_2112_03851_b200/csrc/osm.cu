@@ -1593,6 +1593,63 @@ osm_status osm_solve_batch(osm_ctx* h, int B, const double* alphas, const osm_so
   OSM_API_END
 }
 
+osm_status osm_cmaes_batch_optimize(osm_ctx* h, osm_cmaes* es, int gens, const double* z, int n_outer, int k0,
+                                    int max_iter, double ftol, double* costs, int* gens_done) {
+  OSM_API_BEGIN
+  Ctx& c = ctx_of(h);
+  if (!es || !z || !gens_done) fail(OSM_ERR_INVALID_ARG, "NULL argument");
+  if (gens < 1 || k0 < 1 || n_outer <= k0) fail(OSM_ERR_INVALID_ARG, "need gens >= 1 and 1 <= k0 < n_outer");
+  if (c.nsub < 2) fail(OSM_ERR_STATE, "the alpha search needs at least one interface");
+  // dimension and population from the handle: 1 (symmetric log alpha) or 2 (log alpha_left, log alpha_right)
+  int n = 0, lam = 0;
+  osm_cmaes_dims(es, &n, &lam);
+  if (n < 1 || n > 2) fail(OSM_ERR_INVALID_ARG, "the alpha search has 1 or 2 variables");
+  if (lam > 64) fail(OSM_ERR_INVALID_ARG, "population > 64 (the batched solver's limit)");
+  const int ni = c.nsub - 1;
+  std::vector<double> x((size_t)lam * n), al((size_t)lam * 2 * ni), f(lam);
+  osm_solve_opts o{1e-300, n_outer, 1e-10, 20000, 1, 0};
+  osm_batch_report rep{};
+  *gens_done = 0;
+  for (int g = 0; g < gens; ++g) {
+    osm_status st = osm_cmaes_ask(es, z + (size_t)g * lam * n, x.data());
+    if (st != OSM_OK) return st;
+    for (int b = 0; b < lam; ++b) {
+      const double a_l = std::exp(x[(size_t)b * n]), a_r = std::exp(x[(size_t)b * n + n - 1]);
+      for (int i = 0; i < ni; ++i) {
+        al[((size_t)b * 2 + 0) * ni + i] = a_l;
+        al[((size_t)b * 2 + 1) * ni + i] = a_r;
+      }
+    }
+    std::vector<double> pq((size_t)lam * 4 * ni, 0.0);  // OO0: q = 0
+    for (int b = 0; b < lam; ++b)
+      for (int i = 0; i < ni; ++i) {
+        pq[(b * 4 + 0) * ni + i] = al[((size_t)b * 2 + 0) * ni + i];
+        pq[(b * 4 + 2) * ni + i] = al[((size_t)b * 2 + 1) * ni + i];
+      }
+    solve_batch(c, lam, pq.data(), o, &rep);
+    for (int b = 0; b < lam; ++b) {
+      // empirical contraction (DESIGN R6): (h(N) / h(k0))^(1 / (N - k0)); 1 if unusable
+      int nh = 0;
+      batch_history(c, b, nullptr, 0, &nh);
+      std::vector<double> hv(nh);
+      batch_history(c, b, hv.data(), nh, &nh);
+      double cost = 1.0;
+      if ((int)hv.size() >= n_outer && hv[k0 - 1] > 0 && std::isfinite(hv[n_outer - 1]))
+        cost = std::pow(hv[n_outer - 1] / hv[k0 - 1], 1.0 / (n_outer - k0));
+      f[b] = cost;
+      if (costs) costs[(size_t)g * lam + b] = cost;
+    }
+    st = osm_cmaes_tell(es, f.data());
+    if (st != OSM_OK) return st;
+    *gens_done = g + 1;
+    int stop = 0;
+    osm_cmaes_should_stop(es, max_iter, ftol, &stop);
+    if (stop) break;
+  }
+  return OSM_OK;
+  OSM_API_END
+}
+
 osm_status osm_solve_batch2(osm_ctx* h, int B, const double* pq, const osm_solve_opts* o, osm_batch_report* rep) {
   OSM_API_BEGIN
   Ctx& c = ctx_of(h);

@@ -177,3 +177,25 @@ def test_diverged_status_matches_oracle():
     ok, d = history_ok(o.history(), orep.h)
     assert ok, d.max()
     o.close()
+
+
+def test_gravity_anomaly_matches_newton_integral():
+    """NEXT-3 physical check on the GPU ("Phi(x) = G int rho(x') / ||x - x'||"):
+    osm_gravity_z of a 2-subdomain GPU solve above a compact ball anomaly in a doubled Dirichlet box
+    agrees with the free-space Newton integral of the same cell-constant density within 3 % (the
+    oracle pin test_oracle_gravity.py measures 1.4 % for the oracle's own FE solution)."""
+    import paper_2112_03851_b200 as P
+    import test_oracle_gravity as T
+
+    n, L = 24, 2.0
+    box, d, z0, j, ref = T.newton_case(n, L)
+    o = P.Osm(n, n, n, L, L, L, 2)
+    o.decompose(2)
+    o.set_robin([30.0], [30.0])
+    o.assemble()
+    o.upload_density(d)
+    st, rep = o.solve(tol_outer=1e-8, max_outer=1000)
+    assert st == 0
+    got = o.gravity_z(z0).reshape(n, n)[np.ix_(j, j)].ravel()
+    o.close()
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 0.03

@@ -170,3 +170,35 @@ def test_batch_is_independent_of_the_single_path_row_order():
         assert len(h3) == len(h4) and np.all(np.abs(h3 - h4) <= 1e-14 * h3)
         for a, b in zip(u3, u4):
             assert np.array_equal(a, b)
+
+
+def test_c4_size_batch_matches_oracle():
+    """C4 at its BASELINE size (configs[3]: 64 candidate alphas on the C2 problem, P2 32^3, 2 subdomains,
+    ball density; alpha_b = 56 exp(0.5 z_b), synth.alpha_candidates): one batched solve of 30 outer
+    iterations, and the sampled candidates' histories, inner counts and u_s(30) against the oracle's
+    (tests/golden/c4_b64.npz, written by tools/make_golden.py c4 from oracle/ alone)."""
+    import os
+
+    import paper_2112_03851_b200 as P
+
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "c4_b64.npz")))
+    cfg = dict(synth.CONFIGS["C2"])
+    al = synth.alpha_candidates(cfg["alpha"], B=64)
+    assert np.array_equal(al, g["alpha"])
+    N = int(g["N"])
+    o = P.setup(cfg, synth.density(cfg))
+    rep = o.solve_batch(al[:, None], al[:, None], tol_outer=1e-300, max_outer=N)
+    assert rep.B == 64
+    for b in g["sample"]:
+        h = o.batch_history(int(b))
+        ho = g[f"h_{b}"]
+        ok, d = history_ok(h, ho)
+        assert ok and len(h) == N, (b, d.max())
+        di = np.abs(o.batch_inner_iters(int(b)) - g[f"inner_{b}"])
+        assert di.max() <= 1 and (di > 0).mean() < 0.05, (b, di.max())
+        for s in range(cfg["nsub"]):
+            u = o.batch_local_solution(int(b), s)
+            nrm = float(g[f"unorm_{b}_{s}"])
+            assert abs(np.linalg.norm(u) - nrm) <= 1e-10 * nrm
+            assert np.linalg.norm(u[::31] - g[f"usamp_{b}_{s}"]) <= 1e-10 * np.linalg.norm(g[f"usamp_{b}_{s}"])
+    o.close()

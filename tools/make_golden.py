@@ -83,9 +83,53 @@ def run(name, cfg, K, nproc, checkpoint):
     print("wrote", path, json.dumps({k: meta[k] for k in ("outer_iters", "converged", "seconds")}))
 
 
+C4_SAMPLE = (0, 17, 42, 63)  # candidates of the B = 64 batch compared with the oracle
+
+
+def _c4_one(args):
+    b, alpha, N = args
+    from threadpoolctl import threadpool_limits
+
+    from oracle import schwarz
+
+    threadpool_limits(1)
+    cfg = dict(synth.CONFIGS["C2"])
+    box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
+    prob = schwarz.build_problem(box, cfg["nsub"], drho=synth.density(cfg))
+    A = schwarz.robin_operators(prob, [alpha], [alpha])
+    rep = schwarz.schwarz(prob, A, tol_outer=1e-300, max_outer=N, diverge_window=0)
+    return b, rep.h, rep.inner, [u.copy() for u in rep.u]
+
+
+def run_c4(N=30):
+    """C4 (BASELINE configs[3]): B = 64 candidates alpha_b = 56 exp(0.5 z_b) (synth.alpha_candidates) on
+    C2, both sides alpha_b; the oracle's first N outer iterations for the sampled candidates."""
+    import multiprocessing as mp
+
+    cfg = dict(synth.CONFIGS["C2"])
+    al = synth.alpha_candidates(cfg["alpha"], B=64)
+    t0 = time.time()
+    with mp.get_context("fork").Pool(len(C4_SAMPLE)) as pool:
+        res = pool.map(_c4_one, [(b, float(al[b]), N) for b in C4_SAMPLE])
+    out = {"sample": np.array(C4_SAMPLE), "alpha": al, "N": N}
+    for b, h, inner, u in res:
+        out[f"h_{b}"] = np.array(h)
+        out[f"inner_{b}"] = np.array(inner, dtype=np.int32)
+        for s, us in enumerate(u):  # u_s(N): its norm and every 31st entry (keeps the golden small)
+            out[f"unorm_{b}_{s}"] = float(np.linalg.norm(us))
+            out[f"usamp_{b}_{s}"] = us[::31]
+    path = os.path.join(GOLDEN, "c4_b64.npz")
+    np.savez_compressed(path, **out)
+    json.dump(dict(name="c4_b64", sample=list(C4_SAMPLE), N=N, seconds=time.time() - t0,
+                   written_by="tools/make_golden.py c4 (oracle.schwarz per sampled candidate; no CUDA path)",
+                   cite="BASELINE configs[3]; PAPER.md:60-72, P:95 (population); SURVEY 8(d) C4"),
+              open(os.path.join(GOLDEN, "c4_b64.json"), "w"), indent=1)
+    print("wrote", path, time.time() - t0)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c3", "c5s64", "c5s8"])
+    ap.add_argument("which", choices=["c3", "c5s64", "c5s8", "c4"])
     ap.add_argument("--K", type=int, default=None, help="outer iterations (default: to 1e-8)")
     ap.add_argument("--nproc", type=int, default=os.cpu_count())
     ap.add_argument("--checkpoint", default=None)
@@ -93,6 +137,8 @@ def main():
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     if a.which == "c3":
         run("c3_full", dict(synth.CONFIGS["C3"]), a.K, a.nproc, a.checkpoint)
+    elif a.which == "c4":
+        run_c4()
     else:
         cfg = dict(synth.CONFIGS["C5"])
         cfg["nsub"] = 64 if a.which == "c5s64" else 8

@@ -151,7 +151,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 
 constexpr int kBrickThreads = 256;
-constexpr int kBrickWarps = kBrickThreads / 32;
 constexpr int kMaxSlotGroups = 24;   // slot groups (4 slots) per class: P2 vertex rows need 14
 
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
@@ -224,9 +223,10 @@ __device__ __forceinline__ double chunk_dot(uint32_t xc, const uint32_t (&w)[16]
 // wait; the index stream is read from global memory, the next chunk's words in flight while a chunk
 // computes (the first chunk's before the wait: the stream is static).  Chunks (class c, il) go round
 // robin to the 8 warps.  BI_CT > 0: the P2 Kuhn kernel with compile-time slot offsets (brick_build
-// checked that every row fits them); BI_CT = 0: runtime slot tables.  (A persistent, double-buffered
-// form -- two CTAs per SM, the next brick's boxes loading during the current one's FMAs -- measured
-// slower: 80 against 61 us per C3 launch.)
+// checked that every row fits them); BI_CT = 0: runtime slot tables.  Measured alternatives (C3, one
+// launch over all bricks): a persistent double-buffered form (two CTAs per SM, the next
+// brick's boxes loading during the current one's FMAs) 80 us; 16 warps with one class per warp and
+// exact-count loads 75 us; this form 61 us.
 template <int NC, int BI_CT>
 __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
     const BrickDev D, const __grid_constant__ BrickArg a, SubState* __restrict__ st, double* __restrict__ q,
@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
   unsigned char* bsm = bsm_raw + ((128u - (smem_addr(bsm_raw) & 127u)) & 127u);
   const uint32_t xs_addr = smem_addr(bsm);
   uint64_t* bar = reinterpret_cast<uint64_t*>(bsm + NC * a.box_bytes);
-  __shared__ double red[kBrickWarps];
+  constexpr int NT = kBrickThreads, NW = NT / 32;
+  __shared__ double red[NW];
   __shared__ int flag;
   const int64_t b = blockIdx.x;
   const BrickInfo bi = D.info[b];  // static: before the dependency wait
@@ -316,12 +317,14 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
       pq = fma(lds_f64(xc), s, pq);
     }
   };
-  for (int ch = warp; ch < nch; ch += 2 * kBrickWarps) {
-    load_words(wb, ch + kBrickWarps);
-    compute(wa, ch);
-    if (ch + kBrickWarps >= nch) break;
-    load_words(wa, ch + 2 * kBrickWarps);
-    compute(wb, ch + kBrickWarps);
+  {
+    for (int ch = warp; ch < nch; ch += 2 * NW) {
+      load_words(wb, ch + NW);
+      compute(wa, ch);
+      if (ch + NW >= nch) break;
+      load_words(wa, ch + 2 * NW);
+      compute(wb, ch + NW);
+    }
   }
   // p.q: warp tree, warps in order, one partial per brick; the last brick of the subdomain sums them
   pq = warp_sum_b(pq);
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
   __syncthreads();
   if (threadIdx.x == 0) {
     double v = 0.0;
-    for (int w = 0; w < kBrickWarps; ++w) v += red[w];
+    for (int w = 0; w < NW; ++w) v += red[w];
     part[b] = v;
     __threadfence();
     flag = atomicAdd(&S.cnt, 1u) == (uint32_t)S.nbrick - 1;
@@ -338,14 +341,14 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
   if (!flag) return;
   __threadfence();
   double v = 0.0;  // fixed-order sum of the subdomain's brick partials: strided, then the block tree
-  for (int64_t m = threadIdx.x; m < S.nbrick; m += kBrickThreads) v += __ldcg(part + S.brick0 + m);
+  for (int64_t m = threadIdx.x; m < S.nbrick; m += NT) v += __ldcg(part + S.brick0 + m);
   v = warp_sum_b(v);
   __syncthreads();
   if (lane == 0) red[warp] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
     double pqs = 0.0;
-    for (int w = 0; w < kBrickWarps; ++w) pqs += red[w];
+    for (int w = 0; w < NW; ++w) pqs += red[w];
     S.cnt = 0;
     if (!(pqs > 0.0) || !isfinite(pqs)) {  // breakdown: p = 0 or loss of definiteness
       S.status = 3;
@@ -577,21 +580,6 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
     goff += A.BI * A.ngrp[cc];
   }
   A.brick_words = 32 * (int64_t)goff;
-  {  // warp chunk ranges (class-major chunk order) balanced by slot groups
-    std::vector<int> wgt;
-    for (int cc = 0; cc < nc; ++cc)
-      for (int il = 0; il < A.BI; ++il) wgt.push_back(A.ngrp[cc]);
-    int tot = 0;
-    for (int w : wgt) tot += w;
-    int acc = 0, ch = 0;
-    A.wrange[0] = 0;
-    for (int w = 1; w < 8; ++w) {
-      const int target = (int)((int64_t)tot * w / 8);
-      while (ch < (int)wgt.size() && acc + wgt[ch] / 2 < target) acc += wgt[ch++];
-      A.wrange[w] = ch;
-    }
-    A.wrange[8] = (int)wgt.size();
-  }
   // 3. brick map (subdomain-major, then kk, ii, jj bricks)
   int64_t nb = 0;
   for (int ls = 0; ls < nloc; ++ls) {

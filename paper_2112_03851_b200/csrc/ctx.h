@@ -190,7 +190,6 @@ struct BrickArg {
   int64_t brick_words;                // stream words per brick
   int32_t ngrp[8], goff[8];           // slot groups per class, first group of the class in a brick
   int32_t jsh[8];                     // class box column of jj = -1 (0 or 1: even TMA start)
-  int32_t wrange[9];                  // Kuhn kernel: warp w computes chunks [wrange[w], wrange[w+1])
   int32_t soff[8 * 4 * kBrickMaxGroups];
   double dict[256];
 };

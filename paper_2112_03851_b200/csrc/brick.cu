@@ -230,7 +230,7 @@ __device__ __forceinline__ double chunk_dot(uint32_t xc, const uint32_t (&w)[16]
 template <int NC, int BI_CT>
 __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
     const BrickDev D, const __grid_constant__ BrickArg a, SubState* __restrict__ st, double* __restrict__ q,
-    double* __restrict__ part, int32_t* __restrict__ nactive) {
+    double* __restrict__ part, int32_t* __restrict__ nactive, int64_t b0) {
   extern __shared__ __align__(128) unsigned char bsm_raw[];
   // TMA destinations must be 128-byte aligned in the shared window; the dynamic segment follows the
   // static one, so align by hand (the launch adds 128 bytes)
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
   constexpr int NT = kBrickThreads, NW = NT / 32;
   __shared__ double red[NW];
   __shared__ int flag;
-  const int64_t b = blockIdx.x;
+  const int64_t b = b0 + blockIdx.x;
   const BrickInfo bi = D.info[b];  // static: before the dependency wait
   const BrickSub& B = D.sub[bi.ls];
   const int lane = threadIdx.x & 31;
@@ -682,10 +682,17 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
                  (long long)nb, A.BI, c.brick_kernel, smem, (long long)A.brick_words);
 }
 
-// One launch over the bricks of every local subdomain, one CTA per brick (the variant runs without
-// subdomain-group streams).
-void launch_cg_spmv_brick(Ctx& c, cudaStream_t s) {
-  const int64_t nb = c.brick_total;
+// One launch over the bricks of the local subdomains of group g (all of them for g < 0), one CTA per
+// brick; p.q partials are indexed by the global brick number.
+void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g) {
+  const int nloc = c.s_end - c.s_begin;
+  int s0 = 0, s1 = nloc;
+  if (g >= 0) {
+    s0 = g * nloc / c.ngroups;
+    s1 = (g + 1) * nloc / c.ngroups;
+  }
+  const int64_t b0 = c.h_brick_sub[s0].brick0;
+  const int64_t nb = (s1 < nloc ? c.h_brick_sub[s1].brick0 : c.brick_total) - b0;
   if (nb <= 0) return;
   const int nc = c.mesh.order * c.mesh.order * c.mesh.order;
   const size_t smem = (size_t)nc * c.h_brick_arg.box_bytes + 16 + 128;
@@ -703,7 +710,7 @@ void launch_cg_spmv_brick(Ctx& c, cudaStream_t s) {
   cfg.numAttrs = 1;
   auto go = [&](auto kern) {
     OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, (const BrickDev)c.brick, c.h_brick_arg, c.st, c.q, c.part_brick,
-                                c.d_nactive));
+                                c.d_nactive, b0));
   };
   if (nc != 8) go(k_cg_spmv_brick<1, 0>);
   else if (c.brick_kernel == 9) go(k_cg_spmv_brick<8, 9>);

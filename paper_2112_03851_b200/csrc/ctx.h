@@ -525,7 +525,7 @@ void vi_apply_robin(Ctx& c, const std::vector<double>& p_side, const std::vector
 void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx);  // brick.cu (row order 6)
 void brick_free(Ctx& c);
 void brick_geometry(const Ctx& c, int ls, BrickSub& B);
-void launch_cg_spmv_brick(Ctx& c, cudaStream_t s);
+void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g);
 int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)
 
 // timing helpers (osm.cu)

@@ -868,10 +868,7 @@ static void enqueue_group_chunk(Ctx& c, int g, double tol, int maxit) {
   c.launches += 3 * kCgChunk;
 }
 
-// (the brick SpMV is one persistent launch over every local subdomain: no group streams)
-static bool group_streams(const Ctx& c) {
-  return c.ngroups > 1 && !c.timing && c.use_graph && spmv_variant_of(c) != 11;
-}
+static bool group_streams(const Ctx& c) { return c.ngroups > 1 && !c.timing && c.use_graph; }
 
 static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
   if (group_streams(c)) {

@@ -915,7 +915,7 @@ static void cg_spmv_v(Ctx& c) {
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
   switch (spmv_variant_of(c)) {
-    case 11: launch_cg_spmv_brick(c, launch_stream(c)); break;
+    case 11: launch_cg_spmv_brick(c, launch_stream(c), c.grp_cur); break;
     case 3: cg_spmv_v<3>(c); break;
     case 5: cg_spmv_v<5>(c); break;
     case 6: cg_spmv_v<6>(c); break;

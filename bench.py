@@ -44,12 +44,13 @@ def hbm_peak():
 
 
 def ncu_traffic(kernel="k_cg_spmv"):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary (or None)."""
+    """dram bytes per launch of a kernel from the committed ncu --set full capture (or None), and the
+    capture it came from (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     d = json.load(open(p))
-    return d.get(kernel)
+    return d.get(kernel), d.get("_source")
 
 
 class ClockSampler(threading.Thread):
@@ -164,6 +165,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=200)
     ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (192^3, 56 M DOF) block")
+    ap.add_argument("--no-brick", action="store_true", help="skip the brick-SpMV (variant 11) block")
     ap.add_argument("--no-cpu-full", action="store_true", help="skip the oracle's measured time-to-tolerance")
     ap.add_argument("--timing-steps", type=int, default=1)
     args = ap.parse_args()
@@ -291,16 +293,16 @@ def main():
     peak, peak_src = hbm_peak()
     spmv_launches, spmv_ms = kt["cg_spmv"]
     achieved = traffic["spmv_bytes"] / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
-    tr = ncu_traffic()
+    tr, tr_src = ncu_traffic()
     per_launch_alg = traffic["spmv_bytes"] / max(1, spmv_launches)
     fp64_ach = tm2["spmv_bytes"] / (kt2["cg_spmv"][1] / 1e3) / 1e9 if kt2["cg_spmv"][1] > 0 else None
     roofline_fp64 = {"bound": "hbm", "kernel": "k_cg_spmv<2> (fp64 SELL-256)", "achieved": fp64_ach, "peak": peak,
                      "unit": "GB/s", "frac": fp64_ach / peak if fp64_ach else None,
-                     "traffic": (ncu_traffic("fp64_sell_variant2_k_cg_spmv_r01b")),
+                     "traffic": ncu_traffic("fp64_sell_variant2_k_cg_spmv_r01b")[0],
                      "us_per_launch": 1e3 * kt2["cg_spmv"][1] / max(1, kt2["cg_spmv"][0]), "variant": active}
     roofline = {"bound": "hbm", "kernel": f"k_cg_spmv<{default_variant}>", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None,
-                "traffic": tr, "peak_source": peak_src,
+                "traffic": tr, "traffic_source": tr_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_launch_alg,
                 "share_of_cg_time": spmv_ms / sum(kt[k][1] for k in ("cg_spmv", "cg_update", "cg_dir")),
                 "share_of_step": spmv_ms / ms_instr if ms_instr > 0 else None,
@@ -317,7 +319,7 @@ def main():
                 "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
                 "frac_vs_spec_8000": achieved / SPEC_HBM_GBS if achieved else None,
                 "dram_gbs_from_ncu_traffic": (tr / (1e-3 * spmv_ms / max(1, spmv_launches)) / 1e9
-                                              if tr and spmv_ms > 0 else None),
+                                              if tr and spmv_ms > 0 and default_variant == HOT_VARIANT else None),
                 "exchange": exchange_block(kt, tm, world),
                 "limiter": "latency of the dependent load chains (packed entry -> x gather -> FMA), not HBM, L2 or "
                            "the L1 pipes (ncu, variant 10: l1tex 63% of peak, issue 57%, dram 40%; "
@@ -338,6 +340,12 @@ def main():
     matrix_free = None
     if world == 1:
         matrix_free = run_matrix_free(P, args, cfg, d_drho, stream, peak, torch)
+
+    # the brick SpMV (variant 11, row order 6: TMA-staged lattice bricks + u8 index stream), timed the
+    # same way: an alternative implementation of the same CSR product, reported beside the default
+    brick = None
+    if world == 1 and not args.no_brick:
+        brick = run_alt_spmv(P, args, cfg, d_drho, stream, peak, torch, row_order=6, variant=11)
 
     # C4 (BASELINE configs[3]), reported alongside: one batched-alpha evaluation of a CMA-ES population
     # (lambda = 25) on the C2 problem, 30 outer iterations per candidate (the cost window)
@@ -395,7 +403,7 @@ def main():
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
             "roofline": roofline, "roofline_cg_step": cg_roofline, "roofline_fp64_sell": roofline_fp64,
-            "matrix_free": matrix_free, "batched_alpha": batched, "c5": c5,
+            "matrix_free": matrix_free, "brick_spmv": brick, "batched_alpha": batched, "c5": c5,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)
@@ -447,6 +455,52 @@ def run_batched_alpha(P, stream, torch, B=25, N=30, reps=2):
             "seconds": s, "candidate_outer_iters_per_s": B * N / s,
             "dof_cg_iter_per_s": rows / cfg["nsub"] * rep.inner_total / s,  # equal slabs: mean n_s x inner
             "inner_total": rep.inner_total}
+
+
+def run_alt_spmv(P, args, cfg, d_drho, stream, peak, torch, row_order, variant):
+    """Time an alternative SpMV (row order / variant) on the headline workload: K timed steps after W
+    warm-ups (CUDA events on the library stream), then one instrumented solve for the per-launch time
+    and the roofline in its own bytes (osm traffic model)."""
+    S = cfg["nsub"]
+    o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"], stream=stream.cuda_stream)
+    o.set_row_order(row_order)
+    o.decompose(S)
+    o.set_robin2(*synth.robin(cfg))
+    o.assemble()
+    active = o.set_spmv_variant(variant)
+
+    def step():
+        o.upload_density_device(d_drho.data_ptr())
+        return o.solve(tol_outer=1e-8, max_outer=1000)
+
+    for _ in range(args.warmup):
+        st, rep = step()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    work, outer = 0.0, 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st, rep = step()
+        work += local_cg_work(o, S, 0, 1)
+        outer += rep.outer_iters
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    o.set_kernel_timing(True)
+    step()
+    kt, tm = o.kernel_timing(), o.traffic_model()
+    o.set_kernel_timing(False)
+    o.close()
+    n, t = kt["cg_spmv"]
+    gbs = tm["spmv_bytes"] / (t / 1e3) / 1e9 if t > 0 else None
+    return {"variant": active, "row_order": row_order, "status": int(st), "value": work / (ms / 1e3), "unit": UNIT,
+            "time_to_tol_s": ms / args.steps / 1e3, "outer_iters": outer / args.steps,
+            "spmv_us_per_launch": 1e3 * t / max(1, n), "spmv_bytes_per_launch": tm["spmv_bytes"] / max(1, n),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak if gbs else None,
+                         "note": "bytes = the u8 index stream (1 B per brick point and stencil slot, padding "
+                                 "included) + p read + q write; limited by issue and latency (DESIGN.md 6)"},
+            "cg_kernels_us": {k: 1e3 * v[1] / max(1, v[0]) for k, v in kt.items()}}
 
 
 def run_matrix_free(P, args, cfg, d_drho, stream, peak, torch):

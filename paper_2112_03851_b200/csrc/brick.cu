@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <type_traits>
 #include <vector>
 
 #include "ctx.h"
@@ -219,15 +220,11 @@ __device__ __forceinline__ double chunk_dot(uint32_t xc, const uint32_t (&w)[16]
   return s;
 }
 
-// One CTA per brick (four share an SM): the p boxes of its classes arrive by TMA after the PDL
-// wait; the index stream is read from global memory, the next chunk's words in flight while a chunk
-// computes (the first chunk's before the wait: the stream is static).  Chunks (class c, il) go round
-// robin to the 8 warps.  BI_CT > 0: the P2 Kuhn kernel with compile-time slot offsets (brick_build
-// checked that every row fits them); BI_CT = 0: runtime slot tables.  Measured alternatives (C3, one
-// launch over all bricks): a persistent double-buffered form (two CTAs per SM, the next
-// brick's boxes loading during the current one's FMAs) 80 us; 16 warps with one class per warp and
-// exact-count loads 75 us; this form 61 us.
-template <int NC, int BI_CT>
+// Generic brick kernel (any order, slots not on the P2 Kuhn lists): one CTA per brick; the p boxes of
+// its classes arrive by TMA after the PDL wait; the index stream is read from global memory, the next
+// chunk's words in flight while a chunk computes.  Chunks (class c, il) go round robin to the 8 warps,
+// with runtime slot offsets and group counts.
+template <int NC>
 __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
     const BrickDev D, const __grid_constant__ BrickArg a, SubState* __restrict__ st, double* __restrict__ q,
     double* __restrict__ part, int32_t* __restrict__ nactive, int64_t b0) {
@@ -245,7 +242,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
   const BrickSub& B = D.sub[bi.ls];
   const int lane = threadIdx.x & 31;
   const int warp = __reduce_max_sync(0xffffffffu, (unsigned)(threadIdx.x >> 5));
-  const int BI = BI_CT > 0 ? BI_CT : a.BI;
+  const int BI = a.BI;
   const int nch = NC * BI;
   const uint32_t* ws = D.stream + b * a.brick_words + lane;
   uint32_t wa[16], wb[16];
@@ -259,10 +256,14 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
       if (g < ng) w[g] = __ldg(p + 32 * g);
   };
   load_words(wa, warp);
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // the box barrier is initialised (and the tensor maps prefetched) before the dependency wait, so
+  // that both overlap the previous kernel's tail
+  if (warp == 0) {
+    if (lane == 0) mbar_init(bar, 1);
+    if (lane < NC) asm volatile("prefetch.tensormap [%0];" ::"l"(D.tmap + bi.ls * NC + lane) : "memory");
   }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();  // barrier initialised
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   SubState& S = st[bi.ls];
@@ -270,21 +271,20 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
     if (threadIdx.x == 0 && b == S.brick0) S.xpend = 0;
     return;
   }
-  if (threadIdx.x == 0) {
-    const int j0 = bi.bj * 16 - 1, i0 = bi.bi * BI - 1, k0 = bi.bk * 2 - 1;
-    mbar_expect_tx(bar, (uint32_t)(NC * a.box_elems * 8));
-    double* xs = reinterpret_cast<double*>(bsm);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
+  // one lane of warp 0 per class issues its box (every class's stencil reaches into all 8 boxes, so
+  // one barrier covers them); lane 0 arms it before the loads
+  if (warp == 0) {
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(NC * a.box_elems * 8));
+    __syncwarp();
+    if (lane < NC) {
+      const int c = lane;
+      const int j0 = bi.bj * 16 - 1, i0 = bi.bi * BI - 1, k0 = bi.bk * 2 - 1;
       const BrickClass& C = B.cls[c];
-      const CUtensorMap* map = D.tmap + bi.ls * NC + c;
-      // maps in global memory (written by the host before the launch): acquire for the tensormap proxy
-      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(map) : "memory");
       // innermost TMA coordinates must be 16-byte aligned (even): the class box starts a.jsh[c] early
-      tma_load_3d(xs + c * a.box_stride, map, j0 - C.jjlo - a.jsh[c], i0 - C.iilo, k0 - C.kklo, bar);
+      tma_load_3d(reinterpret_cast<double*>(bsm) + c * a.box_stride, D.tmap + bi.ls * NC + c,
+                  j0 - C.jjlo - a.jsh[c], i0 - C.iilo, k0 - C.kklo, bar);
     }
   }
-  __syncthreads();  // barrier initialised
   // this lane's point in a class box (BJ = 16, BK = 2: lane = jl + 16 kl), box dims (20, BI + 2, 4)
   const int jl = lane & 15, kl = lane >> 4;
   const uint32_t lane_off = 8u * (uint32_t)((jl + 1) + 20 * (BI + 2) * (kl + 1));
@@ -294,21 +294,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
     const int c = ch / BI, il = ch - c * BI;
     const BrickClass& C = B.cls[c];
     const uint32_t xc = xs_addr + 8u * (uint32_t)(c * a.box_stride + a.jsh[c] + 20 * (il + 1)) + lane_off;
-    double s;
-    if constexpr (BI_CT > 0) {
-      switch (c) {
-        case 0: s = kuhn_chunk<0, BI_CT>(xc, w, a.dict); break;
-        case 1: s = kuhn_chunk<1, BI_CT>(xc, w, a.dict); break;
-        case 2: s = kuhn_chunk<2, BI_CT>(xc, w, a.dict); break;
-        case 3: s = kuhn_chunk<3, BI_CT>(xc, w, a.dict); break;
-        case 4: s = kuhn_chunk<4, BI_CT>(xc, w, a.dict); break;
-        case 5: s = kuhn_chunk<5, BI_CT>(xc, w, a.dict); break;
-        case 6: s = kuhn_chunk<6, BI_CT>(xc, w, a.dict); break;
-        default: s = kuhn_chunk<7, BI_CT>(xc, w, a.dict); break;
-      }
-    } else {
-      s = chunk_dot(xc, w, a.soff + c * 4 * kMaxSlotGroups, a.dict, a.ngrp[c]);
-    }
+    const double s = chunk_dot(xc, w, a.soff + c * 4 * kMaxSlotGroups, a.dict, a.ngrp[c]);
     const int jj = bi.bj * 16 + jl, ii = bi.bi * BI + il, kk = bi.bk * 2 + kl;
     if (jj >= C.jjlo && jj <= C.jjhi && ii >= C.iilo && ii <= C.iihi && kk >= C.kklo && kk <= C.kkhi) {
       const int64_t row =
@@ -360,6 +346,174 @@ __global__ void __launch_bounds__(kBrickThreads) k_cg_spmv_brick(
   }
 }
 
+// ---- the P2 Kuhn kernel: one warp per x plane il of the brick (BI warps), each warp running the 8
+// classes in a fixed compile-time sequence.  Every class is then a straight line of immediates: the
+// stream words of chunk (C, il) at a compile-time offset plus il times a constant, the slot offsets
+// as LDS immediates, the row of the result from per-class brick constants staged in shared memory.
+// Every warp does the same work (one chunk of each class: the 53 slot groups of the Kuhn stencil), so
+// the CTA has no load imbalance, and the next class's index words are two classes in flight.
+template <int C>
+constexpr int kuhn_ng() {
+  return (kKuhnSlotCount[C] + 3) / 4;
+}
+template <int C, int BI>
+constexpr int kuhn_goff() {
+  int g = 0;
+  for (int k = 0; k < C; ++k) g += BI * ((kKuhnSlotCount[k] + 3) / 4);
+  return g;
+}
+template <int C, int BI>
+__device__ __forceinline__ void kuhn_words(uint32_t (&w)[16], const uint32_t* ws, int il) {
+  constexpr int ng = kuhn_ng<C>();
+  const uint32_t* p = ws + 32 * (kuhn_goff<C, BI>() + il * ng);
+#pragma unroll
+  for (int g = 0; g < ng; ++g) w[g] = __ldg(p + 32 * g);
+}
+template <int C>
+using IC = std::integral_constant<int, C>;
+
+// Dynamic shared memory of k_cg_spmv_kuhn<BI>: the class boxes (128-byte aligned by hand) and the
+// mbarrier; the reduction slots are static
+constexpr int kuhn_smem_bytes(int BI) { return 8 * box_stride_of(BI) * 8 + 16 + 128; }
+template <int BI>
+__global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
+    const BrickDev D, const __grid_constant__ BrickArg a, SubState* __restrict__ st, double* __restrict__ q,
+    double* __restrict__ part, int32_t* __restrict__ nactive, int64_t b0) {
+  constexpr int NC = 8, NW = BI;
+  constexpr int kStride = box_stride_of(BI);
+  extern __shared__ __align__(128) unsigned char bsm_raw[];
+  unsigned char* bsm = bsm_raw + ((128u - (smem_addr(bsm_raw) & 127u)) & 127u);
+  const uint32_t xs_addr = smem_addr(bsm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bsm + NC * kStride * 8);
+  __shared__ double red[NW];
+  __shared__ int flag[1];
+  const int64_t b = b0 + blockIdx.x;
+  const BrickInfo bi = D.info[b];  // static: before the dependency wait
+  const BrickSub& B = D.sub[bi.ls];
+  const int lane = threadIdx.x & 31;
+  const int w = __reduce_max_sync(0xffffffffu, (unsigned)(threadIdx.x >> 5));  // = il
+  const uint32_t* ws = D.stream + b * a.brick_words + lane;
+  uint32_t W0[16], W1[16];
+  uint32_t W2[16];
+  kuhn_words<0, BI>(W0, ws, w);  // the stream is static: index words before the wait
+  kuhn_words<1, BI>(W1, ws, w);
+  const BrickEpi* E = D.epi + b * NC;
+  const int jl = lane & 15, kl = lane >> 4;
+  uint32_t vm = 0;  // bit C: this thread's point of class C is a row
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const uint2 r = __ldg(reinterpret_cast<const uint2*>(&E[c].jlo));
+    const int jlo = (int8_t)(r.x & 0xff), jhi = (int8_t)((r.x >> 8) & 0xff), ilo = (int8_t)((r.x >> 16) & 0xff),
+              ihi = (int8_t)(r.x >> 24), klo = (int8_t)(r.y & 0xff), khi = (int8_t)((r.y >> 8) & 0xff);
+    vm |= (uint32_t)(jl >= jlo && jl <= jhi && w >= ilo && w <= ihi && kl >= klo && kl <= khi) << c;
+  }
+  if (w == 0) {
+    if (lane == 0) mbar_init(bar, 1);
+    if (lane < NC) asm volatile("prefetch.tensormap [%0];" ::"l"(D.tmap + bi.ls * NC + lane) : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();  // barrier initialised
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  SubState& S = st[bi.ls];
+  if (!S.active) {  // the previous direction kernel has paid the stopped subdomain's x update
+    if (threadIdx.x == 0 && b == S.brick0) S.xpend = 0;
+    return;
+  }
+  if (w == 0) {
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(NC * a.box_elems * 8));
+    __syncwarp();
+    if (lane < NC) {
+      const int c = lane;
+      const BrickClass& C = B.cls[c];
+      tma_load_3d(reinterpret_cast<double*>(bsm) + c * kStride, D.tmap + bi.ls * NC + c,
+                  bi.bj * 16 - 1 - C.jjlo - jsh_of(c), bi.bi * BI - 1 - C.iilo, bi.bk * 2 - 1 - C.kklo, bar);
+    }
+  }
+  const uint32_t lane_off = 8u * (uint32_t)((jl + 1) + 20 * (BI + 2) * (kl + 1) + 20 * (w + 1));
+  mbar_wait_parity(bar, 0);
+  double pq = 0.0;
+  auto run = [&](auto cc, const uint32_t(&Wc)[16]) {
+    constexpr int C = decltype(cc)::value;
+    const uint32_t xc = xs_addr + 8u * (uint32_t)(C * kStride + jsh_of(C)) + lane_off;
+    const double s = kuhn_chunk<C, BI>(xc, Wc, a.dict);
+    if ((vm >> C) & 1u) {
+      const longlong2 e = __ldg(reinterpret_cast<const longlong2*>(E + C));  // qoff | nJp, nJI
+      const int nJp = (int)(e.y & 0xffffffff), nJI = (int)(e.y >> 32);
+      q[e.x + jl + (long long)nJp * w + (long long)nJI * kl] = s;
+      pq = fma(lds_f64(xc), s, pq);
+    }
+  };
+  kuhn_words<2, BI>(W2, ws, w);
+  run(IC<0>{}, W0);
+  kuhn_words<3, BI>(W0, ws, w);
+  run(IC<1>{}, W1);
+  kuhn_words<4, BI>(W1, ws, w);
+  run(IC<2>{}, W2);
+  kuhn_words<5, BI>(W2, ws, w);
+  run(IC<3>{}, W0);
+  kuhn_words<6, BI>(W0, ws, w);
+  run(IC<4>{}, W1);
+  kuhn_words<7, BI>(W1, ws, w);
+  run(IC<5>{}, W2);
+  run(IC<6>{}, W0);
+  run(IC<7>{}, W1);
+  // p.q: warp tree, warps in order, one partial per brick.  Warps 1.. hand their sums to warp 0 over a
+  // named barrier (bar.arrive: they exit at once); warp 0 publishes the partial, and in the last brick
+  // of the subdomain sums all of them in brick order (strided over its lanes, then the warp tree).
+  pq = warp_sum_b(pq);
+  if (lane == 0) red[w] = pq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int k = 0; k < NW; ++k) v += red[k];
+    part[b] = v;
+    __threadfence();
+    flag[0] = atomicAdd(&S.cnt, 1u) == (uint32_t)S.nbrick - 1;
+  }
+  __syncthreads();
+  if (!flag[0]) return;
+  __threadfence();
+  double v = 0.0;  // fixed-order sum of the subdomain's brick partials: strided, then the block tree
+  for (int64_t m = threadIdx.x; m < S.nbrick; m += 32 * NW) v += __ldcg(part + S.brick0 + m);
+  v = warp_sum_b(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    v = 0.0;
+    for (int k = 0; k < NW; ++k) v += red[k];
+    S.cnt = 0;
+    if (!(v > 0.0) || !isfinite(v)) {  // breakdown: p = 0 or loss of definiteness
+      S.status = 3;
+      S.active = 0;
+      atomicSub(nactive, 1);
+    } else {
+      S.alpha = S.rho / v;
+    }
+  }
+}
+
+// f(k_cg_spmv_kuhn<BI>) for a runtime BI in 1..12
+template <class F>
+void with_kuhn_kernel(int BI, F&& f) {
+  switch (BI) {
+    case 1: f(k_cg_spmv_kuhn<1>); break;
+    case 2: f(k_cg_spmv_kuhn<2>); break;
+    case 3: f(k_cg_spmv_kuhn<3>); break;
+    case 4: f(k_cg_spmv_kuhn<4>); break;
+    case 5: f(k_cg_spmv_kuhn<5>); break;
+    case 6: f(k_cg_spmv_kuhn<6>); break;
+    case 7: f(k_cg_spmv_kuhn<7>); break;
+    case 8: f(k_cg_spmv_kuhn<8>); break;
+    case 9: f(k_cg_spmv_kuhn<9>); break;
+    case 10: f(k_cg_spmv_kuhn<10>); break;
+    case 11: f(k_cg_spmv_kuhn<11>); break;
+    case 12: f(k_cg_spmv_kuhn<12>); break;
+    default: fail(OSM_ERR_STATE, "brick: no Kuhn kernel for this BI");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -376,6 +530,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 void brick_free(Ctx& c) {
   if (c.brick.info) cudaFree(c.brick.info);
+  if (c.brick.epi) cudaFree(c.brick.epi);
   if (c.brick.stream) cudaFree(c.brick.stream);
   if (c.brick.tmap) cudaFree(c.brick.tmap);
   if (c.brick.sub) cudaFree(c.brick.sub);
@@ -556,7 +711,7 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
   if (const char* e = std::getenv("OSM_BRICK_IMAX")) imax = std::max(1, std::atoi(e));  // tuning
   const int nchunk = (iext + imax - 1) / imax;
   A.BI = (iext + nchunk - 1) / nchunk;
-  c.brick_kernel = kuhn && (A.BI == 4 || A.BI == 9) ? A.BI : 0;  // instantiated compile-time shapes
+  c.brick_kernel = kuhn && A.BI >= 1 && A.BI <= 12 ? A.BI : 0;  // k_cg_spmv_kuhn<BI> instances
   A.npb = A.BJ * A.BI * A.BK;
   A.box_elems = (A.BJ + 4) * (A.BI + 2) * (A.BK + 2);
   A.box_stride = (int)round_up(A.box_elems, 16);  // 128-byte aligned class boxes
@@ -667,16 +822,47 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
   OSM_CUDA(cudaMemcpy(c.brick.tmap, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
   OSM_CUDA(cudaMalloc(&c.brick.info, sizeof(BrickInfo) * std::max<int64_t>(1, nb)));
   OSM_CUDA(cudaMemcpy(c.brick.info, info.data(), sizeof(BrickInfo) * nb, cudaMemcpyHostToDevice));
+  if (c.brick_kernel > 0) {  // per (brick, class) row constants of the Kuhn kernel
+    std::vector<BrickEpi> epi((size_t)nb * nc);
+    auto clamp8 = [](int v) { return (int8_t)std::max(-128, std::min(127, v)); };
+    for (int64_t bb = 0; bb < nb; ++bb) {
+      const BrickInfo& I = info[bb];
+      const BrickSub& B = subs[I.ls];
+      const int j0 = I.bj * A.BJ, i0 = I.bi * A.BI, k0 = I.bk * A.BK;
+      for (int cc = 0; cc < nc; ++cc) {
+        const BrickClass& C = B.cls[cc];
+        BrickEpi& e = epi[(size_t)bb * nc + cc];
+        e = BrickEpi{};
+        e.nJp = C.nJp;
+        e.nJI = C.nJp * C.nIc;
+        e.qoff = B.row0 + C.base + (j0 - C.jjlo) + (int64_t)C.nJp * ((i0 - C.iilo) + (int64_t)C.nIc * (k0 - C.kklo));
+        e.jlo = clamp8(C.jjlo - j0);
+        e.jhi = clamp8(C.jjhi - j0);
+        e.ilo = clamp8(C.iilo - i0);
+        e.ihi = clamp8(C.iihi - i0);
+        e.klo = clamp8(C.kklo - k0);
+        e.khi = clamp8(C.kkhi - k0);
+      }
+    }
+    OSM_CUDA(cudaMalloc(&c.brick.epi, sizeof(BrickEpi) * epi.size()));
+    OSM_CUDA(cudaMemcpy(c.brick.epi, epi.data(), sizeof(BrickEpi) * epi.size(), cudaMemcpyHostToDevice));
+  }
   c.brick.sub = d_sub;
   OSM_CUDA(cudaMalloc(&c.part_brick, sizeof(double) * std::max<int64_t>(1, nb)));
   c.brick_total = nb;
   c.h_brick_sub = subs;
   c.brick_ok = true;
   const int smem = nc * A.box_bytes + 16 + 128;
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<8, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (c.brick_kernel > 0) {
+    for (int cc = 0; cc < nc; ++cc)  // the Kuhn kernel's compile-time stream layout
+      if (A.ngrp[cc] != (kKuhnSlotCount[cc] + 3) / 4) fail(OSM_ERR_STATE, "brick: Kuhn slot groups");
+    const int ks = kuhn_smem_bytes(c.brick_kernel);
+    with_kuhn_kernel(c.brick_kernel, [&](auto kern) {
+      OSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ks));
+    });
+  }
   if (std::getenv("OSM_DEBUG"))
     std::fprintf(stderr, "osm: brick copy: %lld bricks, BI %d, kernel %d, %d B shared, %lld stream words/brick\n",
                  (long long)nb, A.BI, c.brick_kernel, smem, (long long)A.brick_words);
@@ -712,10 +898,15 @@ void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g) {
     OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, (const BrickDev)c.brick, c.h_brick_arg, c.st, c.q, c.part_brick,
                                 c.d_nactive, b0));
   };
-  if (nc != 8) go(k_cg_spmv_brick<1, 0>);
-  else if (c.brick_kernel == 9) go(k_cg_spmv_brick<8, 9>);
-  else if (c.brick_kernel == 4) go(k_cg_spmv_brick<8, 4>);
-  else go(k_cg_spmv_brick<8, 0>);
+  if (nc != 8) {
+    go(k_cg_spmv_brick<1>);
+  } else if (c.brick_kernel > 0) {
+    cfg.blockDim = dim3(32 * c.brick_kernel);
+    cfg.dynamicSmemBytes = kuhn_smem_bytes(c.brick_kernel);
+    with_kuhn_kernel(c.brick_kernel, go);
+  } else {
+    go(k_cg_spmv_brick<8>);
+  }
 }
 
 }  // namespace osm

@@ -173,8 +173,17 @@ struct BrickInfo {
   int32_t ls;
   int16_t bj, bi, bk, pad;
 };
+// Per (brick, class) constants of the Kuhn kernel: the row of point (jl, il, kl) is
+// qoff + jl + nJp il + nJI kl, a row for jl in [jlo, jhi], il in [ilo, ihi], kl in [klo, khi].
+struct alignas(16) BrickEpi {
+  int64_t qoff;
+  int32_t nJp, nJI;
+  int8_t jlo, jhi, ilo, ihi, klo, khi, pad0, pad1;
+  int64_t pad2;
+};
 struct BrickDev {
   BrickInfo* info = nullptr;
+  BrickEpi* epi = nullptr;       // [brick][8] (Kuhn kernel)
   BrickSub* sub = nullptr;
   uint32_t* stream = nullptr;    // u8 dictionary indices, 4 slots per word
   CUtensorMap* tmap = nullptr;   // (local subdomain, class) TMA maps of p

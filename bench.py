@@ -165,7 +165,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=200)
     ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (192^3, 56 M DOF) block")
-    ap.add_argument("--no-brick", action="store_true", help="skip the brick-SpMV (variant 11) block")
+    ap.add_argument("--no-alt-spmv", action="store_true",
+                    help="skip the block timing the 3-byte value-indexed SELL (variant 10, row order 3)")
     ap.add_argument("--no-cpu-full", action="store_true", help="skip the oracle's measured time-to-tolerance")
     ap.add_argument("--timing-steps", type=int, default=1)
     args = ap.parse_args()
@@ -300,8 +301,12 @@ def main():
                      "unit": "GB/s", "frac": fp64_ach / peak if fp64_ach else None,
                      "traffic": ncu_traffic("fp64_sell_variant2_k_cg_spmv_r01b")[0],
                      "us_per_launch": 1e3 * kt2["cg_spmv"][1] / max(1, kt2["cg_spmv"][0]), "variant": active}
-    roofline = {"bound": "hbm", "kernel": f"k_cg_spmv<{default_variant}>", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None,
+    brick = default_variant == 11
+    kname = f"k_cg_spmv_kuhn<{brick_bi(cfg)}>" if brick else f"k_cg_spmv<{default_variant}>"
+    if brick:
+        tr, tr_src = ncu_traffic("k_cg_spmv_kuhn")
+    roofline = {"bound": "hbm", "kernel": kname, "variant": default_variant, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak if achieved else None,
                 "traffic": tr, "traffic_source": tr_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_launch_alg,
                 "share_of_cg_time": spmv_ms / sum(kt[k][1] for k in ("cg_spmv", "cg_update", "cg_dir")),
@@ -311,19 +316,23 @@ def main():
                                    for k, b in (("cg_update", "update_bytes"), ("cg_dir", "dir_bytes"))},
                 "kernel_ms": {k: v[1] for k, v in kt.items()}, "kernel_launches": {k: v[0] for k, v in kt.items()},
                 "us_per_launch": 1e3 * spmv_ms / max(1, spmv_launches),
-                "format": ("value-indexed SELL-256, 3-byte entries: per 8 entries one 16-B load of int16 column "
+                "format": ("brick copy (row order 6): per (row, stencil slot) one u8 dictionary index, slots "
+                           "in column order, 16 x BI x 2-point bricks of each parity class; + 16 B per row (p "
+                           "read, q write); the p boxes are TMA-staged in shared memory (their halo re-reads "
+                           "come from L2 and are not counted); dictionary (<= 256 slots) in the constant bank"
+                           if brick else
+                           "value-indexed SELL-256, 3-byte entries: per 8 entries one 16-B load of int16 column "
                            "offsets and one 8-B load of u8 dictionary indices, + 16 B per row (p, q); dictionary "
                            "(<= 256 slots) in the constant bank (kernel parameter)" if default_variant == 10 else
-                           "value-indexed SELL-256: 4 B per stored entry (16-bit dictionary index + 16-bit column "
-                           "offset) + 16 B per row (p, q); dictionary in the constant bank (kernel parameter)"),
+                           "SELL-256 (variant %d) + 16 B per row (p, q)" % default_variant),
                 "csr_equivalent_gbs": traffic_csr / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None,
                 "frac_vs_spec_8000": achieved / SPEC_HBM_GBS if achieved else None,
                 "dram_gbs_from_ncu_traffic": (tr / (1e-3 * spmv_ms / max(1, spmv_launches)) / 1e9
                                               if tr and spmv_ms > 0 and default_variant == HOT_VARIANT else None),
                 "exchange": exchange_block(kt, tm, world),
-                "limiter": "latency of the dependent load chains (packed entry -> x gather -> FMA), not HBM, L2 or "
-                           "the L1 pipes (ncu, variant 10: l1tex 63% of peak, issue 57%, dram 40%; "
-                           "profiles/r01r_ncu_summary.md; DESIGN.md 'SM-affine persistent SpMV')"}
+                "limiter": ("instruction issue and latency at ~27 resident warps per SM (shared-memory loads, "
+                            "dictionary LDCs and the FMA chain per row), not HBM: DESIGN.md 'Brick SpMV'"
+                            if brick else "latency of the dependent load chains (packed entry -> x gather -> FMA)")}
 
     # Whole PCG hot loop against the HBM roofline: algorithmic bytes of the three CG kernels (SpMV in
     # its own format + update + direction) of one solve, over the timed step (everything included).
@@ -341,11 +350,11 @@ def main():
     if world == 1:
         matrix_free = run_matrix_free(P, args, cfg, d_drho, stream, peak, torch)
 
-    # the brick SpMV (variant 11, row order 6: TMA-staged lattice bricks + u8 index stream), timed the
-    # same way: an alternative implementation of the same CSR product, reported beside the default
-    brick = None
-    if world == 1 and not args.no_brick:
-        brick = run_alt_spmv(P, args, cfg, d_drho, stream, peak, torch, row_order=6, variant=11)
+    # the 3-byte value-indexed SELL (variant 10, row order 3: the round-1 default), timed the same way:
+    # the same CSR product in a row-wise SELL format, reported beside the default brick copy
+    sell = None
+    if world == 1 and not args.no_alt_spmv:
+        sell = run_alt_spmv(P, args, cfg, d_drho, stream, peak, torch, row_order=3, variant=10)
 
     # C4 (BASELINE configs[3]), reported alongside: one batched-alpha evaluation of a CMA-ES population
     # (lambda = 25) on the C2 problem, 30 outer iterations per candidate (the cost window)
@@ -403,7 +412,7 @@ def main():
             "time_to_tol_s": ms_step / 1e3, "outer_iters": outer / args.steps, "inner_total": inner / args.steps,
             "dof_outer_iter_per_s": cfg["dof"] * outer / (ms / 1e3), "setup_s": t_setup,
             "roofline": roofline, "roofline_cg_step": cg_roofline, "roofline_fp64_sell": roofline_fp64,
-            "matrix_free": matrix_free, "brick_spmv": brick, "batched_alpha": batched, "c5": c5,
+            "matrix_free": matrix_free, "sell_spmv": sell, "batched_alpha": batched, "c5": c5,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "status": int(st)}
     print(json.dumps(line), flush=True)
@@ -426,7 +435,7 @@ def exchange_block(kt, tm, world):
 
 
 _rows = {}
-HOT_VARIANT = 10  # library default SpMV: value-indexed SELL-256 with 3-byte entries (falls back to 6, 7 or 2)
+HOT_VARIANT = 11  # library default SpMV: the brick copy (row order 6; falls back to 10, 6, 7 or 2)
 SPEC_HBM_GBS = 8000.0  # B200 HBM3e specification (SURVEY 8(d) reports against both)
 
 
@@ -455,6 +464,16 @@ def run_batched_alpha(P, stream, torch, B=25, N=30, reps=2):
             "seconds": s, "candidate_outer_iters_per_s": B * N / s,
             "dof_cg_iter_per_s": rows / cfg["nsub"] * rep.inner_total / s,  # equal slabs: mean n_s x inner
             "inner_total": rep.inner_total}
+
+
+def brick_bi(cfg):
+    """x extent (class-local planes) of the brick kernel's bricks, as brick.cu's brick_build picks it:
+    the widest slab's class-local x extent (cells + 1 for P2 interface planes) in chunks of <= 12."""
+    S = cfg["nsub"]
+    cells = -(-cfg["nx"] // S)
+    iext = cells + 1 if cfg["order"] == 2 else cells
+    nchunk = -(-iext // 12)
+    return -(-iext // nchunk)
 
 
 def run_alt_spmv(P, args, cfg, d_drho, stream, peak, torch, row_order, variant):
@@ -498,8 +517,10 @@ def run_alt_spmv(P, args, cfg, d_drho, stream, peak, torch, row_order, variant):
             "spmv_us_per_launch": 1e3 * t / max(1, n), "spmv_bytes_per_launch": tm["spmv_bytes"] / max(1, n),
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
                          "frac": gbs / peak if gbs else None,
-                         "note": "bytes = the u8 index stream (1 B per brick point and stencil slot, padding "
-                                 "included) + p read + q write; limited by issue and latency (DESIGN.md 6)"},
+                         "note": ("bytes = the u8 index stream (1 B per brick point and stencil slot, padding "
+                                  "included) + p read + q write" if active == 11 else
+                                  "bytes = 3 B per kept entry (int16 offset + u8 index) + p read + q write"
+                                  if active == 10 else "bytes: osm traffic model of variant %d" % active)},
             "cg_kernels_us": {k: 1e3 * v[1] / max(1, v[0]) for k, v in kt.items()}}
 
 

@@ -280,34 +280,32 @@ typedef struct osm_plan_side {
 osm_status osm_plan(int64_t nx, int nsub, int nranks, int rank, int* s_begin, int* s_end, osm_plan_side* sides,
                     int cap, int* nsides);
 
-/* SpMV implementation of the PCG kernels (all give bitwise-identical iterations for a given row
- * order, up to the sign of exact zeros):
- * 0 fp64 SELL-256, LDG rows; 1 fp64 SELL-256, warp-specialized cp.async.bulk pipeline;
- * 2 fp64 SELL-256, LDG rows at 32 registers; 3 value-indexed (16-bit dictionary index + 16-bit
- * column offset); 4 = 3 with the dictionary in shared memory; 6 = 3 with the dictionary in the
- * constant bank as a kernel parameter (up to 2048 distinct values); 7 = 6 on wide
- * entries (12-bit index, 20-bit offset), selected automatically when offsets exceed int16;
- * 8 = 5 with each tile's x window staged in shared memory by bulk copies (experimental, slower);
- * 9 value-indexed rows with implicit column offsets (row order 4: each row stores one 16-bit
- * dictionary index per slot of its stencil's offset list, the offset lists and the dictionary are
- * kernel parameters; experimental, slower than 6 and 5; falls back to 6);
- * 5 matrix-free Kuhn
- * stencil (the K_s values are uniform per parity class and row kind on the
- * structured mesh, so a table of (row offset, value) per class replaces the matrix; needs row
- * order 4, see osm_set_row_order).  Variants 3/4/6 fall back to 2 when the matrix does not
- * admit the value-indexed copy (6 to 3 beyond 2048 values); 5 falls back to 4 without row order 4
- * or when a slab is too thin for the tables.  10 (default): 3-byte value-indexed entries (an
- * int16 offset stream and a u8 dictionary-index stream, 8 entries per group; needs <= 256 dictionary
- * slots and 16-bit offsets, else falls back to 6).  *active (may be NULL) receives the variant that
- * will actually run.  INVALID_ARG outside 0..10. */
+/* SpMV implementation of the PCG kernels (the local solves' sparse
+ * matrix-vector product).  Every variant stores the assembled K_s = K_s^N + p M_Gamma + q S_Gamma
+ * (values copied exactly, never recomputed) and forms each row's sum in the row's column order, so
+ * the variants of one row order give the same q; the p.q reduction order differs between the tile
+ * variants (per 256-row tile) and the brick variant (per brick):
+ *   2  fp64 SELL-256 (value + int32 column per entry);
+ *   3  value-indexed SELL: 16-bit dictionary index + 16-bit column offset per entry, dictionary
+ *      through L1;  6 = 3 with the dictionary in the constant bank (<= 2048 distinct values);
+ *   7  6 on wide entries (12-bit index, 20-bit offset), chosen automatically when offsets need it;
+ *   10 3-byte entries: an int16 offset stream and a u8 dictionary-index stream (<= 256 values);
+ *   11 (default) brick copy: needs row order 6; the p values of a lattice brick are staged in
+ *      shared memory by TMA and the matrix is a u8 dictionary-index stream, one byte per (row,
+ *      stencil slot) with the slots in column order (<= 256 values);
+ *   5  matrix-free Kuhn stencil: per-(class, row kind) tables built from
+ *      and verified against the assembled rows; needs row order 4.
+ * A variant whose format does not apply falls back: 11 -> 10 -> 6 -> 3 -> 2, 5 -> 6.  *active
+ * (may be NULL) receives the variant that will actually run.  INVALID_ARG for other values. */
 osm_status osm_set_spmv_variant(osm_ctx* ctx, int variant, int* active);
 
 /* Internal row order of the GPU copy (a permutation private to the library; results are
- * independent of it up to reduction order).  0 SELL rows by length in sigma windows; 1 by parity
- * class; 2 class then length; 3 class, length, then lattice (K, I, J) (default); 4 the class-major
- * lattice layout of the matrix-free variant: every lattice point of the slab box has a row, the
- * Dirichlet points being inert zero rows (+4..12 % rows).  Must precede osm_assemble (STATE after
- * it); INVALID_ARG outside 0..4. */
+ * independent of it up to reduction order).  6 (default): the brick layout of variant 11, per
+ * subdomain one dense array per lattice parity class (class-local jj fastest, then ii, then kk).
+ * 0 SELL rows by length in sigma windows; 1 by parity class; 2 class then length; 3 class,
+ * length, then lattice (K, I, J); 4 the class-major lattice layout of the matrix-free variant:
+ * every lattice point of the slab box has a row, the Dirichlet points being inert zero rows
+ * (+4..12 % rows).  Must precede osm_assemble (STATE after it); INVALID_ARG outside 0..4 and 6. */
 osm_status osm_set_row_order(osm_ctx* ctx, int order);
 
 /* Number of this library's kernel launches on the context's stream since

@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -152,6 +153,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 
 constexpr int kBrickThreads = 256;
+constexpr int kMaxDynSmem = 220 * 1024;  // dynamic shared memory budget of a brick CTA (sm_100 opt-in: 227 KB)
 constexpr int kMaxSlotGroups = 24;   // slot groups (4 slots) per class: P2 vertex rows need 14
 
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
@@ -853,15 +855,35 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
   c.h_brick_sub = subs;
   c.brick_ok = true;
   const int smem = nc * A.box_bytes + 16 + 128;
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  OSM_CUDA(cudaFuncSetAttribute(k_cg_spmv_brick<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  if (c.brick_kernel > 0) {
+  if (smem > kMaxDynSmem || kuhn_smem_bytes(12) > kMaxDynSmem)
+    fail(OSM_ERR_STATE, "brick: class boxes exceed the shared memory of an SM");
+  if (c.brick_kernel > 0)
     for (int cc = 0; cc < nc; ++cc)  // the Kuhn kernel's compile-time stream layout
       if (A.ngrp[cc] != (kKuhnSlotCount[cc] + 3) / 4) fail(OSM_ERR_STATE, "brick: Kuhn slot groups");
-    const int ks = kuhn_smem_bytes(c.brick_kernel);
-    with_kuhn_kernel(c.brick_kernel, [&](auto kern) {
-      OSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ks));
-    });
+  // the opt-in limit is a per-function, process-wide attribute: contexts of other shapes (other
+  // ranks of a hub, other problems) share it, so every brick kernel gets the SM maximum (the opt-in
+  // limit less its static shared memory) once, not a per-shape value
+  static std::mutex attr_mu;
+  static bool attr_done[64] = {};  // per device
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    int dev = 0;
+    OSM_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) fail(OSM_ERR_STATE, "brick: device ordinal out of range");
+    if (!attr_done[dev]) {
+      int optin = 0;
+      OSM_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      auto set_max = [&](auto kern) {
+        cudaFuncAttributes fa{};
+        OSM_CUDA(cudaFuncGetAttributes(&fa, kern));
+        OSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - (int)fa.sharedSizeBytes));
+      };
+      set_max(k_cg_spmv_brick<8>);
+      set_max(k_cg_spmv_brick<1>);
+      for (int bi = 1; bi <= 12; ++bi) with_kuhn_kernel(bi, set_max);
+      attr_done[dev] = true;
+    }
   }
   if (std::getenv("OSM_DEBUG"))
     std::fprintf(stderr, "osm: brick copy: %lld bricks, BI %d, kernel %d, %d B shared, %lld stream words/brick\n",

@@ -411,19 +411,21 @@ struct Ctx {
   bool use_graph = true;
   bool force_remote = false;  // debug: every side goes through NCCL (peer = own rank), see osm_create
   int update_variant = 0;  // 0: k_cg_update at 96 regs, 1: capped for 8 blocks/SM
-  int sort_key = 3;  // 6: brick layout of the brick SpMV (variant 11): per subdomain, one dense array per
-                    // lattice parity class (brick.cu); else the SELL row order inside sigma windows:
-                    // 0 length desc, 1 parity class, 2 class then length,
-                    // 3 class, length, then (K, I, J) with J fastest (default); 4: the matrix-free
+  int sort_key = 6;  // 6 (default): brick layout of the brick SpMV (variant 11): per subdomain, one dense
+                    // array per lattice parity class (brick.cu); else the SELL row order inside sigma
+                    // windows: 0 length desc, 1 parity class, 2 class then length,
+                    // 3 class, length, then (K, I, J) with J fastest; 4: the matrix-free
                     // class-major lattice layout of MfSub (whole subdomain, dummy rows included)
   int sigma = 0;  // SELL sorting window (rows); 0 = automatic (see assemble)
-  int spmv_variant = 10;  // SpMV variant (falls back when its format does not apply, spmv_variant_of):
+  int spmv_variant = 11;  // SpMV variant (falls back when its format does not apply, spmv_variant_of):
                           // 2: fp64 SELL rows (LDG streams, 32 registers, 8 blocks/SM);
                           // 3: value-indexed SELL (packed 16-bit index + offset, dictionary through L1);
                           // 5: matrix-free Kuhn stencil (row order 4 only; else as 6);
                           // 6: 3 with the dictionary in the constant bank; 7: 6 on wide entries (chosen
                           // automatically when offsets need 20 bits);
-                          // 10 (default): 6 with 3-byte entries (int16 offset + u8 index streams; <= 256 slots)
+                          // 10: 6 with 3-byte entries (int16 offset + u8 index streams; <= 256 slots);
+                          // 11 (default): brick copy (row order 6: TMA-staged p bricks, u8 index stream
+                          // per (row, stencil slot)); else as 10
 
   // matrix-free Kuhn-stencil tables (row order 4, SpMV variant 5; osm.cu mf_build)
   bool mf_ok = false;
@@ -452,7 +454,8 @@ struct Ctx {
   double* part_brick = nullptr;  // one p.q partial per brick
 
   // value-indexed SELL (vi.cu)
-  bool vi_ok = false;
+  bool vi_ok = false;         // dictionary and fold tuples built (the brick copy needs only these)
+  bool vi_packed_ok = false;  // the packed value-indexed SELL copy exists (variants 3/6/7)
   bool vi_per_side = false;  // fold slots per interface side (else per side kind)
   uint16_t* vi_idx = nullptr;
   bool vi_wide = false;  // entries (12-bit index << 20) | 20-bit offset (else 16 | 16)

@@ -819,7 +819,7 @@ SellDev sell_of(const Ctx& c) {
 static int tile_variant_for(const Ctx& c, int v) {
   if (v == 11) v = 10;
   if (v == 10) {  // 3-byte entries
-    if (c.vi_ok && c.vi3_ok && c.vi_ndict <= 256) return 10;
+    if (c.vi_packed_ok && c.vi3_ok && c.vi_ndict <= 256) return 10;
     v = 6;
   }
   if (v == 5) {
@@ -828,7 +828,7 @@ static int tile_variant_for(const Ctx& c, int v) {
   }
   if (v == 2) return 2;
   // value-indexed family
-  if (!c.vi_ok) return 2;
+  if (!c.vi_packed_ok) return 2;
   if (c.vi_wide) return c.vi_ndict <= kCDict ? 7 : 2;  // wide entries: constant-bank kernel only
   if (v == 7) v = 6;
   if (v == 6) return c.vi_ndict <= kCDict ? 6 : 3;

@@ -202,6 +202,7 @@ void vi_free(Ctx& c) {
   c.vi_packed = nullptr;
   c.vi_poff = nullptr;
   c.vi_ok = false;
+  c.vi_packed_ok = false;
   c.vi_wide = false;
   c.vi_fold_tuples.clear();
 }
@@ -306,17 +307,28 @@ void vi_build(Ctx& c, bool per_side) {
   cudaFree(unf);
   const int32_t maxoff = flags[2];
   bool wide = false;
+  // index of 0.0 in the sorted dictionary
+  std::vector<double> hd(nd);
+  OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * nd, cudaMemcpyDeviceToHost));
+  const uint32_t zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
   if (maxoff > 32767) {
-    if (maxoff > 524287 || ndict > 4096) {  // neither form fits: stay on the fp64 SELL path
+    if (maxoff > 524287 || ndict > 4096) {  // neither packed form fits
+      if (c.sort_key == 6 && ndict <= 256) {
+        // row order 6 (class arrays: a neighbour in another class is a class array away): no packed
+        // SELL copy, but the brick copy needs only the dictionary and the per-entry indices
+        c.vi_per_side = per_side;
+        c.vi_ok = true;
+        c.vi_packed_ok = false;
+        brick_build(c, c.vi_idx, zero_idx);
+        cudaFree(c.vi_idx);
+        c.vi_idx = nullptr;
+        return;
+      }
       vi_free(c);
       return;
     }
     wide = true;
   }
-  // index of 0.0 in the sorted dictionary
-  std::vector<double> hd(nd);
-  OSM_CUDA(cudaMemcpy(hd.data(), c.vi_dict, sizeof(double) * nd, cudaMemcpyDeviceToHost));
-  const uint32_t zero_idx = (uint32_t)(std::lower_bound(hd.begin(), hd.end(), 0.0) - hd.begin());
   // 5. packed copy (4 entries of a row per 16-byte load).  Entries whose value is exactly 0.0 -- the
   // Kuhn stencil's structural zeros (~19 % of P2 entries) and the SELL padding -- are
   // dropped: they add exact zeros (+-0) to the row sums, so the iterations stay the same.  Fold
@@ -360,6 +372,7 @@ void vi_build(Ctx& c, bool per_side) {
   c.vi_per_side = per_side;
   c.vi_wide = wide;
   c.vi_ok = true;
+  c.vi_packed_ok = true;
   if (c.sort_key == 6) brick_build(c, c.vi_idx, zero_idx);  // the brick copy reads the per-entry indices
   cudaFree(c.vi_idx);
   c.vi_idx = nullptr;

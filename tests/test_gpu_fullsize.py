@@ -108,8 +108,8 @@ def test_c2_converged_is_monolithic_solution(c2):
 
 
 def test_c5_sampled_slab():
-    """C5 (192^3 P2, 56.2 M DOF) with 64 subdomains in bench's launch configuration (value-indexed
-    SpMV, sigma 16384): bit-exact CSR pattern and values of interior slab 31 against the oracle's own
+    """C5 (192^3 P2, 56.2 M DOF) with 64 subdomains in bench's launch configuration (brick SpMV,
+    row order 6): bit-exact CSR pattern and values of interior slab 31 against the oracle's own
     assembly, and the first outer iteration's inner solve of that slab checked with the oracle's
     K_31: ||b_31 - K_31 u_31|| <= 1e-10 ||b_31|| (the PCG stopping test, evaluated independently)."""
     import paper_2112_03851_b200 as P
@@ -122,7 +122,7 @@ def test_c5_sampled_slab():
     p1, p2, q1, q2 = 2e-4, 5e-5, 700.0, 300.0
     o.set_robin2(p1, q1, p2, q2)
     o.assemble()
-    assert o.set_spmv_variant(10) == 10  # the 3-byte value-indexed path applies at S = 64
+    assert o.set_spmv_variant(11) == 11  # the brick path applies at S = 64 (BI = 4 Kuhn kernel)
     o.upload_density(drho)
     st, rep = o.solve(tol_outer=1e-8, max_outer=1)
     box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], 2)
@@ -141,7 +141,7 @@ def test_c5_sampled_slab():
 
 
 def test_c3_runs_the_default_spmv(c3):
-    """bench.py's C3 launch configuration runs SpMV variant 10 (3-byte value-indexed entries), not a
-    silent fallback to variant 6: the library reports 10 as the active variant."""
+    """bench.py's C3 launch configuration runs SpMV variant 11 (the brick copy), not a silent fallback
+    to a SELL variant: the library reports 11 as the active variant."""
     cfg, o, prob = c3
-    assert o.set_spmv_variant(10) == 10
+    assert o.set_spmv_variant(11) == 11

@@ -3,10 +3,11 @@ oracle alone (oracle.slabwise: the in-process oracle's iteration, distributed ov
 tests/test_oracle_slabwise.py pins it to oracle.schwarz).
 
 C3 (BASELINE configs[2]: P2 64^3 paper box, 8 subdomains, OO2) is solved to h <= 1e-8 in bench.py's
-exact launch configuration: SpMV variant 10 (3-byte value-indexed SELL), row order 3, 8 subdomain
-group streams, graph-replayed PDL chunks.  The same solve is repeated with the wide value-indexed
-entries (variant 7, the C5 S = 8 format) and with the matrix-free Kuhn stencil (variant 5, row order 4).
-C5 (192^3 P2, 56.2 M DOF, S = 64) is compared over the first K outer iterations of its golden.
+exact launch configuration: the library defaults (SpMV variant 11 = brick copy, row order 6), 8
+subdomain group streams, graph-replayed PDL chunks.  The same solve is repeated with the 3-byte
+value-indexed SELL (variant 10, row order 3), the fp64 SELL (2), the wide value-indexed entries (7)
+and the matrix-free Kuhn stencil (5, row order 4).  C5 (192^3 P2, 56.2 M DOF, S = 64) is compared over
+the first K outer iterations of its golden, in the default configuration.
 
 Bars (BASELINE north_star; DESIGN 3):
   * equal outer count N (+-1 only at a stopping tie |h_or(N) - tol| <= 1e-12 tol, Q24);
@@ -76,11 +77,12 @@ def _c3_osm(P, cfg, drho, row_order=None):
     return o
 
 
-@pytest.mark.parametrize("variant,row_order", [(10, None), (2, None), (7, 4), (5, 4), (11, 6)])
+@pytest.mark.parametrize("variant,row_order", [(11, None), (10, 3), (2, 3), (2, 6), (7, 4), (5, 4)])
 def test_c3_full_solve_matches_oracle(c3_inputs, variant, row_order):
-    """C3 to h <= 1e-8 (P:165 PCG eps, P:215 outer stop) in bench.py's launch configuration (variant
-    10), with the fp64 SELL (2), and in row order 4 with the wide value-indexed entries (7: 12-bit
-    index, 20-bit offset, the format C5 S = 8 needs) and the matrix-free stencil (5)."""
+    """C3 to h <= 1e-8 (P:165 PCG eps, P:215 outer stop) in bench.py's launch configuration (the
+    defaults: brick copy 11 in row order 6), with the 3-byte value-indexed SELL (10) and the fp64 SELL
+    (2) in row order 3, the fp64 SELL in the brick layout, and in row order 4 with the wide
+    value-indexed entries (7: 12-bit index, 20-bit offset) and the matrix-free stencil (5)."""
     import paper_2112_03851_b200 as P
 
     cfg, drho = c3_inputs

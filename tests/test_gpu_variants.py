@@ -19,7 +19,7 @@ CFG = dict(nx=8, ny=5, nz=4, lx=1.0, ly=0.7, lz=0.5, order=2, nsub=3)
 def _run(variant, drho, robin, dcode=1):
     import paper_2112_03851_b200 as P
 
-    env = {"OSM_SPMV": str(variant), "OSM_DCODE": str(dcode)}
+    env = {"OSM_SPMV": str(variant), "OSM_DCODE": str(dcode), "OSM_SORT": "3"}  # the SELL row order
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -65,7 +65,7 @@ def test_variants_bitwise_identical(robin):
 
 def test_value_indexed_nonuniform_interface_coefficients():
     """Different (p, q) per interface force per-side dictionary slots (vi_build from the UNFOLDED K^N
-    values, then per-side fold slots); every value-indexed variant -- including the default 10, whose
+    values, then per-side fold slots); every value-indexed variant -- including 10, whose
     3-byte copy is rebuilt -- still runs (no silent fallback) and is bitwise equal to fp64."""
     import paper_2112_03851_b200 as P
 
@@ -73,6 +73,7 @@ def test_value_indexed_nonuniform_interface_coefficients():
     hs = []
     for v in (2, 3, 6, 10):
         o = P.Osm(CFG["nx"], CFG["ny"], CFG["nz"], CFG["lx"], CFG["ly"], CFG["lz"], CFG["order"])
+        o.set_row_order(3)
         o.decompose(CFG["nsub"])
         o.set_robin2([10.0, 14.0], [0.05, 0.0], [3.0, 2.0], [0.2, 0.1])
         o.assemble()

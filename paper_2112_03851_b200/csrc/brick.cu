@@ -125,6 +125,52 @@ __global__ void k_brick_pack(const BrickBuildDev D, const int64_t* __restrict__ 
   }
 }
 
+// Row types of the Kuhn layout: one warp per chunk (brick, class, il).  The chunk is uniform when
+// every lane whose point is a row holds the same index words (lanes off the class range are never
+// stored); out: uni[chunk] and the words of the first row lane (words[chunk][0..ng)).
+__global__ void k_brick_chunks(const BrickBuildDev D, const BrickInfo* __restrict__ info,
+                               const uint32_t* __restrict__ stream, int BI, int64_t nchunk,
+                               uint32_t* __restrict__ words, int32_t* __restrict__ uni) {
+  const int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (ch >= nchunk) return;  // whole warps
+  const int64_t b = ch / (8 * BI);
+  const int r = (int)(ch % (8 * BI)), c = r / BI, il = r % BI;
+  const BrickInfo I = info[b];
+  const BrickClass& C = D.sub[I.ls].cls[c];
+  const int jj = I.bj * D.BJ + (lane & 15), ii = I.bi * BI + il, kk = I.bk * D.BK + (lane >> 4);
+  const bool valid = jj >= C.jjlo && jj <= C.jjhi && ii >= C.iilo && ii <= C.iihi && kk >= C.kklo && kk <= C.kkhi;
+  const int ng = D.ngrp[c];
+  const uint32_t* p = stream + b * D.brick_words + 32 * ((int64_t)D.goff[c] + (int64_t)il * ng) + lane;
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  const int src = vmask ? __ffs(vmask) - 1 : 0;
+  bool same = true;
+  for (int g = 0; g < ng; ++g) {
+    const uint32_t w = p[32 * g];
+    const uint32_t w0 = __shfl_sync(0xffffffffu, w, src);
+    same = same && (!valid || w == w0);
+    if (lane == 0) words[ch * 16 + g] = w0;
+  }
+  const bool all = __all_sync(0xffffffffu, same);
+  if (lane == 0) uni[ch] = all ? 1 : 0;
+}
+
+// Copies the per-lane words of the non-uniform chunks into the compact stream (one warp per chunk).
+__global__ void k_brick_compact(const BrickBuildDev D, const uint32_t* __restrict__ stream, int BI,
+                                const int64_t* __restrict__ src_chunk, const int64_t* __restrict__ dst_group,
+                                int64_t n, uint32_t* __restrict__ cstream) {
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= n) return;
+  const int64_t ch = src_chunk[k];
+  const int64_t b = ch / (8 * BI);
+  const int r = (int)(ch % (8 * BI)), c = r / BI, il = r % BI;
+  const int ng = D.ngrp[c];
+  const uint32_t* p = stream + b * D.brick_words + 32 * ((int64_t)D.goff[c] + (int64_t)il * ng) + lane;
+  uint32_t* q = cstream + 32 * dst_group[k] + lane;
+  for (int g = 0; g < ng; ++g) q[32 * g] = p[32 * g];
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n) : "memory");
 }
@@ -358,18 +404,15 @@ template <int C>
 constexpr int kuhn_ng() {
   return (kKuhnSlotCount[C] + 3) / 4;
 }
-template <int C, int BI>
-constexpr int kuhn_goff() {
-  int g = 0;
-  for (int k = 0; k < C; ++k) g += BI * ((kKuhnSlotCount[k] + 3) / 4);
-  return g;
-}
-template <int C, int BI>
-__device__ __forceinline__ void kuhn_words(uint32_t (&w)[16], const uint32_t* ws, int il) {
+// The index words of chunk (C, il): a row type's words (the same address in every lane: one
+// broadcast transaction) or the chunk's per-lane words in the compact stream.
+template <int C>
+__device__ __forceinline__ void kuhn_words(uint32_t (&w)[16], const BrickDev& D, int d, int lane) {
   constexpr int ng = kuhn_ng<C>();
-  const uint32_t* p = ws + 32 * (kuhn_goff<C, BI>() + il * ng);
+  const uint32_t* p = d >= 0 ? D.typetab + 16 * (int64_t)d : D.cstream + 32 * (int64_t)(-d - 1) + lane;
+  const int stride = d >= 0 ? 1 : 32;
 #pragma unroll
-  for (int g = 0; g < ng; ++g) w[g] = __ldg(p + 32 * g);
+  for (int g = 0; g < ng; ++g) w[g] = __ldg(p + g * stride);
 }
 template <int C>
 using IC = std::integral_constant<int, C>;
@@ -394,11 +437,13 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   const BrickSub& B = D.sub[bi.ls];
   const int lane = threadIdx.x & 31;
   const int w = __reduce_max_sync(0xffffffffu, (unsigned)(threadIdx.x >> 5));  // = il
-  const uint32_t* ws = D.stream + b * a.brick_words + lane;
+  // chunk descriptors of this warp's 8 chunks (C, il = w): lane C holds class C's
+  const int dreg = lane < NC ? __ldg(D.desc + (b * NC + lane) * BI + w) : 0;
+  auto dsc = [&](int C) { return __shfl_sync(0xffffffffu, dreg, C); };
   uint32_t W0[16], W1[16];
   uint32_t W2[16];
-  kuhn_words<0, BI>(W0, ws, w);  // the stream is static: index words before the wait
-  kuhn_words<1, BI>(W1, ws, w);
+  kuhn_words<0>(W0, D, dsc(0), lane);  // the stream is static: index words before the wait
+  kuhn_words<1>(W1, D, dsc(1), lane);
   const BrickEpi* E = D.epi + b * NC;
   const int jl = lane & 15, kl = lane >> 4;
   uint32_t vm = 0;  // bit C: this thread's point of class C is a row
@@ -446,17 +491,17 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
       pq = fma(lds_f64(xc), s, pq);
     }
   };
-  kuhn_words<2, BI>(W2, ws, w);
+  kuhn_words<2>(W2, D, dsc(2), lane);
   run(IC<0>{}, W0);
-  kuhn_words<3, BI>(W0, ws, w);
+  kuhn_words<3>(W0, D, dsc(3), lane);
   run(IC<1>{}, W1);
-  kuhn_words<4, BI>(W1, ws, w);
+  kuhn_words<4>(W1, D, dsc(4), lane);
   run(IC<2>{}, W2);
-  kuhn_words<5, BI>(W2, ws, w);
+  kuhn_words<5>(W2, D, dsc(5), lane);
   run(IC<3>{}, W0);
-  kuhn_words<6, BI>(W0, ws, w);
+  kuhn_words<6>(W0, D, dsc(6), lane);
   run(IC<4>{}, W1);
-  kuhn_words<7, BI>(W1, ws, w);
+  kuhn_words<7>(W1, D, dsc(7), lane);
   run(IC<5>{}, W2);
   run(IC<6>{}, W0);
   run(IC<7>{}, W1);
@@ -533,6 +578,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 void brick_free(Ctx& c) {
   if (c.brick.info) cudaFree(c.brick.info);
   if (c.brick.epi) cudaFree(c.brick.epi);
+  if (c.brick.desc) cudaFree(c.brick.desc);
+  if (c.brick.typetab) cudaFree(c.brick.typetab);
+  if (c.brick.cstream) cudaFree(c.brick.cstream);
+  c.brick_cwords = 0;
+  c.brick_ntypes = 0;
+  c.h_brick_sub_cwords.clear();
   if (c.brick.stream) cudaFree(c.brick.stream);
   if (c.brick.tmap) cudaFree(c.brick.tmap);
   if (c.brick.sub) cudaFree(c.brick.sub);
@@ -848,6 +899,82 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
     }
     OSM_CUDA(cudaMalloc(&c.brick.epi, sizeof(BrickEpi) * epi.size()));
     OSM_CUDA(cudaMemcpy(c.brick.epi, epi.data(), sizeof(BrickEpi) * epi.size(), cudaMemcpyHostToDevice));
+    // row types: chunks whose rows all carry the same index words are stored once (a type table),
+    // the others keep their per-lane words in a compact stream (interior chunks are uniform: the
+    // stencil of a parity class is translation invariant away from the Dirichlet faces and planes)
+    const int64_t nchunk = nb * nc * A.BI;
+    uint32_t* d_words = nullptr;
+    int32_t* d_uni = nullptr;
+    OSM_CUDA(cudaMalloc(&d_words, sizeof(uint32_t) * 16 * std::max<int64_t>(1, nchunk)));
+    OSM_CUDA(cudaMalloc(&d_uni, sizeof(int32_t) * std::max<int64_t>(1, nchunk)));
+    OSM_CUDA(cudaMemsetAsync(d_words, 0, sizeof(uint32_t) * 16 * std::max<int64_t>(1, nchunk), c.stream));
+    k_brick_chunks<<<(unsigned)ceil_div(nchunk * 32, 256), 256, 0, c.stream>>>(D, c.brick.info, c.brick.stream,
+                                                                             A.BI, nchunk, d_words, d_uni);
+    OSM_CHECK_LAUNCH();
+    ++c.launches;
+    std::vector<uint32_t> words((size_t)nchunk * 16);
+    std::vector<int32_t> uni((size_t)nchunk);
+    OSM_CUDA(cudaMemcpyAsync(words.data(), d_words, sizeof(uint32_t) * words.size(), cudaMemcpyDeviceToHost,
+                             c.stream));
+    OSM_CUDA(cudaMemcpyAsync(uni.data(), d_uni, sizeof(int32_t) * uni.size(), cudaMemcpyDeviceToHost, c.stream));
+    OSM_CUDA(cudaStreamSynchronize(c.stream));
+    cudaFree(d_words);
+    cudaFree(d_uni);
+    std::map<std::vector<uint32_t>, int32_t> types;  // key: class, then the class's ng words
+    std::vector<uint32_t> typetab;
+    std::vector<int32_t> desc((size_t)nchunk);
+    std::vector<int64_t> src_chunk, dst_group;
+    c.h_brick_sub_cwords.assign(nloc, 0);
+    int64_t groups = 0;
+    for (int64_t ch = 0; ch < nchunk; ++ch) {
+      const int cc = (int)((ch % (nc * A.BI)) / A.BI);
+      const int ng = A.ngrp[cc];
+      if (uni[ch]) {
+        std::vector<uint32_t> key(1 + ng);
+        key[0] = (uint32_t)cc;
+        std::copy(words.begin() + ch * 16, words.begin() + ch * 16 + ng, key.begin() + 1);
+        auto it = types.find(key);
+        if (it == types.end()) {
+          it = types.emplace(key, (int32_t)types.size()).first;
+          typetab.resize(typetab.size() + 16, 0u);
+          std::copy(key.begin() + 1, key.end(), typetab.end() - 16);
+        }
+        desc[ch] = it->second;
+      } else {
+        src_chunk.push_back(ch);
+        dst_group.push_back(groups);
+        desc[ch] = (int32_t)(-(groups + 1));
+        c.h_brick_sub_cwords[info[ch / (nc * A.BI)].ls] += 32 * (int64_t)ng;
+        groups += ng;
+        if (groups >= (int64_t)1 << 30) fail(OSM_ERR_STATE, "brick: compact stream too large");
+      }
+    }
+    OSM_CUDA(cudaMalloc(&c.brick.desc, sizeof(int32_t) * std::max<int64_t>(1, nchunk)));
+    OSM_CUDA(cudaMemcpy(c.brick.desc, desc.data(), sizeof(int32_t) * nchunk, cudaMemcpyHostToDevice));
+    OSM_CUDA(cudaMalloc(&c.brick.typetab, sizeof(uint32_t) * std::max<size_t>(16, typetab.size())));
+    if (!typetab.empty())
+      OSM_CUDA(cudaMemcpy(c.brick.typetab, typetab.data(), sizeof(uint32_t) * typetab.size(), cudaMemcpyHostToDevice));
+    OSM_CUDA(cudaMalloc(&c.brick.cstream, sizeof(uint32_t) * 32 * std::max<int64_t>(1, groups)));
+    if (!src_chunk.empty()) {
+      int64_t *d_src = nullptr, *d_dst = nullptr;
+      OSM_CUDA(cudaMalloc(&d_src, sizeof(int64_t) * src_chunk.size()));
+      OSM_CUDA(cudaMalloc(&d_dst, sizeof(int64_t) * dst_group.size()));
+      OSM_CUDA(cudaMemcpy(d_src, src_chunk.data(), sizeof(int64_t) * src_chunk.size(), cudaMemcpyHostToDevice));
+      OSM_CUDA(cudaMemcpy(d_dst, dst_group.data(), sizeof(int64_t) * dst_group.size(), cudaMemcpyHostToDevice));
+      const int64_t n = (int64_t)src_chunk.size();
+      k_brick_compact<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(D, c.brick.stream, A.BI, d_src, d_dst, n,
+                                                                           c.brick.cstream);
+      OSM_CHECK_LAUNCH();
+      ++c.launches;
+      OSM_CUDA(cudaStreamSynchronize(c.stream));
+      cudaFree(d_src);
+      cudaFree(d_dst);
+    }
+    c.brick_cwords = 32 * groups;
+    c.brick_ntypes = (int)types.size();
+
+    cudaFree(c.brick.stream);  // the Kuhn kernel reads the type table and the compact stream only
+    c.brick.stream = nullptr;
   }
   c.brick.sub = d_sub;
   OSM_CUDA(cudaMalloc(&c.part_brick, sizeof(double) * std::max<int64_t>(1, nb)));
@@ -886,8 +1013,11 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
     }
   }
   if (std::getenv("OSM_DEBUG"))
-    std::fprintf(stderr, "osm: brick copy: %lld bricks, BI %d, kernel %d, %d B shared, %lld stream words/brick\n",
-                 (long long)nb, A.BI, c.brick_kernel, smem, (long long)A.brick_words);
+    std::fprintf(stderr,
+                 "osm: brick copy: %lld bricks, BI %d, kernel %d, %d B shared, %lld stream words/brick, %d row "
+                 "types, compact stream %lld words (%.1f %% of the full one)\n",
+                 (long long)nb, A.BI, c.brick_kernel, smem, (long long)A.brick_words, c.brick_ntypes,
+                 (long long)c.brick_cwords, 100.0 * (double)c.brick_cwords / std::max(1.0, (double)nb * A.brick_words));
 }
 
 // One launch over the bricks of the local subdomains of group g (all of them for g < 0), one CTA per
@@ -925,7 +1055,10 @@ void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g) {
   } else if (c.brick_kernel > 0) {
     cfg.blockDim = dim3(32 * c.brick_kernel);
     cfg.dynamicSmemBytes = kuhn_smem_bytes(c.brick_kernel);
-    with_kuhn_kernel(c.brick_kernel, go);
+    with_kuhn_kernel(c.brick_kernel, [&](auto kern) {
+      OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, (const BrickDev)c.brick, c.h_brick_arg, c.st, c.q, c.part_brick,
+                                  c.d_nactive, b0));
+    });
   } else {
     go(k_cg_spmv_brick<8>);
   }

@@ -187,6 +187,12 @@ struct BrickDev {
   BrickSub* sub = nullptr;
   uint32_t* stream = nullptr;    // u8 dictionary indices, 4 slots per word
   CUtensorMap* tmap = nullptr;   // (local subdomain, class) TMA maps of p
+  // Kuhn kernel: chunk (brick, class, il) descriptors: >= 0 a row-type id (every row of the chunk
+  // has the same index words: typetab[id][0..ng)), < 0 -(g + 1) with the chunk's per-lane words at
+  // cstream[32 g + 32 k + lane], k < ng
+  int32_t* desc = nullptr;
+  uint32_t* typetab = nullptr;   // [ntypes][16]
+  uint32_t* cstream = nullptr;   // per-lane words of the non-uniform chunks
 };
 constexpr int kBrickMaxGroups = 24;
 // Kernel parameter (constant bank): brick shape, per-class slot groups and shared-memory offsets of
@@ -450,7 +456,10 @@ struct Ctx {
   BrickArg h_brick_arg{};
   std::vector<BrickSub> h_brick_sub;
   int64_t brick_total = 0;
-  int brick_kernel = 0;          // 4 / 9: the P2 Kuhn kernel with compile-time slots for that BI; 0 generic
+  int64_t brick_cwords = 0;     // words of the compact stream (non-uniform chunks)
+  std::vector<int64_t> h_brick_sub_cwords;  // per local subdomain
+  int brick_ntypes = 0;
+  int brick_kernel = 0;          // 1..12: the P2 Kuhn kernel k_cg_spmv_kuhn<BI>; 0: the generic brick kernel
   double* part_brick = nullptr;  // one p.q partial per brick
 
   // value-indexed SELL (vi.cu)

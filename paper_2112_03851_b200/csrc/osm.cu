@@ -1029,9 +1029,15 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     // (tables in the constant bank); vectors p, q 16 B/row
     const double kept = ls < (int)c.vi_kept.size() ? (double)c.vi_kept[ls] : (double)S.nnz;
     // (variant 5 reads a 1-byte table code per row)
-    // (variant 11: its u8 index stream, 1 byte per (class-box point, slot), padding included)
+    // (variant 11: its u8 index stream, 1 byte per (class-box point, slot), padding included; with
+    // the Kuhn kernel the per-lane words of the non-uniform chunks and one descriptor per chunk)
     const double mat = mf ? (c.d_mf_code ? (double)S.npad : 0.0)
-                     : br ? 4.0 * (double)c.h_brick_arg.brick_words * (double)c.h_brick_sub[ls].nbrick
+                     : br ? (c.brick_kernel > 0
+                                 // Kuhn kernel: compact per-lane words + one descriptor per chunk (the
+                                 // row-type table is a few KB, cached)
+                                 ? 4.0 * (double)c.h_brick_sub_cwords[ls] +
+                                       4.0 * 8.0 * c.h_brick_arg.BI * (double)c.h_brick_sub[ls].nbrick
+                                 : 4.0 * (double)c.h_brick_arg.brick_words * (double)c.h_brick_sub[ls].nbrick)
                           : (vi ? (sv == 10 ? 3.0 : 4.0) * kept : 12.0 * S.nnz + 4.0 * (S.n + 1));
     c.traffic[0] += (double)its * (mat + 16.0 * S.n);
     c.traffic[6] += (double)its * (12.0 * S.nnz + 4.0 * (S.n + 1) + 16.0 * S.n);  // CSR-equivalent

@@ -95,20 +95,22 @@ def test_c3_full_solve_matches_oracle(c3_inputs, variant, row_order):
     o.close()
 
 
-def test_c5_s64_first_outer_iterations():
-    """C5 (the >= 50 M-DOF target, BASELINE configs[4]) with S = 64 on one B200, default launch
-    configuration: the first K outer iterations against the oracle's (K from the golden)."""
+@pytest.mark.parametrize("S", [64, 8])
+def test_c5_first_outer_iterations(S):
+    """C5 (the >= 50 M-DOF target, BASELINE configs[4]) on one B200 in the default launch configuration,
+    with S = 64 and with S = 8 (bench.py's c5 block): the first K outer iterations
+    against the oracle's (K from the golden)."""
     import paper_2112_03851_b200 as P
 
-    names = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.startswith("c5s64_k") and f.endswith(".npz"))
+    names = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.startswith(f"c5s{S}_k") and f.endswith(".npz"))
     if not names:
         pytest.skip("C5 golden not generated")
     g = _golden(names[-1])
     K = len(g["h"])
     cfg = dict(synth.CONFIGS["C5"])
-    cfg["nsub"] = 64
+    cfg["nsub"] = S
     o = P.Osm(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], 2)
-    o.decompose(64)
+    o.decompose(S)
     o.set_robin2(*synth.robin(cfg))
     o.assemble()
     o.upload_density(synth.density(cfg))

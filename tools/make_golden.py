@@ -5,6 +5,7 @@ the seeded synthetic inputs of synth/ -- never the CUDA path.
     python tools/make_golden.py c3            # C3: full Schwarz solve to 1e-8, 8 workers
     python tools/make_golden.py c5s64 --K 3   # C5 (192^3 P2, S = 64): the first K outer iterations
     python tools/make_golden.py c5s64 --K 3 --checkpoint /tmp/c5ck   (resumable)
+    python tools/make_golden.py c5s8 --K 2 --max-asm 1 --checkpoint /tmp/c5s8ck   (C5 as bench.py runs it)
 
 Each golden (.npz) holds: h(1..N) and the inner PCG counts [N][S] of oracle.slabwise.schwarz_slabwise
 (bitwise the in-process oracle's iteration, tests/test_oracle_slabwise.py), ||Phi_N||_2 over the full
@@ -51,7 +52,7 @@ def projections(phi, k=4):
     return np.array([float(np.dot(rng.choice([-1.0, 1.0], size=phi.size), phi)) for _ in range(k)])
 
 
-def run(name, cfg, K, nproc, checkpoint):
+def run(name, cfg, K, nproc, checkpoint, max_asm=4):
     box = mesh.Box(cfg["nx"], cfg["ny"], cfg["nz"], cfg["lx"], cfg["ly"], cfg["lz"], cfg["order"])
     drho = synth.density(cfg)
     S = cfg["nsub"]
@@ -65,7 +66,7 @@ def run(name, cfg, K, nproc, checkpoint):
     rep = slabwise.schwarz_slabwise(box, S, drho, (pl, ql, pr, qr), tol_outer=tol,
                                     max_outer=1000 if K is None else K, tol_inner=1e-10, max_inner=20000,
                                     diverge_window=0 if K is not None else 10, nproc=nproc, want_phi=True,
-                                    checkpoint=checkpoint, log=log)
+                                    checkpoint=checkpoint, log=log, max_assemblies=max_asm)
     phi = rep.phi
     idx = sample_points(box, S)
     out = dict(h=np.array(rep.h), inner=np.array(rep.inner, dtype=np.int32), outer_iters=rep.outer_iters,
@@ -133,6 +134,7 @@ def main():
     ap.add_argument("--K", type=int, default=None, help="outer iterations (default: to 1e-8)")
     ap.add_argument("--nproc", type=int, default=os.cpu_count())
     ap.add_argument("--checkpoint", default=None)
+    ap.add_argument("--max-asm", type=int, default=4, help="slab assemblies at a time (C5 S = 8: 1, ~21 GB each)")
     a = ap.parse_args()
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     if a.which == "c3":
@@ -143,7 +145,7 @@ def main():
         cfg = dict(synth.CONFIGS["C5"])
         cfg["nsub"] = 64 if a.which == "c5s64" else 8
         cfg["robin"] = synth.C5_ROBIN
-        run(f"{a.which}_k{a.K}", cfg, a.K or 3, a.nproc, a.checkpoint)
+        run(f"{a.which}_k{a.K}", cfg, a.K or 3, a.nproc, a.checkpoint, a.max_asm)
 
 
 if __name__ == "__main__":

@@ -88,3 +88,21 @@ def test_brick_nonuniform_interface_coefficients():
     prob, rep = oracle_run(cfg, drho, robin[0], robin[2], q=(robin[1], robin[3]))
     ok, d = history_ok(h, rep.h)
     assert st == 0 and ok and len(h) == len(rep.h), d.max()
+
+
+@pytest.mark.parametrize("nx,S", [(2, 1), (3, 1), (5, 1), (8, 1), (11, 1), (12, 1), (13, 1), (19, 1), (26, 1),
+                                  (20, 2), (44, 2)])
+def test_brick_shapes_cover_every_kernel_instance(nx, S):
+    """The brick x extent BI follows the slab width (brick.cu: the class-local x extent in chunks of
+    <= 12): these widths reach BI = 2, 3, 5, 8, 11, 12 (one brick per slab) and 7, 10, 9 (two or three
+    bricks across the slab), so every compiled shape of the Kuhn kernel that a P2 slab can pick runs at
+    least once against the fp64 SELL in the same layout (and, with S = 2, the Robin planes)."""
+    cfg = dict(nx=nx, ny=5, nz=4, lx=1.0 * nx / 8, ly=0.6, lz=0.5, order=2, nsub=S)
+    drho = synth.random_field(cfg["nx"], cfg["ny"], cfg["nz"], seed=71 + nx)
+    robin = ([9.0] * (S - 1), [0.02] * (S - 1), [4.0] * (S - 1), [0.1] * (S - 1))
+    br = _solve(cfg, drho, robin, 11, 6)
+    ref = _solve(cfg, drho, robin, 2, 6)
+    assert br["active"] == 11 and ref["active"] == 2
+    assert br["st"] == ref["st"] == 0 and len(br["h"]) == len(ref["h"])
+    assert np.all(np.abs(br["h"] - ref["h"]) <= 1e-10 * ref["h"] + 1e-15)
+    assert rel_l2(br["phi"], ref["phi"]) <= 1e-12

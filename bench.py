@@ -332,7 +332,8 @@ def main():
                 "exchange": exchange_block(kt, tm, world),
                 "limiter": ("instruction issue and latency at ~27 resident warps per SM (shared-memory loads, "
                             "dictionary LDCs and the FMA chain per row), not HBM: DESIGN.md 'Brick SpMV'"
-                            if brick else "latency of the dependent load chains (packed entry -> x gather -> FMA)")}
+                            if brick else "latency of the dependent load chains (packed entry -> x gather -> FMA)"),
+                "limiter_metrics": ncu_traffic("k_cg_spmv_kuhn_pipes")[0] if brick else None}
 
     # Whole PCG hot loop against the HBM roofline: algorithmic bytes of the three CG kernels (SpMV in
     # its own format + update + direction) of one solve, over the timed step (everything included).

@@ -409,10 +409,15 @@ constexpr int kuhn_ng() {
 template <int C>
 __device__ __forceinline__ void kuhn_words(uint32_t (&w)[16], const BrickDev& D, int d, int lane) {
   constexpr int ng = kuhn_ng<C>();
-  const uint32_t* p = d >= 0 ? D.typetab + 16 * (int64_t)d : D.cstream + 32 * (int64_t)(-d - 1) + lane;
-  const int stride = d >= 0 ? 1 : 32;
+  if (d >= 0) {  // a row type: the same ng consecutive words in every lane (broadcast loads)
+    const uint32_t* p = D.typetab + 16 * (int64_t)d;
 #pragma unroll
-  for (int g = 0; g < ng; ++g) w[g] = __ldg(p + g * stride);
+    for (int g = 0; g < ng; ++g) w[g] = __ldg(p + g);
+  } else {  // per-lane words, lane-interleaved: immediate offsets
+    const uint32_t* p = D.cstream + 32 * (int64_t)(-d - 1) + lane;
+#pragma unroll
+    for (int g = 0; g < ng; ++g) w[g] = __ldg(p + 32 * g);
+  }
 }
 template <int C>
 using IC = std::integral_constant<int, C>;

@@ -442,23 +442,17 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   const BrickSub& B = D.sub[bi.ls];
   const int lane = threadIdx.x & 31;
   const int w = __reduce_max_sync(0xffffffffu, (unsigned)(threadIdx.x >> 5));  // = il
-  // chunk descriptors of this warp's 8 chunks (C, il = w): lane C holds class C's
-  const int dreg = lane < NC ? __ldg(D.desc + (b * NC + lane) * BI + w) : 0;
-  auto dsc = [&](int C) { return __shfl_sync(0xffffffffu, dreg, C); };
+  // the constants of this warp's 8 chunks (C, il = w): lane C holds class C's (desc, row mask, row
+  // offset, kk stride), broadcast by shuffles when the class runs
+  const int4 creg = lane < NC ? __ldg(reinterpret_cast<const int4*>(D.chunk) + (b * NC + lane) * BI + w)
+                              : make_int4(0, 0, 0, 0);
+  auto dsc = [&](int C) { return __shfl_sync(0xffffffffu, creg.x, C); };
   uint32_t W0[16], W1[16];
   uint32_t W2[16];
   kuhn_words<0>(W0, D, dsc(0), lane);  // the stream is static: index words before the wait
   kuhn_words<1>(W1, D, dsc(1), lane);
-  const BrickEpi* E = D.epi + b * NC;
   const int jl = lane & 15, kl = lane >> 4;
-  uint32_t vm = 0;  // bit C: this thread's point of class C is a row
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const uint2 r = __ldg(reinterpret_cast<const uint2*>(&E[c].jlo));
-    const int jlo = (int8_t)(r.x & 0xff), jhi = (int8_t)((r.x >> 8) & 0xff), ilo = (int8_t)((r.x >> 16) & 0xff),
-              ihi = (int8_t)(r.x >> 24), klo = (int8_t)(r.y & 0xff), khi = (int8_t)((r.y >> 8) & 0xff);
-    vm |= (uint32_t)(jl >= jlo && jl <= jhi && w >= ilo && w <= ihi && kl >= klo && kl <= khi) << c;
-  }
+  double* qs = q + B.row0;  // the subdomain's rows
   if (w == 0) {
     if (lane == 0) mbar_init(bar, 1);
     if (lane < NC) asm volatile("prefetch.tensormap [%0];" ::"l"(D.tmap + bi.ls * NC + lane) : "memory");
@@ -489,10 +483,10 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
     constexpr int C = decltype(cc)::value;
     const uint32_t xc = xs_addr + 8u * (uint32_t)(C * kStride + jsh_of(C)) + lane_off;
     const double s = kuhn_chunk<C, BI>(xc, Wc, a.dict);
-    if ((vm >> C) & 1u) {
-      const longlong2 e = __ldg(reinterpret_cast<const longlong2*>(E + C));  // qoff | nJp, nJI
-      const int nJp = (int)(e.y & 0xffffffff), nJI = (int)(e.y >> 32);
-      q[e.x + jl + (long long)nJp * w + (long long)nJI * kl] = s;
+    const uint32_t m = (uint32_t)__shfl_sync(0xffffffffu, creg.y, C);
+    const int ro = __shfl_sync(0xffffffffu, creg.z, C), nji = __shfl_sync(0xffffffffu, creg.w, C);
+    if ((m >> lane) & 1u) {
+      qs[ro + jl + nji * kl] = s;
       pq = fma(lds_f64(xc), s, pq);
     }
   };
@@ -582,8 +576,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 void brick_free(Ctx& c) {
   if (c.brick.info) cudaFree(c.brick.info);
-  if (c.brick.epi) cudaFree(c.brick.epi);
-  if (c.brick.desc) cudaFree(c.brick.desc);
+  if (c.brick.chunk) cudaFree(c.brick.chunk);
   if (c.brick.typetab) cudaFree(c.brick.typetab);
   if (c.brick.cstream) cudaFree(c.brick.cstream);
   c.brick_cwords = 0;
@@ -880,30 +873,31 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
   OSM_CUDA(cudaMemcpy(c.brick.tmap, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
   OSM_CUDA(cudaMalloc(&c.brick.info, sizeof(BrickInfo) * std::max<int64_t>(1, nb)));
   OSM_CUDA(cudaMemcpy(c.brick.info, info.data(), sizeof(BrickInfo) * nb, cudaMemcpyHostToDevice));
-  if (c.brick_kernel > 0) {  // per (brick, class) row constants of the Kuhn kernel
-    std::vector<BrickEpi> epi((size_t)nb * nc);
-    auto clamp8 = [](int v) { return (int8_t)std::max(-128, std::min(127, v)); };
+  if (c.brick_kernel > 0) {  // per (brick, class, il) chunk constants of the Kuhn kernel
+    std::vector<BrickChunk> chunks((size_t)nb * nc * A.BI);
     for (int64_t bb = 0; bb < nb; ++bb) {
       const BrickInfo& I = info[bb];
       const BrickSub& B = subs[I.ls];
       const int j0 = I.bj * A.BJ, i0 = I.bi * A.BI, k0 = I.bk * A.BK;
       for (int cc = 0; cc < nc; ++cc) {
         const BrickClass& C = B.cls[cc];
-        BrickEpi& e = epi[(size_t)bb * nc + cc];
-        e = BrickEpi{};
-        e.nJp = C.nJp;
-        e.nJI = C.nJp * C.nIc;
-        e.qoff = B.row0 + C.base + (j0 - C.jjlo) + (int64_t)C.nJp * ((i0 - C.iilo) + (int64_t)C.nIc * (k0 - C.kklo));
-        e.jlo = clamp8(C.jjlo - j0);
-        e.jhi = clamp8(C.jjhi - j0);
-        e.ilo = clamp8(C.iilo - i0);
-        e.ihi = clamp8(C.iihi - i0);
-        e.klo = clamp8(C.kklo - k0);
-        e.khi = clamp8(C.kkhi - k0);
+        for (int il = 0; il < A.BI; ++il) {
+          BrickChunk& e = chunks[((size_t)bb * nc + cc) * A.BI + il];
+          e = BrickChunk{};
+          const int64_t ro =
+              C.base + (j0 - C.jjlo) + (int64_t)C.nJp * ((i0 + il - C.iilo) + (int64_t)C.nIc * (k0 - C.kklo));
+          if (ro < INT32_MIN || ro > INT32_MAX || (int64_t)C.nJp * C.nIc > INT32_MAX)
+            fail(OSM_ERR_STATE, "brick: subdomain too large for 32-bit row offsets");
+          e.rowoff = (int32_t)ro;
+          e.nJI = C.nJp * C.nIc;
+          for (int lane = 0; lane < 32; ++lane) {
+            const int jj = j0 + (lane & 15), ii = i0 + il, kk = k0 + (lane >> 4);
+            if (jj >= C.jjlo && jj <= C.jjhi && ii >= C.iilo && ii <= C.iihi && kk >= C.kklo && kk <= C.kkhi)
+              e.mask |= 1u << lane;
+          }
+        }
       }
     }
-    OSM_CUDA(cudaMalloc(&c.brick.epi, sizeof(BrickEpi) * epi.size()));
-    OSM_CUDA(cudaMemcpy(c.brick.epi, epi.data(), sizeof(BrickEpi) * epi.size(), cudaMemcpyHostToDevice));
     // row types: chunks whose rows all carry the same index words are stored once (a type table),
     // the others keep their per-lane words in a compact stream (interior chunks are uniform: the
     // stencil of a parity class is translation invariant away from the Dirichlet faces and planes)
@@ -954,8 +948,9 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
         if (groups >= (int64_t)1 << 30) fail(OSM_ERR_STATE, "brick: compact stream too large");
       }
     }
-    OSM_CUDA(cudaMalloc(&c.brick.desc, sizeof(int32_t) * std::max<int64_t>(1, nchunk)));
-    OSM_CUDA(cudaMemcpy(c.brick.desc, desc.data(), sizeof(int32_t) * nchunk, cudaMemcpyHostToDevice));
+    for (int64_t ch = 0; ch < nchunk; ++ch) chunks[ch].desc = desc[ch];
+    OSM_CUDA(cudaMalloc(&c.brick.chunk, sizeof(BrickChunk) * std::max<int64_t>(1, nchunk)));
+    OSM_CUDA(cudaMemcpy(c.brick.chunk, chunks.data(), sizeof(BrickChunk) * nchunk, cudaMemcpyHostToDevice));
     OSM_CUDA(cudaMalloc(&c.brick.typetab, sizeof(uint32_t) * std::max<size_t>(16, typetab.size())));
     if (!typetab.empty())
       OSM_CUDA(cudaMemcpy(c.brick.typetab, typetab.data(), sizeof(uint32_t) * typetab.size(), cudaMemcpyHostToDevice));

@@ -173,24 +173,22 @@ struct BrickInfo {
   int32_t ls;
   int16_t bj, bi, bk, pad;
 };
-// Per (brick, class) constants of the Kuhn kernel: the row of point (jl, il, kl) is
-// qoff + jl + nJp il + nJI kl, a row for jl in [jlo, jhi], il in [ilo, ihi], kl in [klo, khi].
-struct alignas(16) BrickEpi {
-  int64_t qoff;
-  int32_t nJp, nJI;
-  int8_t jlo, jhi, ilo, ihi, klo, khi, pad0, pad1;
-  int64_t pad2;
+// Per (brick, class, il) chunk of the Kuhn kernel: desc >= 0 a row-type id (every row of the chunk has
+// the same index words: typetab[desc][0..ng)), < 0 -(g + 1) with the chunk's per-lane words at
+// cstream[32 g + 32 k + lane], k < ng; mask bit lane: the lane's point (jl = lane & 15, kl = lane >> 4)
+// is a row; its row is the subdomain's row0 + rowoff + jl + nJI kl.
+struct alignas(16) BrickChunk {
+  int32_t desc;
+  uint32_t mask;
+  int32_t rowoff;
+  int32_t nJI;
 };
 struct BrickDev {
   BrickInfo* info = nullptr;
-  BrickEpi* epi = nullptr;       // [brick][8] (Kuhn kernel)
+  BrickChunk* chunk = nullptr;   // [brick][class][il] (Kuhn kernel)
   BrickSub* sub = nullptr;
   uint32_t* stream = nullptr;    // u8 dictionary indices, 4 slots per word
   CUtensorMap* tmap = nullptr;   // (local subdomain, class) TMA maps of p
-  // Kuhn kernel: chunk (brick, class, il) descriptors: >= 0 a row-type id (every row of the chunk
-  // has the same index words: typetab[id][0..ng)), < 0 -(g + 1) with the chunk's per-lane words at
-  // cstream[32 g + 32 k + lane], k < ng
-  int32_t* desc = nullptr;
   uint32_t* typetab = nullptr;   // [ntypes][16]
   uint32_t* cstream = nullptr;   // per-lane words of the non-uniform chunks
 };

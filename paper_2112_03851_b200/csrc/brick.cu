@@ -436,7 +436,6 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   const uint32_t xs_addr = smem_addr(bsm);
   uint64_t* bar = reinterpret_cast<uint64_t*>(bsm + NC * kStride * 8);
   __shared__ double red[NW];
-  __shared__ int flag[1];
   const int64_t b = b0 + blockIdx.x;
   const BrickInfo bi = D.info[b];  // static: before the dependency wait
   const BrickSub& B = D.sub[bi.ls];
@@ -510,32 +509,38 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   pq = warp_sum_b(pq);
   if (lane == 0) red[w] = pq;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // the brick's partial; k_brick_alpha sums them (no atomic on this path)
     double v = 0.0;
     for (int k = 0; k < NW; ++k) v += red[k];
     part[b] = v;
-    __threadfence();
-    flag[0] = atomicAdd(&S.cnt, 1u) == (uint32_t)S.nbrick - 1;
   }
-  __syncthreads();
-  if (!flag[0]) return;
-  __threadfence();
-  double v = 0.0;  // fixed-order sum of the subdomain's brick partials: strided, then the block tree
-  for (int64_t m = threadIdx.x; m < S.nbrick; m += 32 * NW) v += __ldcg(part + S.brick0 + m);
+}
+
+// alpha = rho / p.q of each subdomain of a group from its brick partials (brick order: lane-strided
+// over the block, then the warp tree, then the warps in order): one block per subdomain, launched
+// after the Kuhn kernel (PDL), so the SpMV's CTAs retire without an atomic.
+__global__ void __launch_bounds__(256) k_brick_alpha(SubState* __restrict__ st, const double* __restrict__ part,
+                                                     int32_t* __restrict__ nactive, int ls0) {
+  __shared__ double red[8];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  SubState& S = st[ls0 + blockIdx.x];
+  if (!S.active) return;
+  double v = 0.0;
+  for (int64_t m = threadIdx.x; m < S.nbrick; m += 256) v += __ldcg(part + S.brick0 + m);
   v = warp_sum_b(v);
-  __syncthreads();
-  if (lane == 0) red[w] = v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
-    v = 0.0;
-    for (int k = 0; k < NW; ++k) v += red[k];
-    S.cnt = 0;
-    if (!(v > 0.0) || !isfinite(v)) {  // breakdown: p = 0 or loss of definiteness
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += red[k];
+    if (!(t > 0.0) || !isfinite(t)) {  // breakdown: p = 0 or loss of definiteness
       S.status = 3;
       S.active = 0;
       atomicSub(nactive, 1);
     } else {
-      S.alpha = S.rho / v;
+      S.alpha = S.rho / t;
     }
   }
 }
@@ -1059,6 +1064,11 @@ void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g) {
       OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, (const BrickDev)c.brick, c.h_brick_arg, c.st, c.q, c.part_brick,
                                   c.d_nactive, b0));
     });
+    cudaLaunchConfig_t ac = cfg;
+    ac.gridDim = dim3((unsigned)(s1 - s0));
+    ac.blockDim = dim3(256);
+    ac.dynamicSmemBytes = 0;
+    OSM_CUDA(cudaLaunchKernelEx(&ac, k_brick_alpha, c.st, (const double*)c.part_brick, c.d_nactive, s0));
   } else {
     go(k_cg_spmv_brick<8>);
   }

@@ -915,7 +915,10 @@ static void cg_spmv_v(Ctx& c) {
 void launch_cg_spmv(Ctx& c) {
   timer_begin(c, T_SPMV);
   switch (spmv_variant_of(c)) {
-    case 11: launch_cg_spmv_brick(c, launch_stream(c), c.grp_cur); break;
+    case 11:
+      launch_cg_spmv_brick(c, launch_stream(c), c.grp_cur);
+      if (c.brick_kernel > 0) ++c.launches;  // + k_brick_alpha
+      break;
     case 3: cg_spmv_v<3>(c); break;
     case 5: cg_spmv_v<5>(c); break;
     case 6: cg_spmv_v<6>(c); break;

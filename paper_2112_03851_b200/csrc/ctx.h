@@ -414,6 +414,7 @@ struct Ctx {
   int graph_maxit = -1;
   bool use_graph = true;
   bool force_remote = false;  // debug: every side goes through NCCL (peer = own rank), see osm_create
+  bool split_update = true;  // k_cg_update + k_cg_update_fin (no last-block atomic); OSM_SPLIT_UPD=0: one kernel
   int update_variant = 0;  // 0: k_cg_update at 96 regs, 1: capped for 8 blocks/SM
   int sort_key = 6;  // 6 (default): brick layout of the brick SpMV (variant 11): per subdomain, one dense
                     // array per lattice parity class (brick.cu); else the SELL row order inside sigma

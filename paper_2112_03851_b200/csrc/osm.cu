@@ -1159,6 +1159,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_NO_GRAPH")) c.use_graph = std::atoi(e) == 0;
     if (const char* e = std::getenv("OSM_SPMV")) c.spmv_variant = std::atoi(e);
     if (const char* e = std::getenv("OSM_UPD")) c.update_variant = std::atoi(e);
+    if (const char* e = std::getenv("OSM_SPLIT_UPD")) c.split_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("OSM_SORT")) c.sort_key = std::atoi(e);
     if (const char* e = std::getenv("OSM_DCODE")) c.dcode_on = std::atoi(e) != 0;
     c.timers.resize(T_COUNT);

@@ -503,7 +503,8 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
                                                            const double* __restrict__ dinv, double* __restrict__ part,
                                                            int64_t stride, double tol, int maxit,
                                                            int32_t* __restrict__ nactive, const uint8_t* __restrict__ mcode,
-                                                           const __grid_constant__ MfArg<V> mf, int64_t vb_base) {
+                                                           const __grid_constant__ MfArg<V> mf, int64_t vb_base,
+                                                           int split) {
   constexpr bool MF = V == 5;
   __shared__ double sm[(kVecThreads / 32) * 2];
   const int64_t vb = blockIdx.x + vb_base;
@@ -547,6 +548,13 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
     }
   block_sum<2, kVecThreads / 32>(v, sm);
   SubState& S = st[ls];
+  if (split) {  // k_cg_update_fin sums the partials: no atomic, the block retires at once
+    if (threadIdx.x == 0) {
+      part[vb] = v[0];
+      part[stride + vb] = v[1];
+    }
+    return;
+  }
   if (publish<2>(v, part, stride, vb, &S.cnt, S.nvblk)) {
     double t[2];
     gather_partials<2, kVecThreads / 32>(t, part, stride, S.vblk0, S.nvblk, sm);
@@ -569,6 +577,39 @@ __global__ void __launch_bounds__(kVecThreads, MINB) k_cg_update(const int32_t* 
         S.beta = rz / S.rho;
         S.rho = rz;
       }
+    }
+  }
+}
+
+// The update's per-subdomain step without the last-block atomic: one block (kVecThreads threads, the
+// update's own gather order, so the sums are bitwise the same) per subdomain of the group sums the
+// vector blocks' (r.z, r.r) partials and takes the stop test and beta.
+__global__ void __launch_bounds__(kVecThreads) k_cg_update_fin(SubState* __restrict__ st, const double* __restrict__ part,
+                                                               int64_t stride, double tol, int maxit,
+                                                               int32_t* __restrict__ nactive, int ls0) {
+  __shared__ double sm[(kVecThreads / 32) * 2];
+  pdl_enter();
+  SubState& S = st[ls0 + blockIdx.x];
+  if (!S.active) return;
+  double t[2];
+  gather_partials<2, kVecThreads / 32>(t, part, stride, S.vblk0, S.nvblk, sm);
+  if (threadIdx.x == 0) {
+    const double rz = t[0], rr = t[1];
+    S.rr = rr;
+    S.iters += 1;
+    if (sqrt(rr) <= tol * sqrt(S.bb)) {
+      S.status = 1;
+      S.active = 0;
+      S.xpend = 1;
+      atomicSub(nactive, 1);
+    } else if (S.iters >= maxit) {
+      S.status = 2;
+      S.active = 0;
+      S.xpend = 1;
+      atomicSub(nactive, 1);
+    } else {
+      S.beta = rz / S.rho;
+      S.rho = rz;
     }
   }
 }
@@ -952,7 +993,18 @@ static void cg_update_v(Ctx& c, double tol, int maxit, const uint8_t* code, cons
   launch_pdl(c, k_cg_update<MINB, V>, (unsigned)grp_nvb(c), kVecThreads, (size_t)0, (const int32_t*)c.vblk_sub,
              (const int32_t*)c.vblk_tile0, (const int32_t*)c.vblk_ntile, c.st, c.x, c.r, (const double*)c.p,
              (const double*)c.q, (const double*)c.dinv, c.part_upd, c.nvblk_total, tol, maxit, c.d_nactive, code,
-             mf, grp_vb0(c));
+             mf, grp_vb0(c), c.split_update ? 1 : 0);
+  if (c.split_update) {
+    const int nloc = c.s_end - c.s_begin;
+    int s0 = 0, s1 = nloc;
+    if (c.grp_cur >= 0) {
+      s0 = c.grp_cur * nloc / c.ngroups;
+      s1 = (c.grp_cur + 1) * nloc / c.ngroups;
+    }
+    launch_pdl(c, k_cg_update_fin, (unsigned)(s1 - s0), kVecThreads, (size_t)0, c.st, (const double*)c.part_upd,
+               c.nvblk_total, tol, maxit, c.d_nactive, s0);
+    ++c.launches;
+  }
 }
 
 void launch_cg_update(Ctx& c, double tol, int maxit) {

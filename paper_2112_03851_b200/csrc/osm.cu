@@ -690,7 +690,10 @@ static void assemble(Ctx& c) {
   // two subdomain groups for the two-stream PCG (halves of the local subdomains, in block order)
   c.ngroups = 1;
   while (c.ngroups * 2 <= std::min(c.want_groups, nloc)) c.ngroups *= 2;
-  {  // groups only pay while a group's SpMV is a few waves (C3: ~1 wave); at C5 they thrash L2
+  // with the tile SpMVs, groups only pay while a group's SpMV is a few waves (C3: ~1 wave); at C5 they
+  // thrash L2.  The brick path (the default) gains from them at C5 too (33.3 s with 8 groups against
+  // 34.2 s with one, tools/cg_bench.py, r02), so it keeps them.
+  if (c.spmv_variant != 11) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
     const int64_t wave = 8LL * sms;  // SpMV blocks resident per wave

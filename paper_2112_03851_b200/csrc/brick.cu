@@ -460,11 +460,8 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   __syncthreads();  // barrier initialised
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  SubState& S = st[bi.ls];
-  if (!S.active) {  // the previous direction kernel has paid the stopped subdomain's x update
-    if (threadIdx.x == 0 && b == S.brick0) S.xpend = 0;
-    return;
-  }
+  // the boxes are requested before the subdomain's active flag is read (its load would otherwise sit
+  // on every CTA's critical path); a stopped subdomain's CTAs drain them and leave
   if (w == 0) {
     if (lane == 0) mbar_expect_tx(bar, (uint32_t)(NC * a.box_elems * 8));
     __syncwarp();
@@ -474,6 +471,12 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
       tma_load_3d(reinterpret_cast<double*>(bsm) + c * kStride, D.tmap + bi.ls * NC + c,
                   bi.bj * 16 - 1 - C.jjlo - jsh_of(c), bi.bi * BI - 1 - C.iilo, bi.bk * 2 - 1 - C.kklo, bar);
     }
+  }
+  SubState& S = st[bi.ls];
+  if (!S.active) {  // the previous direction kernel has paid the stopped subdomain's x update
+    if (threadIdx.x == 0 && b == S.brick0) S.xpend = 0;
+    mbar_wait_parity(bar, 0);  // no CTA leaves with bulk copies into its shared memory in flight
+    return;
   }
   const uint32_t lane_off = 8u * (uint32_t)((jl + 1) + 20 * (BI + 2) * (kl + 1) + 20 * (w + 1));
   mbar_wait_parity(bar, 0);

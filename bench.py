@@ -302,9 +302,12 @@ def main():
                      "traffic": ncu_traffic("fp64_sell_variant2_k_cg_spmv_r01b")[0],
                      "us_per_launch": 1e3 * kt2["cg_spmv"][1] / max(1, kt2["cg_spmv"][0]), "variant": active}
     brick = default_variant == 11
-    kname = f"k_cg_spmv_kuhn<{brick_bi(cfg)}>" if brick else f"k_cg_spmv<{default_variant}>"
+    # the Kuhn SpMV carries the direction update (k_cg_dir then runs only as the per-solve flush)
+    fused = brick and kt["cg_dir"][0] < kt["cg_spmv"][0] // 2
+    kname = (f"k_cg_spmv_kuhn{'_fused' if fused else ''}<{brick_bi(cfg)}>" if brick
+             else f"k_cg_spmv<{default_variant}>")
     if brick:
-        tr, tr_src = ncu_traffic("k_cg_spmv_kuhn")
+        tr, tr_src = ncu_traffic("k_cg_spmv_kuhn_fused" if fused else "k_cg_spmv_kuhn")
     roofline = {"bound": "hbm", "kernel": kname, "variant": default_variant, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak if achieved else None,
                 "traffic": tr, "traffic_source": tr_src, "peak_source": peak_src,
@@ -320,6 +323,8 @@ def main():
                            "in column order, 16 x BI x 2-point bricks of each parity class; + 16 B per row (p "
                            "read, q write); the p boxes are TMA-staged in shared memory (their halo re-reads "
                            "come from L2 and are not counted); dictionary (<= 256 slots) in the constant bank"
+                           + ("; fused direction update: + 33 B per row (r and the 1-byte D^-1 code read, x "
+                              "read and written, p_{k+1} written)" if fused else "")
                            if brick else
                            "value-indexed SELL-256, 3-byte entries: per 8 entries one 16-B load of int16 column "
                            "offsets and one 8-B load of u8 dictionary indices, + 16 B per row (p, q); dictionary "
@@ -333,7 +338,9 @@ def main():
                 "limiter": ("instruction issue and latency at ~27 resident warps per SM (shared-memory loads, "
                             "dictionary LDCs and the FMA chain per row), not HBM: DESIGN.md 'Brick SpMV'"
                             if brick else "latency of the dependent load chains (packed entry -> x gather -> FMA)"),
-                "limiter_metrics": ncu_traffic("k_cg_spmv_kuhn_pipes")[0] if brick else None}
+                "fused_direction": fused,
+                "limiter_metrics": ncu_traffic("k_cg_spmv_kuhn_fused_pipes" if fused else "k_cg_spmv_kuhn_pipes")[0]
+                if brick else None}
 
     # Whole PCG hot loop against the HBM roofline: algorithmic bytes of the three CG kernels (SpMV in
     # its own format + update + direction) of one solve, over the timed step (everything included).

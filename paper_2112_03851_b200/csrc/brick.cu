@@ -425,10 +425,15 @@ using IC = std::integral_constant<int, C>;
 // Dynamic shared memory of k_cg_spmv_kuhn<BI>: the class boxes (128-byte aligned by hand) and the
 // mbarrier; the reduction slots are static
 constexpr int kuhn_smem_bytes(int BI) { return 8 * box_stride_of(BI) * 8 + 16 + 128; }
-template <int BI>
-__global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
-    const BrickDev D, const __grid_constant__ BrickArg a, SubState* __restrict__ st, double* __restrict__ q,
-    double* __restrict__ part, int32_t* __restrict__ nactive, int64_t b0) {
+// FUSE: the PCG direction update rides on the SpMV (BrickFuse, ctx.h).  After the boxes of p_k land,
+// the CTA pays x_{k+1} = x_k + alpha_k p_k on its own rows (p_k from shared memory), then forms
+// p_{k+1} = fma(beta_k, p_k, D^{-1} r_{k+1}) in place on every staged point -- the halo too, whose
+// values other CTAs form identically -- and the stencil runs on p_{k+1}; own rows of p_{k+1} go to the
+// other p buffer.  Bitwise the same x, p and q as k_cg_dir followed by the plain kernel.
+template <int BI, bool FUSE>
+__device__ __forceinline__ void kuhn_spmv_body(
+    const BrickDev& D, const BrickArg& a, SubState* __restrict__ st, double* __restrict__ q,
+    double* __restrict__ part, int32_t* __restrict__ nactive, int64_t b0, const BrickFuse& f) {
   constexpr int NC = 8, NW = BI;
   constexpr int kStride = box_stride_of(BI);
   extern __shared__ __align__(128) unsigned char bsm_raw[];
@@ -436,9 +441,14 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   const uint32_t xs_addr = smem_addr(bsm);
   uint64_t* bar = reinterpret_cast<uint64_t*>(bsm + NC * kStride * 8);
   __shared__ double red[NW];
+  // fused path: per class, the box origin in the class array (jj, ii, kk), nJp, nIc, nKc, first row
+  __shared__ int4 fgeo[FUSE ? NC : 1];
+  __shared__ int2 fext[FUSE ? NC : 1];
+  __shared__ long long fbase[FUSE ? NC : 1];
   const int64_t b = b0 + blockIdx.x;
   const BrickInfo bi = D.info[b];  // static: before the dependency wait
   const BrickSub& B = D.sub[bi.ls];
+  const CUtensorMap* tm = (FUSE ? f.tmap : D.tmap) + bi.ls * NC;
   const int lane = threadIdx.x & 31;
   const int w = __reduce_max_sync(0xffffffffu, (unsigned)(threadIdx.x >> 5));  // = il
   // the constants of this warp's 8 chunks (C, il = w): lane C holds class C's (desc, row mask, row
@@ -454,7 +464,16 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   double* qs = q + B.row0;  // the subdomain's rows
   if (w == 0) {
     if (lane == 0) mbar_init(bar, 1);
-    if (lane < NC) asm volatile("prefetch.tensormap [%0];" ::"l"(D.tmap + bi.ls * NC + lane) : "memory");
+    if (lane < NC) asm volatile("prefetch.tensormap [%0];" ::"l"(tm + lane) : "memory");
+  }
+  if constexpr (FUSE) {
+    if (threadIdx.x < NC) {
+      const int c = threadIdx.x;
+      const BrickClass& C = B.cls[c];
+      fgeo[c] = make_int4(bi.bj * 16 - 1 - C.jjlo - jsh_of(c), bi.bi * BI - 1 - C.iilo, bi.bk * 2 - 1 - C.kklo, C.nJp);
+      fext[c] = make_int2(C.nIc, C.nKc);
+      fbase[c] = B.row0 + C.base;
+    }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();  // barrier initialised
@@ -468,18 +487,88 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
     if (lane < NC) {
       const int c = lane;
       const BrickClass& C = B.cls[c];
-      tma_load_3d(reinterpret_cast<double*>(bsm) + c * kStride, D.tmap + bi.ls * NC + c,
-                  bi.bj * 16 - 1 - C.jjlo - jsh_of(c), bi.bi * BI - 1 - C.iilo, bi.bk * 2 - 1 - C.kklo, bar);
+      tma_load_3d(reinterpret_cast<double*>(bsm) + c * kStride, tm + c, bi.bj * 16 - 1 - C.jjlo - jsh_of(c),
+                  bi.bi * BI - 1 - C.iilo, bi.bk * 2 - 1 - C.kklo, bar);
     }
   }
   SubState& S = st[bi.ls];
-  if (!S.active) {  // the previous direction kernel has paid the stopped subdomain's x update
-    if (threadIdx.x == 0 && b == S.brick0) S.xpend = 0;
-    mbar_wait_parity(bar, 0);  // no CTA leaves with bulk copies into its shared memory in flight
-    return;
-  }
   const uint32_t lane_off = 8u * (uint32_t)((jl + 1) + 20 * (BI + 2) * (kl + 1) + 20 * (w + 1));
-  mbar_wait_parity(bar, 0);
+  if constexpr (FUSE) {
+    const int act = S.active;
+    if (!act && !S.xpend) {  // stopped earlier (its x is paid; k_brick_alpha cleared xpend)
+      mbar_wait_parity(bar, 0);
+      return;
+    }
+    const double al = S.alpha, be = S.beta;
+    mbar_wait_parity(bar, 0);
+    // x_{k+1} = x_k + alpha_k p_k on the brick's rows (the update k_cg_dir would have made)
+    double* xs = f.x + B.row0;
+    double xo[NC];
+    int xi[NC];
+    uint32_t own = 0;
+#pragma unroll
+    for (int C = 0; C < NC; ++C) {
+      const uint32_t m = (uint32_t)__shfl_sync(0xffffffffu, creg.y, C);
+      const int ro = __shfl_sync(0xffffffffu, creg.z, C), nji = __shfl_sync(0xffffffffu, creg.w, C);
+      xi[C] = ro + jl + nji * kl;
+      if ((m >> lane) & 1u) {
+        own |= 1u << C;
+        xo[C] = xs[xi[C]];
+      }
+    }
+#pragma unroll
+    for (int C = 0; C < NC; ++C)
+      if ((own >> C) & 1u)
+        xs[xi[C]] = fma(al, lds_f64(xs_addr + 8u * (uint32_t)(C * kStride + jsh_of(C)) + lane_off), xo[C]);
+    if (!act) return;  // stopped in the last update: only its x was owed (uniform over the CTA)
+    __syncthreads();   // every p_k read above precedes the overwrite below
+    // p_{k+1} on every staged point: columns (class, box kk, box jj) of BI + 2 points along ii, jj
+    // fastest over the threads (coalesced r and code loads); points outside the class array stay
+    // the TMA's zero fill
+    double* pb = reinterpret_cast<double*>(bsm);
+    constexpr int kCols = NC * 4 * 20;
+    for (int col = threadIdx.x; col < kCols; col += 32 * BI) {
+      const int c = col / 80, rem = col - 80 * c, ek = rem / 20, ej = rem - 20 * ek;
+      const int4 g = fgeo[c];
+      const int2 e = fext[c];
+      const int gj = g.x + ej, gk = g.z + ek;
+      if (gj < 0 || gj >= g.w || gk < 0 || gk >= e.y) continue;
+      const int64_t o0 = fbase[c] + gj + (int64_t)g.w * e.x * gk;
+      double* pc = pb + c * kStride + ej + 20 * (BI + 2) * ek;
+      constexpr int NE = BI + 2, NB = (NE + 1) / 2;  // two batches of loads in flight
+#pragma unroll
+      for (int e0 = 0; e0 < NE; e0 += NB) {
+        double rv[NB];
+        uint32_t cv[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int gi = g.y + e0 + u;
+          if (e0 + u < NE && gi >= 0 && gi < e.x) {
+            const int64_t o = o0 + (int64_t)g.w * gi;
+            rv[u] = __ldg(f.r + o);
+            cv[u] = __ldg(f.code + o);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int gi = g.y + e0 + u;
+          if (e0 + u < NE && gi >= 0 && gi < e.x) {
+            const double d = cv[u] != 0xffu ? f.dtab[cv[u]] : 0.0;
+            pc[20 * (e0 + u)] = fma(be, pc[20 * (e0 + u)], __dmul_rn(d, rv[u]));
+          }
+        }
+      }
+    }
+    __syncthreads();
+  } else {
+    if (!S.active) {  // the previous direction kernel has paid the stopped subdomain's x update
+      if (threadIdx.x == 0 && b == S.brick0) S.xpend = 0;
+      mbar_wait_parity(bar, 0);  // no CTA leaves with bulk copies into its shared memory in flight
+      return;
+    }
+    mbar_wait_parity(bar, 0);
+  }
+  double* pns = FUSE ? f.pn + B.row0 : nullptr;
   double pq = 0.0;
   auto run = [&](auto cc, const uint32_t(&Wc)[16]) {
     constexpr int C = decltype(cc)::value;
@@ -488,8 +577,10 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
     const uint32_t m = (uint32_t)__shfl_sync(0xffffffffu, creg.y, C);
     const int ro = __shfl_sync(0xffffffffu, creg.z, C), nji = __shfl_sync(0xffffffffu, creg.w, C);
     if ((m >> lane) & 1u) {
+      const double pv = lds_f64(xc);
       qs[ro + jl + nji * kl] = s;
-      pq = fma(lds_f64(xc), s, pq);
+      if constexpr (FUSE) pns[ro + jl + nji * kl] = pv;
+      pq = fma(pv, s, pq);
     }
   };
   kuhn_words<2>(W2, D, dsc(2), lane);
@@ -519,6 +610,24 @@ __global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(
   }
 }
 
+// The plain kernel, and the fused one held to the plain one's occupancy (3 CTAs per SM up to BI = 9,
+// else 2: the phase-B registers would otherwise cost a CTA per SM).
+template <int BI, bool FUSE>
+__global__ void __launch_bounds__(32 * BI) k_cg_spmv_kuhn(const BrickDev D, const __grid_constant__ BrickArg a,
+                                                          SubState* __restrict__ st, double* __restrict__ q,
+                                                          double* __restrict__ part, int32_t* __restrict__ nactive,
+                                                          int64_t b0, const __grid_constant__ BrickFuse f) {
+  static_assert(!FUSE, "the fused instance is k_cg_spmv_kuhn_fused");
+  kuhn_spmv_body<BI, false>(D, a, st, q, part, nactive, b0, f);
+}
+template <int BI>
+__global__ void __launch_bounds__(32 * BI, BI <= 9 ? 3 : 2)
+    k_cg_spmv_kuhn_fused(const BrickDev D, const __grid_constant__ BrickArg a, SubState* __restrict__ st,
+                         double* __restrict__ q, double* __restrict__ part, int32_t* __restrict__ nactive, int64_t b0,
+                         const __grid_constant__ BrickFuse f) {
+  kuhn_spmv_body<BI, true>(D, a, st, q, part, nactive, b0, f);
+}
+
 // alpha = rho / p.q of each subdomain of a group from its brick partials (brick order: lane-strided
 // over the block, then the warp tree, then the warps in order): one block per subdomain, launched
 // after the Kuhn kernel (PDL), so the SpMV's CTAs retire without an atomic.
@@ -528,7 +637,10 @@ __global__ void __launch_bounds__(256) k_brick_alpha(SubState* __restrict__ st, 
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   SubState& S = st[ls0 + blockIdx.x];
-  if (!S.active) return;
+  if (!S.active) {  // a stopped subdomain's pending x update has been paid by the SpMV (fused or k_cg_dir)
+    if (threadIdx.x == 0) S.xpend = 0;
+    return;
+  }
   double v = 0.0;
   for (int64_t m = threadIdx.x; m < S.nbrick; m += 256) v += __ldcg(part + S.brick0 + m);
   v = warp_sum_b(v);
@@ -548,22 +660,27 @@ __global__ void __launch_bounds__(256) k_brick_alpha(SubState* __restrict__ st, 
   }
 }
 
-// f(k_cg_spmv_kuhn<BI>) for a runtime BI in 1..12
-template <class F>
+// f(k_cg_spmv_kuhn<BI, FUSE>) for a runtime BI in 1..12
+template <int BI, bool FUSE>
+constexpr auto kuhn_kernel() {
+  if constexpr (FUSE) return k_cg_spmv_kuhn_fused<BI>;
+  else return k_cg_spmv_kuhn<BI, false>;
+}
+template <bool FUSE, class F>
 void with_kuhn_kernel(int BI, F&& f) {
   switch (BI) {
-    case 1: f(k_cg_spmv_kuhn<1>); break;
-    case 2: f(k_cg_spmv_kuhn<2>); break;
-    case 3: f(k_cg_spmv_kuhn<3>); break;
-    case 4: f(k_cg_spmv_kuhn<4>); break;
-    case 5: f(k_cg_spmv_kuhn<5>); break;
-    case 6: f(k_cg_spmv_kuhn<6>); break;
-    case 7: f(k_cg_spmv_kuhn<7>); break;
-    case 8: f(k_cg_spmv_kuhn<8>); break;
-    case 9: f(k_cg_spmv_kuhn<9>); break;
-    case 10: f(k_cg_spmv_kuhn<10>); break;
-    case 11: f(k_cg_spmv_kuhn<11>); break;
-    case 12: f(k_cg_spmv_kuhn<12>); break;
+    case 1: f(kuhn_kernel<1, FUSE>()); break;
+    case 2: f(kuhn_kernel<2, FUSE>()); break;
+    case 3: f(kuhn_kernel<3, FUSE>()); break;
+    case 4: f(kuhn_kernel<4, FUSE>()); break;
+    case 5: f(kuhn_kernel<5, FUSE>()); break;
+    case 6: f(kuhn_kernel<6, FUSE>()); break;
+    case 7: f(kuhn_kernel<7, FUSE>()); break;
+    case 8: f(kuhn_kernel<8, FUSE>()); break;
+    case 9: f(kuhn_kernel<9, FUSE>()); break;
+    case 10: f(kuhn_kernel<10, FUSE>()); break;
+    case 11: f(kuhn_kernel<11, FUSE>()); break;
+    case 12: f(kuhn_kernel<12, FUSE>()); break;
     default: fail(OSM_ERR_STATE, "brick: no Kuhn kernel for this BI");
   }
 }
@@ -595,6 +712,8 @@ void brick_free(Ctx& c) {
   if (c.brick.sub) cudaFree(c.brick.sub);
   if (c.part_brick) cudaFree(c.part_brick);
   c.part_brick = nullptr;
+  if (c.p2) cudaFree(c.p2);
+  c.p2 = nullptr;
   c.brick = BrickDev{};
   c.brick_ok = false;
   c.brick_total = 0;
@@ -859,9 +978,17 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
     c.brick = BrickDev{};
     return;
   }
-  // 5. TMA tensor maps of p: one per (local subdomain, class), dims (nJp, nIc, nKc), jj fastest
-  std::vector<CUtensorMap> maps((size_t)nloc * nc);
+  // 5. TMA tensor maps of p: one per (local subdomain, class), dims (nJp, nIc, nKc), jj fastest; with the
+  // Kuhn kernel a second set over p2 (the fused direction update's other p buffer, zero-initialised:
+  // its padding rows are never written)
+  if (c.brick_kernel > 0 && !c.p2) {
+    OSM_CUDA(cudaMalloc(&c.p2, sizeof(double) * std::max<int64_t>(1, c.nrows_total)));
+    OSM_CUDA(cudaMemset(c.p2, 0, sizeof(double) * c.nrows_total));
+  }
+  const int nset = c.brick_kernel > 0 ? 2 : 1;
+  std::vector<CUtensorMap> maps((size_t)nset * nloc * nc);
   auto enc = encode_fn();
+  for (int set = 0; set < nset; ++set)
   for (int ls = 0; ls < nloc; ++ls)
     for (int cc = 0; cc < nc; ++cc) {
       const BrickClass& C = subs[ls].cls[cc];
@@ -871,8 +998,8 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
                                      (cuuint64_t)std::max(2, C.nJp) * std::max(1, C.nIc) * 8};
       const cuuint32_t box[3] = {(cuuint32_t)(A.BJ + 4), (cuuint32_t)(A.BI + 2), (cuuint32_t)(A.BK + 2)};
       const cuuint32_t es[3] = {1, 1, 1};
-      void* base = c.p + subs[ls].row0 + C.base;
-      const CUresult r = enc(&maps[(size_t)ls * nc + cc], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
+      void* base = (set ? c.p2 : c.p) + subs[ls].row0 + C.base;
+      const CUresult r = enc(&maps[((size_t)set * nloc + ls) * nc + cc], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) fail(OSM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -1016,7 +1143,10 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
       };
       set_max(k_cg_spmv_brick<8>);
       set_max(k_cg_spmv_brick<1>);
-      for (int bi = 1; bi <= 12; ++bi) with_kuhn_kernel(bi, set_max);
+      for (int bi = 1; bi <= 12; ++bi) {
+        with_kuhn_kernel<false>(bi, set_max);
+        with_kuhn_kernel<true>(bi, set_max);
+      }
       attr_done[dev] = true;
     }
   }
@@ -1063,10 +1193,24 @@ void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g) {
   } else if (c.brick_kernel > 0) {
     cfg.blockDim = dim3(32 * c.brick_kernel);
     cfg.dynamicSmemBytes = kuhn_smem_bytes(c.brick_kernel);
-    with_kuhn_kernel(c.brick_kernel, [&](auto kern) {
+    BrickFuse& F = c.h_brick_fuse;
+    auto launch = [&](auto kern) {
       OSM_CUDA(cudaLaunchKernelEx(&cfg, kern, (const BrickDev)c.brick, c.h_brick_arg, c.st, c.q, c.part_brick,
-                                  c.d_nactive, b0));
-    });
+                                  c.d_nactive, b0, F));
+    };
+    if (fused_dir(c)) {  // p_k in p (parity 0) or p2 (parity 1); p_{k+1} to the other buffer
+      F.tmap = c.brick.tmap + (size_t)(c.cg_par & 1) * nloc * nc;
+      F.pn = (c.cg_par & 1) ? c.p : c.p2;
+      F.x = c.x;
+      F.r = c.r;
+      F.code = c.d_dcode;
+      std::fill(F.dtab, F.dtab + kMfMaxTab, 0.0);
+      std::copy(c.h_dcode_tab.begin(), c.h_dcode_tab.end(), F.dtab);
+      with_kuhn_kernel<true>(c.brick_kernel, launch);
+    } else {
+      F = BrickFuse{};
+      with_kuhn_kernel<false>(c.brick_kernel, launch);
+    }
     cudaLaunchConfig_t ac = cfg;
     ac.gridDim = dim3((unsigned)(s1 - s0));
     ac.blockDim = dim3(256);

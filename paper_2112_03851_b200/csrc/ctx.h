@@ -206,6 +206,18 @@ struct BrickArg {
   int32_t soff[8 * 4 * kBrickMaxGroups];
   double dict[256];
 };
+// The PCG direction update fused into the Kuhn SpMV (brick.cu, Ctx::fuse_dir): the kernel of iteration
+// k+1 forms p_{k+1} = D^{-1} r_{k+1} + beta_k p_k on its staged boxes (halo included) and pays
+// x_{k+1} = x_k + alpha_k p_k on its own rows, so k_cg_dir does not run; p alternates between Ctx::p
+// and Ctx::p2 (neighbouring CTAs still read p_k while a CTA writes p_{k+1}).
+struct BrickFuse {
+  const CUtensorMap* tmap;  // TMA maps of p_k (the buffer read in this iteration)
+  double* pn;               // p_{k+1} (the other buffer)
+  double* x;
+  const double* r;
+  const uint8_t* code;      // D^{-1} codes (osm.cu dcode_build; 0xff = +0.0)
+  double dtab[kMfMaxTab];
+};
 // Build-time view (brick.cu).
 struct BrickBuildDev {
   int o;
@@ -402,6 +414,8 @@ struct Ctx {
   cudaStream_t gstream[kMaxGroups] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
   cudaGraphExec_t cg_graph_g[kMaxGroups] = {};
+  int64_t cg_graph_launches_g[kMaxGroups] = {};  // kernels in one replay of cg_graph_g[g] / cg_graph
+  int64_t cg_graph_launches = 0;
   int64_t g_blk0[kMaxGroups] = {}, g_nblk[kMaxGroups] = {}, g_vb0[kMaxGroups] = {}, g_nvb[kMaxGroups] = {};
   int vec_tiles = kVecTiles;  // tiles per vector block (update/dir kernels), chosen at assembly
   int vt_override = 0;         // OSM_VT
@@ -460,6 +474,11 @@ struct Ctx {
   int brick_ntypes = 0;
   int brick_kernel = 0;          // 1..12: the P2 Kuhn kernel k_cg_spmv_kuhn<BI>; 0: the generic brick kernel
   double* part_brick = nullptr;  // one p.q partial per brick
+  // direction update fused into the Kuhn SpMV (BrickFuse; OSM_FUSE_DIR=0: k_cg_dir runs)
+  bool fuse_dir = false;  // measured slower: opt-in
+  double* p2 = nullptr;          // the second p buffer of the fused path
+  int cg_par = 0;                // PCG iteration parity within a chunk: p_k in p (0) or p2 (1)
+  BrickFuse h_brick_fuse{};      // the fused kernel's parameter (host copy, rebuilt per launch)
 
   // value-indexed SELL (vi.cu)
   bool vi_ok = false;         // dictionary and fold tuples built (the brick copy needs only these)
@@ -546,6 +565,8 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx);  // brick.c
 void brick_free(Ctx& c);
 void brick_geometry(const Ctx& c, int ls, BrickSub& B);
 void launch_cg_spmv_brick(Ctx& c, cudaStream_t s, int g);
+bool fused_dir(const Ctx& c);  // schwarz_kernels.cu: the Kuhn SpMV carries the direction update
+void launch_cg_dir_flush(Ctx& c);
 int spmv_variant_of(const Ctx& c);  // the variant actually launched (3 falls back to 2 without vi)
 
 // timing helpers (osm.cu)

@@ -849,6 +849,7 @@ static void enqueue_group_chunk(Ctx& c, int g, double tol, int maxit) {
     c.grp_cur = g;
     OSM_CUDA(cudaStreamBeginCapture(c.gstream[g], cudaStreamCaptureModeThreadLocal));
     try {
+      c.cg_par = 0;
       for (int it = 0; it < kCgChunk; ++it) {
         launch_cg_spmv(c);
         launch_cg_update(c, tol, maxit);
@@ -864,11 +865,12 @@ static void enqueue_group_chunk(Ctx& c, int g, double tol, int maxit) {
     OSM_CUDA(cudaStreamEndCapture(c.gstream[g], &gr));
     const cudaError_t e = cudaGraphInstantiate(&c.cg_graph_g[g], gr, 0);
     cudaGraphDestroy(gr);
+    c.cg_graph_launches_g[g] = c.launches - l0;
     c.launches = l0;
     if (e != cudaSuccess) fail(OSM_ERR_CUDA, "graph instantiation failed");
   }
   OSM_CUDA(cudaGraphLaunch(c.cg_graph_g[g], c.gstream[g]));
-  c.launches += 3 * kCgChunk;
+  c.launches += c.cg_graph_launches_g[g];
 }
 
 static bool group_streams(const Ctx& c) { return c.ngroups > 1 && !c.timing && c.use_graph; }
@@ -881,6 +883,7 @@ static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
     return;
   }
   if (c.timing || !c.use_graph) {
+    c.cg_par = 0;
     for (int it = 0; it < kCgChunk; ++it) {
       launch_cg_spmv(c);
       launch_cg_update(c, tol, maxit);
@@ -894,6 +897,7 @@ static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
     cudaGraph_t g = nullptr;
     OSM_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     try {
+      c.cg_par = 0;
       for (int it = 0; it < kCgChunk; ++it) {
         launch_cg_spmv(c);
         launch_cg_update(c, tol, maxit);
@@ -907,6 +911,7 @@ static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
     OSM_CUDA(cudaStreamEndCapture(c.stream, &g));
     const cudaError_t e = cudaGraphInstantiate(&c.cg_graph, g, 0);
     cudaGraphDestroy(g);
+    c.cg_graph_launches = c.launches - l0;
     c.launches = l0;
     if (e != cudaSuccess) {  // graphs unavailable: plain stream launches (same kernels)
       cudaGetLastError();
@@ -919,7 +924,7 @@ static void enqueue_cg_chunk(Ctx& c, double tol, int maxit) {
     c.graph_maxit = maxit;
   }
   OSM_CUDA(cudaGraphLaunch(c.cg_graph, c.stream));
-  c.launches += 3 * kCgChunk;
+  c.launches += c.cg_graph_launches;
 }
 
 static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
@@ -981,6 +986,7 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
         if ((int64_t)ch * kCgChunk > (int64_t)o.max_inner + 2 * kCgChunk) break;  // safety net
       }
       if (grp) OSM_CUDA(cudaStreamWaitEvent(c.stream, c.ev_chunk[ch & 1], 0));
+      launch_cg_dir_flush(c);  // fused path: an x update still owed after the last SpMV
     }
     {
       NvtxRange nv_x("trace_exchange");
@@ -1048,7 +1054,10 @@ static osm_status solve(Ctx& c, const osm_solve_opts& o, osm_report* rep) {
     const bool coded = mf ? c.d_mf_code != nullptr : !c.h_dcode_tab.empty();
     const double db = coded ? 1.0 : 8.0;
     c.traffic[1] += (double)its * (24.0 + db) * S.n;  // update: read r, q, D^-1; write r
-    c.traffic[2] += (double)its * (40.0 + db) * S.n;  // direction: read r, D^-1, p, x; write p, x
+    if (fused_dir(c))  // the SpMV reads r, D^-1 (codes) and x, writes x and p_{k+1}
+      c.traffic[0] += (double)its * (32.0 + db) * S.n;
+    else
+      c.traffic[2] += (double)its * (40.0 + db) * S.n;  // direction: read r, D^-1, p, x; write p, x
     c.traffic[3] += (double)(S.sell_entries - S.nnz);
     c.traffic[4] += (double)S.nnz;
     c.traffic[5] += (double)S.n;
@@ -1165,6 +1174,7 @@ osm_status osm_create(const osm_mesh_desc* mesh, const osm_dist_desc* dist, osm_
     if (const char* e = std::getenv("OSM_SPLIT_UPD")) c.split_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("OSM_SORT")) c.sort_key = std::atoi(e);
     if (const char* e = std::getenv("OSM_DCODE")) c.dcode_on = std::atoi(e) != 0;
+    if (const char* e = std::getenv("OSM_FUSE_DIR")) c.fuse_dir = std::atoi(e) != 0;
     c.timers.resize(T_COUNT);
     const char* names[T_COUNT] = {"cg_spmv", "cg_update", "cg_dir", "warm_spmv", "resid_spmv", "exchange"};
     for (int i = 0; i < T_COUNT; ++i) c.timers[i].name = names[i];

@@ -709,6 +709,8 @@ __global__ void OSM_SPMV_BOUNDS(V) k_warm(SellDev A, const int32_t* __restrict__
       S.bb = t[2];
       S.iters = 0;
       S.xpend = 0;
+      S.alpha = 0.0;  // the fused path's first SpMV then keeps x and forms p = fma(0, p, z) = z
+      S.beta = 0.0;
       S.zero_rhs = (t[2] == 0.0);
       if (t[2] == 0.0 || sqrt(t[1]) <= tol * sqrt(t[2])) {
         S.status = 1;
@@ -1028,7 +1030,30 @@ static void cg_dir_v(Ctx& c, const uint8_t* code, const MfArg<V>& mf) {
              (const double*)c.dinv, c.p, c.x, code, mf, grp_vb0(c));
 }
 
+// The Kuhn brick SpMV carries the direction update (BrickFuse): it needs the D^{-1} codes and the p2
+// buffer (brick.cu builds it with the Kuhn kernel).
+bool fused_dir(const Ctx& c) {
+  return c.fuse_dir && spmv_variant_of(c) == 11 && c.brick_kernel > 0 && c.p2 && dcode_vectors(c) &&
+         c.h_dcode_tab.size() <= (size_t)kMfMaxTab;
+}
+
+// k_cg_dir once after a batched PCG run of the fused path: x += alpha p for a subdomain that stopped
+// in the last update of the run (xpend) with no SpMV after it.  p_k is in Ctx::p (chunks hold an even
+// number of iterations); an already paid x has xpend cleared by k_brick_alpha.
+void launch_cg_dir_flush(Ctx& c) {
+  if (!fused_dir(c)) return;
+  c.cg_par = 0;
+  timer_begin(c, T_DIR);
+  cg_dir_v<5>(c, c.d_dcode, dcode_arg(c));
+  ++c.launches;
+  timer_end(c, T_DIR);
+}
+
 void launch_cg_dir(Ctx& c) {
+  if (fused_dir(c)) {  // done by the next SpMV
+    c.cg_par ^= 1;
+    return;
+  }
   timer_begin(c, T_DIR);
   if (mf_vectors(c))
     cg_dir_v<5>(c, c.d_mf_code, mf_arg<5>(c));

@@ -14,7 +14,7 @@ python bench.py --steps 2 --warmup 1 --no-c5 --no-cpu-baseline --no-alt-spmv > g
     python bench.py --steps 2 --warmup 1 --no-c5 --no-cpu-baseline --no-alt-spmv > gpurun_out/${tag}_ncu_launch.log 2>&1
 # full captures: one launch each of the SpMV / k_cg_update / k_cg_dir over all 8 C3 subdomains
 python tools/cg_bench.py --solves 1 --timing --no-warm > gpurun_out/${tag}_cg_plain.log 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k regex:"k_cg_(spmv_kuhn|update|dir)($|<)" -s 30 -c 3 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_cg_(spmv_kuhn|spmv_kuhn_fused|update|dir)($|<)" -s 30 -c 3 \
     -o gpurun_out/${tag}_cg python tools/cg_bench.py --solves 1 --timing --no-warm > gpurun_out/${tag}_ncu_cg.log 2>&1
 python tools/cg_bench.py --solves 1 --timing --no-warm --row-order 3 --spmv 10 > gpurun_out/${tag}_sell_plain.log 2>&1 &&
   ncu --set full --clock-control none --import-source on -k regex:"k_cg_spmv" -s 20 -c 1 \

@@ -1,7 +1,8 @@
-"""The fused SpMV + direction update (OSM_FUSE_DIR, brick.cu BrickFuse) against the three-kernel PCG:
-histories, inner counts and the solution must be bitwise equal; also times both (uninstrumented).
+"""A PCG restructuring knob (default OSM_FUSE_DIR: the direction update fused into the brick SpMV,
+brick.cu BrickFuse; OSM_FOLD_ALPHA: alpha formed inside k_cg_update) set to 1 against 0: histories, inner
+counts and the solution must be bitwise equal; also times both (uninstrumented).
 
-    python tools/fuse_check.py [--config C3] [--solves 2]
+    python tools/fuse_check.py [--config C3] [--solves 2] [--knob OSM_FUSE_DIR]
 """
 import argparse
 import json
@@ -18,11 +19,12 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--solves", type=int, default=2)
+ap.add_argument("--knob", default="OSM_FUSE_DIR")
 a = ap.parse_args()
 cfg = dict(synth.CONFIGS[a.config])
 res = {}
 for fuse in (0, 1):
-    os.environ["OSM_FUSE_DIR"] = str(fuse)
+    os.environ[a.knob] = str(fuse)
     o = P.setup(cfg, synth.density(cfg))
     o.solve()
     ts = []
@@ -35,7 +37,7 @@ for fuse in (0, 1):
     o.close() if hasattr(o, "close") else None
     del o
 f0, f1 = res[0], res[1]
-out = dict(config=a.config, seconds_plain=f0["seconds"], seconds_fused=f1["seconds"], outer=(f0["outer"], f1["outer"]),
+out = dict(config=a.config, knob=a.knob, seconds_plain=f0["seconds"], seconds_fused=f1["seconds"], outer=(f0["outer"], f1["outer"]),
            inner=(f0["inner"], f1["inner"]),
            hist_bitwise=bool(np.array_equal(f0["hist"], f1["hist"])),
            its_equal=bool(np.array_equal(f0["its"], f1["its"])),

@@ -979,13 +979,14 @@ void brick_build(Ctx& c, const uint16_t* d_vidx, uint32_t zero_idx) {
     return;
   }
   // 5. TMA tensor maps of p: one per (local subdomain, class), dims (nJp, nIc, nKc), jj fastest; with the
-  // Kuhn kernel a second set over p2 (the fused direction update's other p buffer, zero-initialised:
+  // fused Kuhn kernel (Ctx::fuse_dir) a second set over p2 (the fused direction update's other p buffer, zero-initialised:
   // its padding rows are never written)
-  if (c.brick_kernel > 0 && !c.p2) {
+  const bool fuse = c.brick_kernel > 0 && c.fuse_dir;  // only the opt-in fused path needs p2
+  if (fuse && !c.p2) {
     OSM_CUDA(cudaMalloc(&c.p2, sizeof(double) * std::max<int64_t>(1, c.nrows_total)));
     OSM_CUDA(cudaMemset(c.p2, 0, sizeof(double) * c.nrows_total));
   }
-  const int nset = c.brick_kernel > 0 ? 2 : 1;
+  const int nset = fuse ? 2 : 1;
   std::vector<CUtensorMap> maps((size_t)nset * nloc * nc);
   auto enc = encode_fn();
   for (int set = 0; set < nset; ++set)
